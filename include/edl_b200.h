@@ -1,0 +1,201 @@
+/*
+ * edl_b200.h — C ABI of the B200-native elastic data-parallel SGD hot path.
+ *
+ * Drop-in boundary for the reference EDL implementation (/root/reference/proj, C++20).
+ * Every entry point names the reference interface it replaces (file:line, relative to
+ * /root/reference/proj).  Conventions:
+ *   - plain pointers and sizes only; no C++ or torch types cross this boundary;
+ *   - no exceptions cross it: each reference exception class maps to an EDL_E* code and
+ *     the message is kept in a thread-local string read by edl_last_error();
+ *   - "_dev" pointers are caller-owned device buffers on the current CUDA device; the
+ *     `stream` argument is a cudaStream_t passed as void* (NULL = legacy default stream);
+ *   - worker ids are NUL-terminated strings, as in the reference (std::string).
+ */
+#ifndef EDL_B200_H
+#define EDL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status codes
+ * Union of ReduceStatus (include/edl/allreduce.hpp:39), PipeStatus
+ * (include/edl/datapipeline.hpp:53), SendStatus (include/edl/transport.hpp:51) and the
+ * exception classes thrown by trainer.cpp / dataset.cpp / bytes.hpp.                  */
+enum {
+  EDL_OK = 0,
+  EDL_RETRY = 1,               /* a scaling operation is in flight          */
+  EDL_EINVAL = 2,              /* std::invalid_argument (trainer.cpp:16-17,57-58), Invalid */
+  EDL_PEER_GONE = 3,           /* ReduceStatus::PeerGone                                  */
+  EDL_TIMEOUT = 4,             /* ReduceStatus::Timeout                                   */
+  EDL_VERSION_MISMATCH = 5,    /* ReduceStatus::VersionMismatch                           */
+  EDL_UNKNOWN_WORKER = 6,      /* PipeStatus::UnknownWorker                               */
+  EDL_STALE_SHARD = 7,         /* PipeStatus::StaleShard                                  */
+  EDL_SHAPE_MISMATCH = 8,      /* PipeStatus::ShapeMismatch                               */
+  EDL_OUT_OF_RANGE = 9,        /* std::out_of_range (dataset.cpp:37)                      */
+  EDL_ECUDA = 10,              /* CUDA runtime / driver failure                           */
+  EDL_ENOMEM = 11,             /* allocation failure                                      */
+  EDL_ALLOWANCE_EXCEEDED = 12, /* scale_in leaver missed its allowance      */
+  EDL_EIO = 13,                /* std::runtime_error on file I/O (trainer.cpp:104)        */
+  EDL_ETRUNCATED = 14          /* std::runtime_error "truncated payload" (bytes.hpp:112)  */
+};
+
+const char* edl_last_error(void);
+const char* edl_version(void);
+
+/* ------------------------------------------------------------------ enums */
+enum { EDL_MODEL_LEAST_SQUARES = 0, EDL_MODEL_LOGISTIC = 1, EDL_MODEL_MLP = 2 }; /* trainer.hpp:18 */
+enum { EDL_REDUCE_SUM = 0, EDL_REDUCE_AVERAGE = 1 };                           /* allreduce.hpp:25 */
+enum { EDL_DTYPE_F64 = 0, EDL_DTYPE_BF16 = 1, EDL_DTYPE_F32 = 2 };
+enum { EDL_NEXT_SHARD = 0, EDL_NEXT_EPOCH_END = 1, EDL_NEXT_PENDING = 2 };    /* datapipeline.hpp:51 */
+
+/* ================================================================== partition leasing
+ * Replaces edl::ShardManager (include/edl/datapipeline.hpp:58-127, src/datapipeline.cpp).
+ * Bit-compatible: same std::mt19937_64 + std::shuffle permutation stream, same
+ * reclaimed-first hand-out order and the same snapshot byte layout.                     */
+typedef struct EdlLeaseManager EdlLeaseManager;
+
+typedef struct {
+  uint32_t index;   /* PartitionMeta::index  */
+  uint64_t offset;  /* PartitionMeta::offset (first global sample id) */
+  uint64_t length;  /* PartitionMeta::length */
+} EdlPartitionMeta;
+
+typedef struct {
+  int32_t kind;            /* EDL_NEXT_SHARD | EDL_NEXT_EPOCH_END | EDL_NEXT_PENDING */
+  EdlPartitionMeta meta;   /* valid for EDL_NEXT_SHARD                              */
+  uint64_t resume_offset;  /* Shard::resume_offset                                  */
+  uint64_t epoch;          /* EpochEnd::epoch                                       */
+} EdlNextShard;
+
+/* default_partition_count, datapipeline.cpp:9-11 */
+int32_t edl_default_partition_count(int32_t max_expected_workers);
+/* ShardManager::ShardManager, datapipeline.cpp:13-17 */
+int edl_lease_create(uint64_t dataset_size, int32_t partitions, uint64_t seed,
+                     const char* locator, EdlLeaseManager** out);
+void edl_lease_destroy(EdlLeaseManager* lm);
+/* register_worker / unregister_worker / is_registered, datapipeline.cpp:26-32 */
+int edl_lease_register(EdlLeaseManager* lm, const char* worker);
+int edl_lease_unregister(EdlLeaseManager* lm, const char* worker);
+int edl_lease_is_registered(const EdlLeaseManager* lm, const char* worker);
+/* next_shard, datapipeline.cpp:43-62; returns EDL_UNKNOWN_WORKER like PipeStatus */
+int edl_lease_next(EdlLeaseManager* lm, const char* worker, EdlNextShard* out);
+/* report_progress, datapipeline.cpp:64-71 */
+int edl_lease_report(EdlLeaseManager* lm, const char* worker, uint32_t partition,
+                     uint64_t next_sample_offset);
+/* reclaim / reclaim_at / reclaim_missing, datapipeline.cpp:73-104 */
+int edl_lease_reclaim(EdlLeaseManager* lm, const char* worker);
+int edl_lease_reclaim_at(EdlLeaseManager* lm, const char* worker, const uint32_t* partitions,
+                         const uint64_t* offsets, size_t n);
+int edl_lease_reclaim_missing(EdlLeaseManager* lm, const char* const* live, size_t n);
+/* partition_meta, datapipeline.cpp:34-41 */
+int edl_lease_partition_meta(const EdlLeaseManager* lm, uint32_t index, EdlPartitionMeta* out);
+/* worker_shards, datapipeline.cpp:106-113; returns count, fills up to cap entries */
+size_t edl_lease_worker_shards(const EdlLeaseManager* lm, const char* worker,
+                               uint32_t* partitions, uint64_t* offsets, size_t cap);
+/* snapshot / restore, datapipeline.cpp:115-178 (identical byte layout).
+ * snapshot: writes up to cap bytes, stores the full size in *len.                      */
+int edl_lease_snapshot(const EdlLeaseManager* lm, uint8_t* buf, size_t cap, size_t* len);
+int edl_lease_restore(EdlLeaseManager* lm, const uint8_t* buf, size_t len);
+/* accessors, datapipeline.hpp:86-95 */
+uint64_t edl_lease_epoch(const EdlLeaseManager* lm);
+uint64_t edl_lease_epochs_completed(const EdlLeaseManager* lm);
+uint64_t edl_lease_cursor(const EdlLeaseManager* lm);
+size_t edl_lease_permutation(const EdlLeaseManager* lm, uint32_t* out, size_t cap);
+size_t edl_lease_reclaimed_count(const EdlLeaseManager* lm);
+size_t edl_lease_in_flight_count(const EdlLeaseManager* lm);
+
+/* ================================================================== batch splits
+ * split_batch (absent in the reference): sizes floor/ceil(B/p), larger
+ * shares to the lowest ranks.  Returns EDL_EINVAL when B < p or p < 1.                   */
+int edl_split_batch(int64_t B, int32_t p, int64_t* out);
+/* k = max(1, ceil(T_a / T_b)) */
+int64_t edl_switch_delay(double t_a_ms, double t_b_ms);
+/* eta_at, trainer.hpp:27-29 */
+double edl_eta_at(double eta, double decay, uint64_t t);
+
+/* ================================================================== synthetic dataset
+ * Replaces edl::SyntheticDataset (dataset.hpp:25-50, dataset.cpp:11-58), materialised
+ * once in HBM.  Features are bit-identical to SyntheticDataset::get; with dtype F64 the
+ * labels are bit-identical too (sequential, FMA-free dot product as dataset.cpp:49).
+ * dtype BF16 (the MLP workload) stores features rounded f64 -> f32 -> bf16 (RNE) and
+ * int32 class labels  splitmix64(seed ^ ~(i*0xd1342543de82ef95+1)) % num_classes.        */
+typedef struct EdlDataset EdlDataset;
+typedef struct {
+  uint64_t size;
+  int32_t dim;
+  uint64_t seed;
+  double noise;
+  int32_t sign_labels;
+} EdlSyntheticSpec;
+
+int edl_dataset_create_synthetic(const EdlSyntheticSpec* spec, int32_t dtype,
+                                 int32_t num_classes, EdlDataset** out);
+void edl_dataset_destroy(EdlDataset* ds);
+uint64_t edl_dataset_size(const EdlDataset* ds);
+int32_t edl_dataset_dim(const EdlDataset* ds);
+/* device pointers: features [size][dim] (f64 or bf16), labels [size] (f64 or int32) */
+const void* edl_dataset_features(const EdlDataset* ds);
+const void* edl_dataset_labels(const EdlDataset* ds);
+/* SyntheticDataset::true_weights (host copy, dim doubles) */
+int edl_dataset_true_weights(const EdlDataset* ds, double* out);
+/* SyntheticDataset::get (dataset.cpp:36-54): D2H copy of one sample; EDL_OUT_OF_RANGE
+ * when index >= size.  features_out holds dim doubles (bf16 datasets are widened).      */
+int edl_dataset_get(const EdlDataset* ds, uint64_t index, double* features_out,
+                    double* label_out);
+
+/* A contiguous run of sample ids [first, first+count) — what one shard lease yields. */
+typedef struct {
+  uint64_t first;
+  uint64_t count;
+} EdlRun;
+
+/* Coalesced gather of leased runs into a contiguous batch: x_out [n][dim] in the
+ * dataset's dtype, y_out [n] labels.  runs_dev may be a device or mapped-host pointer.  */
+int edl_gather(const EdlDataset* ds, const EdlRun* runs_dev, int32_t n_runs, int64_t n_rows,
+               void* x_out_dev, void* y_out_dev, void* stream);
+
+/* ================================================================== linear trainer (f64)
+ * Device versions of trainer.cpp.  All reproduce the reference's operation order
+ * (sequential per-sample accumulation, no FMA contraction) and are bit-identical.       */
+/* local_gradient, trainer.cpp:30-39: grad_out_dev[0..dim) = grad_sum, grad_out_dev[dim]
+ * = count (the allreduce convention of trainer.cpp:244-254).                            */
+int edl_local_gradient(int32_t kind, const double* w_dev, const double* x_dev,
+                       const double* y_dev, int64_t n, int32_t dim, double* grad_out_dev,
+                       void* stream);
+/* batch_loss, trainer.cpp:41-54 */
+int edl_batch_loss(int32_t kind, const double* w_dev, const double* x_dev, const double* y_dev,
+                   int64_t n, int32_t dim, double* loss_out_dev, void* stream);
+/* sgd_step, trainer.cpp:56-61: w -= (eta / count) * g.  count is read from
+ * g_dev[dim] when count < 0 (device-side count), otherwise the given value.
+ * EDL_EINVAL when count == 0.                                                           */
+int edl_sgd_step(double* w_dev, const double* g_dev, int64_t count, double eta, int32_t dim,
+                 void* stream);
+
+/* ================================================================== collective
+ * ring_allreduce (allreduce.cpp:60-130) executed as one kernel over n device buffers
+ * (local workers, or peer buffers mapped over NVLink).  Chunk c = [c*len/n, (c+1)*len/n)
+ * folds ranks c, c+1, ..., c+n-1 left to right (ring_order_reduce, allreduce.cpp:132-148)
+ * so the f64 result is bit-identical to the reference collective.  `out_dev` receives
+ * the reduced vector; inputs are untouched.                                             */
+int edl_ring_allreduce_f64(const double* const* inputs_dev, int32_t n, size_t len,
+                           int32_t op, double* out_dev, void* stream);
+
+/* ================================================================== MLP step kernels  */
+/* tcgen05/TMA GEMM: C[M][N] = sum_k A(m,k) B(n,k), bf16 in, fp32 accumulate.
+ * a_mn = 0: A row-major [M][lda];  a_mn = 1: A row-major [K][lda] (A^T stored).
+ * b_mn = 0: B row-major [N][ldb];  b_mn = 1: B row-major [K][ldb].
+ * Epilogue: optional ReLU, optional mask (C = 0 where mask <= 0, mask [M][ldm] bf16),
+ * bf16 or fp32 output.  bn = N tile (0 = auto).                                         */
+int edl_gemm_bf16(const void* A, int32_t lda, int32_t a_mn, const void* B, int32_t ldb,
+                  int32_t b_mn, void* C, int32_t ldc, int32_t M, int32_t N, int32_t K,
+                  int32_t relu, int32_t out_f32, const void* mask, int32_t ldm, int32_t bn,
+                  void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EDL_B200_H */

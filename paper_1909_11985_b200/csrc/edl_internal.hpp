@@ -1,0 +1,29 @@
+// Internal declarations shared by the CUDA translation units and the C-ABI layer.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/edl_b200.h"
+
+namespace edl {
+
+// Thread-local last-error string surfaced through edl_last_error().
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define EDL_CUDA_TRY(expr)                                  \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) return ::edl::cuda_fail(_e, #expr); \
+  } while (0)
+
+// ---- GEMM (gemm_sm100.cu)
+int gemm_pick_bn(int M, int N, bool b_mn);
+int gemm_bf16(const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
+              int ldc, int M, int N, int K, int relu, int out_f32, const void* mask, int ldm,
+              int bn, cudaStream_t stream);
+
+}  // namespace edl
