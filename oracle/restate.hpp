@@ -52,6 +52,10 @@ struct Sample {
 // SyntheticDataset, src/dataset.cpp:27-54
 class Synth {
  public:
+  using SampleT = Sample;
+  static Sample make_sample(uint64_t id, std::vector<double> f, double label) {
+    return Sample{id, std::move(f), label};
+  }
   explicit Synth(SynthSpec s) : spec_(s) {
     w_true_.resize(static_cast<size_t>(s.dim));
     uint64_t st = splitmix64(s.seed ^ 0x77ee55aa11cc33ddULL);  // :29
