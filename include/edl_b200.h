@@ -195,6 +195,79 @@ int edl_gemm_bf16(const void* A, int32_t lda, int32_t a_mn, const void* B, int32
                   int32_t relu, int32_t out_f32, const void* mask, int32_t ldm, int32_t bn,
                   void* stream);
 
+/* ================================================================== elastic job runtime
+ * The reference runtime is absent (CMake lists src/runtime.cpp, which does not exist);
+ * its API is specified in SPEC.md:272-392 / PAPER.md Table 1.  A job owns the partition
+ * leases (leader role), the versioned ring (Topology, include/edl/topology.hpp:13-51),
+ * the per-worker batch splits, the assignment log (trainer.hpp:59-90) and one model
+ * replica per GPU.  Mini-batch protocol: see DESIGN.md §3 (identical to
+ * oracle/job_driver.hpp).                                                              */
+typedef struct EdlJob EdlJob;
+
+typedef struct {
+  int32_t model;             /* EDL_MODEL_LEAST_SQUARES | EDL_MODEL_LOGISTIC | EDL_MODEL_MLP */
+  EdlSyntheticSpec data;     /* synthetic dataset (dataset.hpp:32-38)                      */
+  int32_t num_classes;       /* MLP: classes of the softmax layer                          */
+  int32_t layers;            /* MLP: number of Linear layers (ReLU between them)           */
+  int32_t hidden;            /* MLP: width of hidden layers                                */
+  double eta;                /* HyperParams::eta   (trainer.hpp:20)                        */
+  double decay;              /* HyperParams::decay                                         */
+  double momentum;           /* 0 = plain sgd_step (reference)                             */
+  int64_t batch;             /* aggregate batch B, constant across scaling   */
+  int64_t per_worker_batch;  /* > 0: fixed per-worker batch (static throughput sweeps)     */
+  uint64_t lease_seed;       /* ShardManager seed                                          */
+  int32_t partitions;        /* 0 = default_partition_count(max_workers)                   */
+  int32_t max_workers;       /* expected maximum parallelism                               */
+  uint64_t init_seed;        /* MLP weight init seed                                       */
+  double t_a_ms;             /* switch allowance T_a, default 500             */
+  int32_t keep_log;          /* record the assignment log                                  */
+} EdlJobConfig;
+
+typedef struct {
+  uint64_t t;         /* mini-batch index described                                         */
+  uint64_t version;   /* topology version in effect for this mini-batch                     */
+  int32_t ring_size;  /* workers in the ring                                                */
+  int32_t switched;   /* 1 when a topology switch was installed right before this batch     */
+  uint64_t count;     /* samples in the global mini-batch                                   */
+  double loss;        /* mean loss over the global mini-batch, before the update (NaN if
+                         not yet known)                                                     */
+  double step_ms;     /* device time of the mini-batch (CUDA events)                        */
+  double stall_ms;    /* device idle time between the previous mini-batch and this one     */
+} EdlStepReport;
+
+void edl_job_config_default(EdlJobConfig* cfg);
+/* ring: worker ids in rank order; devices: CUDA device hosting each worker */
+int edl_job_create(const EdlJobConfig* cfg, const char* const* ring, const int32_t* devices,
+                   int32_t n, EdlJob** out);
+void edl_job_destroy(EdlJob* job);
+/* One mini-batch on every ring member with notify_batch_end folded in:
+ * due topology switches are installed first.  Asynchronous: fills t/version/ring/count
+ * and returns once the device work is enqueued.                                        */
+int edl_job_step(EdlJob* job, EdlStepReport* rep);
+/* Waits for the last launched mini-batch and fills its full report.                   */
+int edl_job_sync(EdlJob* job, EdlStepReport* rep);
+/* scale_out: newcomers are prepared on a side thread while the job keeps
+ * stepping; they join at switch_t = t + max(1, ceil(T_a / T_b)).  EDL_RETRY while another
+ * scaling operation is pending.                                           */
+int edl_job_scale_out(EdlJob* job, const char* const* ids, const int32_t* devices, int32_t n,
+                      int64_t* switch_t);
+/* scale_in: leavers train until switch_t, then their leases are
+ * reclaimed (datapipeline.cpp:73-84) and they leave; no restart.                        */
+int edl_job_scale_in(EdlJob* job, const char* const* ids, int32_t n, double allowance_ms,
+                     int64_t* switch_t);
+/* Scripted topology event at an explicit switch step (test and benchmark protocols).    */
+int edl_job_schedule(EdlJob* job, int64_t switch_t, int32_t out, const char* const* ids,
+                     const int32_t* devices, int32_t n);
+/* Parameters of a worker's replica: linear f64[dim]; MLP fp32 master [param_count].    */
+int edl_job_params(EdlJob* job, const char* worker, void* host_out, size_t bytes);
+size_t edl_job_param_count(const EdlJob* job);
+uint64_t edl_job_t(const EdlJob* job);
+double edl_job_median_step_ms(const EdlJob* job);
+/* Assignment log in the reference text format (trainer.cpp:79-100).                    */
+int edl_job_log(const EdlJob* job, char* buf, size_t cap, size_t* len);
+int edl_job_ring(const EdlJob* job, char* buf, size_t cap, size_t* len);
+int edl_job_lease_snapshot(const EdlJob* job, uint8_t* buf, size_t cap, size_t* len);
+
 #ifdef __cplusplus
 }
 #endif

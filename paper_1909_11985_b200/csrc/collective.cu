@@ -1,0 +1,147 @@
+// Gradient allreduce fused with the SGD update, over NVLink peer memory.
+//
+// Replaces ring_allreduce (src/allreduce.cpp:60-130) followed by sgd_step
+// (src/trainer.cpp:56-61, applied as in trainer.cpp:244-271) for the MLP workload.
+// One kernel per replica (= per GPU), all replicas launched with the same grid:
+//
+//   phase 0  barrier: CTA b of every replica signals CTA b of every peer (st.release.sys)
+//            and waits for the peers' signals -> every peer's wgrad GEMMs have finished
+//   phase 1  reduce-scatter + sharded update: replica r owns params [lo_r, hi_r); it reads
+//            the bf16 gradients of ALL ring members for its shard (local HBM or peer HBM
+//            over NVLink), sums them in ring order, applies SGD/momentum to its fp32
+//            master shard and writes the bf16 weights of the shard into EVERY replica
+//            (all-gather by peer stores)
+//   phase 2  barrier again -> every shard of every replica's weights has been written
+//
+// Per replica and step that moves 2P/N + 2P(N-1)/N bytes over NVLink each way (the
+// reduce-scatter + all-gather lower bound of a bf16 allreduce) and touches HBM for
+// 4P + 8P/N bytes instead of the 12P of "allreduce then full update".  With one
+// replica both barriers vanish and the kernel is the plain fused update.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "collective.hpp"
+#include "edl_internal.hpp"
+
+namespace edl {
+namespace {
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// flags[phase][block][source]
+__device__ __forceinline__ uint32_t* flag_slot(uint32_t* base, int phase, int block, int src) {
+  return base + (static_cast<size_t>(phase) * kCollMaxBlocks + block) * kCollMaxReplicas + src;
+}
+
+__device__ void cross_replica_barrier(const CollArgs& a, int phase) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int r = 0; r < a.n_rep; ++r)
+      if (r != a.me) st_release_sys(flag_slot(a.flags[r], phase, blockIdx.x, a.me), a.epoch);
+    for (int r = 0; r < a.n_rep; ++r) {
+      if (r == a.me) continue;
+      const uint32_t* f = flag_slot(a.flags[a.me], phase, blockIdx.x, r);
+      while (static_cast<int32_t>(ld_acquire_sys(f) - a.epoch) < 0) __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 t = __bfloat1622float2(h[k]);
+    f[2 * k] = t.x;
+    f[2 * k + 1] = t.y;
+  }
+}
+
+// 8 parameters per thread-iteration.
+template <bool kMomentum>
+__global__ void __launch_bounds__(256) allreduce_sgd_kernel(CollArgs a) {
+  if (a.n_rep > 1) cross_replica_barrier(a, 0);
+  const size_t lo = a.lo8, hi = a.hi8;
+  for (size_t i = lo + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < hi;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float gs[8];
+    bf16x8_to_f32(__ldcs(reinterpret_cast<const uint4*>(a.grads[0]) + i), gs);
+    for (int k = 1; k < a.n_src; ++k) {
+      float t[8];
+      bf16x8_to_f32(__ldcs(reinterpret_cast<const uint4*>(a.grads[k]) + i), t);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) gs[e] = __fadd_rn(gs[e], t[e]);
+    }
+    float4* mp = reinterpret_cast<float4*>(a.master) + 2 * i;
+    const float4 m0 = __ldcs(mp), m1 = __ldcs(mp + 1);
+    float m[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+    if (kMomentum) {
+      float4* vp = reinterpret_cast<float4*>(a.mom) + 2 * i;
+      const float4 v0 = __ldcs(vp), v1 = __ldcs(vp + 1);
+      float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        v[e] = __fadd_rn(__fmul_rn(a.mu, v[e]), __fmul_rn(gs[e], a.inv_count));
+        m[e] = __fsub_rn(m[e], __fmul_rn(a.eta, v[e]));
+      }
+      __stcs(vp, make_float4(v[0], v[1], v[2], v[3]));
+      __stcs(vp + 1, make_float4(v[4], v[5], v[6], v[7]));
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) m[e] = __fsub_rn(m[e], __fmul_rn(a.scale, gs[e]));
+    }
+    __stcs(mp, make_float4(m[0], m[1], m[2], m[3]));
+    __stcs(mp + 1, make_float4(m[4], m[5], m[6], m[7]));
+    uint4 o;
+    __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) oh[k] = __floats2bfloat162_rn(m[2 * k], m[2 * k + 1]);
+    for (int d = 0; d < a.n_dst; ++d) reinterpret_cast<uint4*>(a.w_dst[d])[i] = o;
+  }
+  if (a.n_rep > 1) cross_replica_barrier(a, 1);
+}
+
+__global__ void barrier_kernel(CollArgs a) { cross_replica_barrier(a, 0); }
+
+}  // namespace
+
+int coll_blocks() { return 148 * 4; }
+
+int allreduce_sgd(const CollArgs& a, cudaStream_t s) {
+  if (a.n_src < 1 || a.n_src > kCollMaxSources) return fail(EDL_EINVAL, "allreduce_sgd: sources");
+  if (a.n_dst < 0 || a.n_dst > kCollMaxReplicas || a.n_rep > kCollMaxReplicas)
+    return fail(EDL_EINVAL, "allreduce_sgd: replicas");
+  const int blocks = coll_blocks();
+  if (a.mu != 0.0f)
+    allreduce_sgd_kernel<true><<<blocks, 256, 0, s>>>(a);
+  else
+    allreduce_sgd_kernel<false><<<blocks, 256, 0, s>>>(a);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
+
+int replica_barrier(const CollArgs& a, cudaStream_t s) {
+  if (a.n_rep <= 1) return EDL_OK;
+  barrier_kernel<<<1, 32, 0, s>>>(a);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
+
+// Shard boundaries in units of 8 parameters: replica r owns [r*n8/N, (r+1)*n8/N), the
+// same rounding as chunk_range (allreduce.cpp:33-37).
+void shard_range(size_t n8, int n_rep, int r, size_t* lo, size_t* hi) {
+  *lo = n8 * static_cast<size_t>(r) / static_cast<size_t>(n_rep);
+  *hi = n8 * static_cast<size_t>(r + 1) / static_cast<size_t>(n_rep);
+}
+
+}  // namespace edl

@@ -1,0 +1,36 @@
+// Fused allreduce + SGD update over NVLink peer memory (collective.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace edl {
+
+constexpr int kCollMaxReplicas = 8;   // GPUs in one NVLink domain
+constexpr int kCollMaxSources = 16;   // ring members contributing gradients
+constexpr int kCollMaxBlocks = 1024;  // >= coll_blocks()
+// Flag buffer per replica: [2 phases][kCollMaxBlocks][kCollMaxReplicas] uint32.
+constexpr size_t kCollFlagBytes = 2ull * kCollMaxBlocks * kCollMaxReplicas * sizeof(uint32_t);
+
+struct CollArgs {
+  const __nv_bfloat16* grads[kCollMaxSources];  // ring order; local or peer pointers
+  int n_src = 0;
+  __nv_bfloat16* w_dst[kCollMaxReplicas];  // bf16 working weights of every replica
+  int n_dst = 0;
+  uint32_t* flags[kCollMaxReplicas];  // flag buffers of every replica (peer-mapped)
+  int me = 0, n_rep = 1;
+  uint32_t epoch = 0;  // strictly increasing per launch
+  size_t lo8 = 0, hi8 = 0;  // owned shard, in units of 8 params
+  float* master = nullptr;  // this replica's fp32 master (full size; shard updated)
+  float* mom = nullptr;
+  float scale = 0.f, inv_count = 0.f, eta = 0.f, mu = 0.f;
+};
+
+int coll_blocks();
+int allreduce_sgd(const CollArgs& a, cudaStream_t s);
+int replica_barrier(const CollArgs& a, cudaStream_t s);
+void shard_range(size_t n8, int n_rep, int r, size_t* lo, size_t* hi);
+
+}  // namespace edl

@@ -1,5 +1,7 @@
 // Internal declarations shared by the CUDA translation units and the C-ABI layer.
 #pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -21,6 +23,24 @@ int cuda_fail(cudaError_t e, const char* what);
   } while (0)
 
 // ---- GEMM (gemm_sm100.cu)
+struct EpiParams {
+  void* C;                     // bf16 or fp32 output [M][ldc]
+  const __nv_bfloat16* mask;   // optional: zero outputs where mask <= 0 ([M][ldm])
+  int ldc;
+  int ldm;
+  int relu;     // apply max(0, x)
+  int out_f32;  // store fp32 instead of bf16
+};
+// Pre-encoded launch (TMA descriptors built once; launching costs one kernel launch).
+struct GemmPlan {
+  CUtensorMap ta, tb;
+  int M = 0, N = 0, K = 0, a_mn = 0, b_mn = 0, bn = 0;
+  EpiParams ep{};
+};
+int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B, int ldb,
+                   int b_mn, void* C, int ldc, int M, int N, int K, int relu, int out_f32,
+                   const void* mask, int ldm, int bn);
+int gemm_plan_run(const GemmPlan& p, cudaStream_t stream);
 int gemm_pick_bn(int M, int N, bool b_mn);
 int gemm_bf16(const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
               int ldc, int M, int N, int K, int relu, int out_f32, const void* mask, int ldm,

@@ -37,15 +37,6 @@ constexpr int BK = 64;  // one 128-byte swizzle row of bf16
 constexpr int kThreads = 192;
 constexpr uint32_t kMnBlockBytes = 64 * BK * 2;  // one 64(MN) x 64(K) TMA box = 8 KB
 
-struct EpiParams {
-  void* C;                  // bf16 or fp32 output [M][ldc]
-  const __nv_bfloat16* mask;  // optional: zero outputs where mask <= 0 ([M][ldm])
-  int ldc;
-  int ldm;
-  int relu;      // apply max(0, x)
-  int out_f32;   // store fp32 instead of bf16
-};
-
 template <int BN>
 struct Cfg {
   static constexpr uint32_t kABytes = BM * BK * 2;  // 16 KB
@@ -326,7 +317,8 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   kern<<<grid, kThreads, Cf::kSmemBytes, stream>>>(ta, tb, M, N, K, ep);
-  return cudaGetLastError() == cudaSuccess ? EDL_OK : EDL_ECUDA;
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
 }
 
 }  // namespace
@@ -353,33 +345,35 @@ int gemm_pick_bn(int M, int N, bool b_mn) {
   return best;
 }
 
-int gemm_bf16(const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* Cout,
-              int ldc, int M, int N, int K, int relu, int out_f32, const void* mask, int ldm,
-              int bn, cudaStream_t stream) {
-  if (M <= 0 || N <= 0 || K <= 0) return EDL_EINVAL;
-  if ((lda * 2) % 16 || (ldb * 2) % 16) return EDL_EINVAL;
+int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B, int ldb,
+                   int b_mn, void* Cout, int ldc, int M, int N, int K, int relu, int out_f32,
+                   const void* mask, int ldm, int bn) {
+  if (M <= 0 || N <= 0 || K <= 0) return fail(EDL_EINVAL, "gemm: empty shape");
+  if ((lda * 2) % 16 || (ldb * 2) % 16) return fail(EDL_EINVAL, "gemm: 16-byte row alignment");
   if (bn <= 0) bn = gemm_pick_bn(M, N, b_mn != 0);
-  CUtensorMap ta, tb;
-  int rc;
-  if (a_mn)
-    rc = make_tmap(&ta, A, K, M, lda, 64);
-  else
-    rc = make_tmap(&ta, A, M, K, lda, BM);
-  if (rc) return rc;
-  if (b_mn)
-    rc = make_tmap(&tb, B, K, N, ldb, 64);
-  else
-    rc = make_tmap(&tb, B, N, K, ldb, bn);
-  if (rc) return rc;
-  EpiParams ep{Cout, static_cast<const __nv_bfloat16*>(mask), ldc, ldm, relu, out_f32};
+  int rc = a_mn ? make_tmap(&p->ta, A, K, M, lda, 64) : make_tmap(&p->ta, A, M, K, lda, BM);
+  if (rc) return fail(rc, "gemm: tensor map A");
+  rc = b_mn ? make_tmap(&p->tb, B, K, N, ldb, 64) : make_tmap(&p->tb, B, N, K, ldb, bn);
+  if (rc) return fail(rc, "gemm: tensor map B");
+  p->M = M;
+  p->N = N;
+  p->K = K;
+  p->a_mn = a_mn;
+  p->b_mn = b_mn;
+  p->bn = bn;
+  p->ep = EpiParams{Cout, static_cast<const __nv_bfloat16*>(mask), ldc, ldm, relu, out_f32};
+  return EDL_OK;
+}
 
-#define EDL_GEMM_CASE(BNV)                                                    \
-  case BNV:                                                                   \
-    if (!a_mn && !b_mn) return launch_gemm<BNV, false, false>(ta, tb, M, N, K, ep, stream); \
-    if (!a_mn && b_mn) return launch_gemm<BNV, false, true>(ta, tb, M, N, K, ep, stream);   \
-    if (a_mn && !b_mn) return launch_gemm<BNV, true, false>(ta, tb, M, N, K, ep, stream);   \
-    return launch_gemm<BNV, true, true>(ta, tb, M, N, K, ep, stream);
-  switch (bn) {
+int gemm_plan_run(const GemmPlan& p, cudaStream_t stream) {
+  const int a_mn = p.a_mn, b_mn = p.b_mn;
+#define EDL_GEMM_CASE(BNV)                                                                  \
+  case BNV:                                                                                 \
+    if (!a_mn && !b_mn) return launch_gemm<BNV, false, false>(p.ta, p.tb, p.M, p.N, p.K, p.ep, stream); \
+    if (!a_mn && b_mn) return launch_gemm<BNV, false, true>(p.ta, p.tb, p.M, p.N, p.K, p.ep, stream);   \
+    if (a_mn && !b_mn) return launch_gemm<BNV, true, false>(p.ta, p.tb, p.M, p.N, p.K, p.ep, stream);   \
+    return launch_gemm<BNV, true, true>(p.ta, p.tb, p.M, p.N, p.K, p.ep, stream);
+  switch (p.bn) {
     EDL_GEMM_CASE(64)
     EDL_GEMM_CASE(96)
     EDL_GEMM_CASE(112)
@@ -389,9 +383,19 @@ int gemm_bf16(const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn
     EDL_GEMM_CASE(224)
     EDL_GEMM_CASE(256)
     default:
-      return EDL_EINVAL;
+      return fail(EDL_EINVAL, "gemm: unsupported N tile");
   }
 #undef EDL_GEMM_CASE
+}
+
+int gemm_bf16(const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* Cout,
+              int ldc, int M, int N, int K, int relu, int out_f32, const void* mask, int ldm,
+              int bn, cudaStream_t stream) {
+  GemmPlan p;
+  int rc = gemm_plan_init(&p, A, lda, a_mn, B, ldb, b_mn, Cout, ldc, M, N, K, relu, out_f32, mask,
+                          ldm, bn);
+  if (rc) return rc;
+  return gemm_plan_run(p, stream);
 }
 
 }  // namespace edl

@@ -1,0 +1,160 @@
+// MLP step kernels around the tcgen05 GEMMs (gemm_sm100.cu):
+//   * deterministic weight init (fp32 master + bf16 working copy);
+//   * softmax cross-entropy: warp-shuffle row reductions producing per-row loss and
+//     dlogits = softmax - onehot (sum semantics: the 1/count of sgd_step is applied in the
+//     update, as trainer.cpp:56-61 / 244-271 do for the linear model);
+//   * the fused gradient-average + SGD/momentum update: one pass over HBM that reads the
+//     bf16 gradient(s), updates the fp32 master and writes the bf16 working weights.
+// The update restates sgd_step (trainer.cpp:56-61) in fp32 with explicit round-to-nearest
+// multiply/subtract so the CPU oracle (oracle/mlp.py) can reproduce it exactly.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "collective.hpp"
+#include "edl_internal.hpp"
+#include "kernels.hpp"
+
+namespace edl {
+namespace {
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+__global__ void init_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ w, size_t n,
+                            uint64_t seed, uint64_t offset, double bound) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const uint64_t idx = offset + i;
+    const uint64_t h = splitmix64(seed ^ (idx * 0x9e3779b97f4a7c15ULL + 0x632be59bd9b4e019ULL));
+    const double u = static_cast<double>(h >> 11) * 0x1.0p-53;
+    const float v = __double2float_rn(__dmul_rn(__dsub_rn(__dmul_rn(2.0, u), 1.0), bound));
+    master[i] = v;
+    w[i] = __float2bfloat16_rn(v);
+  }
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One CTA (256 threads) per row; classes <= 256 * kPer values held in registers.
+constexpr int kXentThreads = 256;
+constexpr int kPer = 16;
+__global__ void __launch_bounds__(kXentThreads)
+    xent_kernel(const float* __restrict__ logits, const int32_t* __restrict__ labels, int classes,
+                __nv_bfloat16* __restrict__ dlogits, float* __restrict__ row_loss) {
+  __shared__ float red[kXentThreads / 32];
+  const int row = blockIdx.x;
+  const float* x = logits + static_cast<size_t>(row) * classes;
+  float v[kPer];
+  float m = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int c = j * kXentThreads + threadIdx.x;
+    v[j] = c < classes ? x[c] : -INFINITY;
+    m = fmaxf(m, v[j]);
+  }
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  m = warp_max(m);
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  m = red[0];
+#pragma unroll
+  for (int w = 1; w < kXentThreads / 32; ++w) m = fmaxf(m, red[w]);
+  __syncthreads();
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    v[j] = (j * kXentThreads + static_cast<int>(threadIdx.x) < classes) ? __expf(v[j] - m) : 0.f;
+    s += v[j];
+  }
+  s = warp_sum(s);
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  s = 0.f;
+#pragma unroll
+  for (int w = 0; w < kXentThreads / 32; ++w) s += red[w];
+  const float inv = 1.0f / s;
+  const int label = labels[row];
+  __nv_bfloat16* d = dlogits + static_cast<size_t>(row) * classes;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int c = j * kXentThreads + threadIdx.x;
+    if (c < classes) d[c] = __float2bfloat16_rn(v[j] * inv - (c == label ? 1.0f : 0.0f));
+  }
+  if (threadIdx.x == 0) row_loss[row] = logf(s) + m - x[label];
+}
+
+__global__ void sum_rows_kernel(const float* __restrict__ v, int rows, double* __restrict__ out) {
+  __shared__ double part[256];
+  double acc = 0.0;
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) acc += static_cast<double>(v[r]);
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < static_cast<int>(blockDim.x); ++k) t += part[k];
+    *out += t;
+  }
+}
+
+}  // namespace
+
+int mlp_init_weights(float* master, __nv_bfloat16* w, size_t n, uint64_t seed, uint64_t offset,
+                     double bound, cudaStream_t s) {
+  init_kernel<<<148 * 8, 256, 0, s>>>(master, w, n, seed, offset, bound);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
+
+int softmax_xent(const float* logits, const int32_t* labels, int rows, int classes,
+                 __nv_bfloat16* dlogits, float* row_loss, cudaStream_t s) {
+  if (classes > kXentThreads * kPer) return fail(EDL_EINVAL, "softmax_xent: classes > 4096");
+  if (rows <= 0) return EDL_OK;
+  xent_kernel<<<rows, kXentThreads, 0, s>>>(logits, labels, classes, dlogits, row_loss);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
+
+int sum_rows(const float* row_loss, int rows, double* loss_out, cudaStream_t s) {
+  sum_rows_kernel<<<1, 256, 0, s>>>(row_loss, rows, loss_out);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
+
+int sgd_update_bf16(const __nv_bfloat16* const* grads, int n_src, float* master, float* mom,
+                    __nv_bfloat16* const* w_out, int n_dst, size_t n, float scale,
+                    float inv_count, float eta, float mu, cudaStream_t s) {
+  if (n % 8) return fail(EDL_EINVAL, "sgd_update: n must be a multiple of 8");
+  if (n_src < 1 || n_src > kCollMaxSources || n_dst < 0 || n_dst > kCollMaxReplicas)
+    return fail(EDL_EINVAL, "sgd_update: fan-in/out");
+  CollArgs a;
+  for (int k = 0; k < n_src; ++k) a.grads[k] = grads[k];
+  for (int k = 0; k < n_dst; ++k) a.w_dst[k] = w_out[k];
+  a.n_src = n_src;
+  a.n_dst = n_dst;
+  a.lo8 = 0;
+  a.hi8 = n / 8;
+  a.master = master;
+  a.mom = mom;
+  a.scale = scale;
+  a.inv_count = inv_count;
+  a.eta = eta;
+  a.mu = mu;
+  return allreduce_sgd(a, s);
+}
+
+}  // namespace edl

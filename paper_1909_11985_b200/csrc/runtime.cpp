@@ -1,0 +1,692 @@
+// Elastic data-parallel job runtime.
+//
+// The reference's runtime layer is absent: JobState, scale_out/scale_in,
+// notify_batch_end and split_batch exist only in SPEC.md:272-392.  This is the B200-native
+// realisation.  Host C++ owns the control plane (leases, ring, splits, log, switch
+// scheduling); per mini-batch the device work is
+//   H2D lease runs -> gather -> model fwd/bwd (tcgen05 GEMMs or f64 linear kernels)
+//   -> fused allreduce + SGD update -> D2H loss
+// all enqueued asynchronously on the replica's stream.
+//
+// Mini-batch protocol (shared verbatim with the CPU oracle, oracle/job_driver.hpp):
+//   1. install topology events with switch_t == t (notify_batch_end of step t-1):
+//      scale-out appends newcomers in ascending id order and enrolls them; scale-in
+//      reclaims each leaver's shards in ring order and retires it; version += 1;
+//      logged as `topo <t-1> <version> <ring...>`;
+//   2. workers draw split[rank] samples in ring order from their shard lease (next_shard
+//      when exhausted; EpochEnd -> ask again; ShardPending -> fewer samples this step);
+//      progress is reported after each worker's draw;
+//   3. per-worker [grad_sum, count] vectors are summed in ring order and applied with
+//      sgd_step(eta_at(t)) — reference-exact f64 for the linear models, bf16 gradients +
+//      fp32 master for the MLP.
+#include "runtime.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+
+namespace edl {
+
+namespace {
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    cudaSetDevice(dev);
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+template <class T>
+int dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) return EDL_OK;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * count);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  return EDL_OK;
+}
+
+#define EDL_TRY(expr)          \
+  do {                         \
+    int _rc = (expr);          \
+    if (_rc != EDL_OK) return _rc; \
+  } while (0)
+
+std::vector<int64_t> split_batch_vec(int64_t B, int p) {
+  std::vector<int64_t> out(static_cast<size_t>(p), B / p);
+  for (int64_t r = 0; r < B % p; ++r) out[static_cast<size_t>(r)] += 1;
+  return out;
+}
+
+}  // namespace
+
+int Job::create(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
+                const std::vector<int>& devices, Job** out) {
+  auto* j = new Job;
+  int rc = j->init(cfg, ring, devices);
+  if (rc != EDL_OK) {
+    delete j;
+    return rc;
+  }
+  *out = j;
+  return EDL_OK;
+}
+
+int Job::init(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
+              const std::vector<int>& devices) {
+  cfg_ = cfg;
+  if (ring.empty() || ring.size() != devices.size()) return fail(EDL_EINVAL, "job: empty ring");
+  if (cfg.model != EDL_MODEL_LEAST_SQUARES && cfg.model != EDL_MODEL_LOGISTIC &&
+      cfg.model != EDL_MODEL_MLP)
+    return fail(EDL_EINVAL, "job: unknown model");
+  if (cfg.per_worker_batch <= 0 && cfg.batch < static_cast<int64_t>(ring.size()))
+    return fail(EDL_EINVAL, "split_batch: B < p");
+  mlp_ = cfg.model == EDL_MODEL_MLP;
+  if (mlp_) {
+    L_ = cfg.layers;
+    if (L_ < 1 || cfg.hidden <= 0 || cfg.num_classes <= 0) return fail(EDL_EINVAL, "job: MLP shape");
+    if (cfg.data.dim % 8 || cfg.hidden % 8 || cfg.num_classes % 8)
+      return fail(EDL_EINVAL, "job: MLP widths must be multiples of 8 (16-byte TMA rows)");
+    if (cfg.num_classes > 4096) return fail(EDL_EINVAL, "job: num_classes > 4096");
+    for (int l = 0; l < L_; ++l) {
+      in_.push_back(l == 0 ? cfg.data.dim : cfg.hidden);
+      out_.push_back(l == L_ - 1 ? cfg.num_classes : cfg.hidden);
+      off_.push_back(P_);
+      P_ += static_cast<size_t>(in_.back()) * out_.back();
+    }
+  } else {
+    P_ = static_cast<size_t>(cfg.data.dim);
+  }
+  const int parts = cfg.partitions > 0 ? cfg.partitions
+                                       : default_partitions(std::max<int>(cfg.max_workers,
+                                                                          static_cast<int>(ring.size())));
+  std::ostringstream loc;
+  loc << "synthetic:" << cfg.data.seed << ":" << cfg.data.size;  // dataset.cpp:56-58
+  lm_ = std::make_unique<LeaseManager>(cfg.data.size, parts, cfg.lease_seed, loc.str());
+  for (size_t i = 0; i < ring.size(); ++i) {
+    int rc = EDL_OK;
+    Replica* r = replica_for(devices[i], &rc);
+    if (!r) return rc;
+    auto w = std::make_unique<Worker>();
+    EDL_TRY(build_worker(w.get(), r));
+    w->id = ring[i];
+    if (workers_.count(ring[i])) return fail(EDL_EINVAL, "job: duplicate worker id");
+    lm_->enroll(ring[i]);
+    workers_[ring[i]] = std::move(w);
+  }
+  ring_ = ring;
+  version_ = 1;
+  resplit();
+  if (cfg_.keep_log) {
+    LogRec r;
+    r.kind = LogRec::Topo;
+    r.t = 0;
+    r.version = version_;
+    r.ring = ring_;
+    log_.push_back(r);
+  }
+  return EDL_OK;
+}
+
+Replica* Job::replica_for(int device, int* rc) {
+  auto it = reps_.find(device);
+  if (it != reps_.end()) return it->second.get();
+  if (!reps_.empty()) {
+    *rc = fail(EDL_EINVAL, "job: one GPU per process in this build (multi-GPU runs use one "
+                           "process per GPU)");
+    return nullptr;
+  }
+  auto r = std::make_unique<Replica>();
+  r->device = device;
+  *rc = build_replica(r.get());
+  if (*rc != EDL_OK) return nullptr;
+  Replica* raw = r.get();
+  reps_[device] = std::move(r);
+  return raw;
+}
+
+int Job::build_replica(Replica* r) {
+  DeviceGuard g(r->device);
+  EDL_CUDA_TRY(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
+  for (int s = 0; s < kSlots; ++s) {
+    EDL_CUDA_TRY(cudaEventCreate(&r->ev_begin[s]));
+    EDL_CUDA_TRY(cudaEventCreate(&r->ev_end[s]));
+  }
+  EDL_CUDA_TRY(cudaMallocHost(&r->host_loss, sizeof(double) * kSlots));
+  EDL_TRY(dataset_create(cfg_.data, mlp_ ? EDL_DTYPE_BF16 : EDL_DTYPE_F64,
+                         mlp_ ? cfg_.num_classes : 0, &r->ds));
+  const int64_t rows = cfg_.per_worker_batch > 0 ? cfg_.per_worker_batch : cfg_.batch;
+  r->rows_cap = rows;
+  EDL_TRY(dalloc(&r->flags, kCollFlagBytes / 4));
+  EDL_CUDA_TRY(cudaMemset(r->flags, 0, kCollFlagBytes));
+  if (mlp_) {
+    EDL_TRY(dalloc(&r->master, P_));
+    EDL_TRY(dalloc(&r->W, P_));
+    if (cfg_.momentum != 0.0) {
+      EDL_TRY(dalloc(&r->mom, P_));
+      EDL_CUDA_TRY(cudaMemset(r->mom, 0, sizeof(float) * P_));
+    }
+    for (int l = 0; l < L_; ++l) {
+      const double bound = std::sqrt(6.0 / static_cast<double>(in_[l]));  // Kaiming-uniform
+      EDL_TRY(mlp_init_weights(r->master + off_[l], r->W + off_[l],
+                               static_cast<size_t>(in_[l]) * out_[l], cfg_.init_seed, off_[l],
+                               bound, r->stream));
+    }
+    r->act.resize(static_cast<size_t>(L_));
+    for (int l = 0; l < L_; ++l) EDL_TRY(dalloc(&r->act[l], static_cast<size_t>(rows) * in_[l]));
+    EDL_TRY(dalloc(&r->logits, static_cast<size_t>(rows) * cfg_.num_classes));
+    EDL_TRY(dalloc(&r->dlog, static_cast<size_t>(rows) * cfg_.num_classes));
+    int widest = cfg_.data.dim > cfg_.hidden ? cfg_.data.dim : cfg_.hidden;
+    EDL_TRY(dalloc(&r->dx[0], static_cast<size_t>(rows) * widest));
+    EDL_TRY(dalloc(&r->dx[1], static_cast<size_t>(rows) * widest));
+    EDL_TRY(dalloc(&r->row_loss, static_cast<size_t>(rows)));
+    EDL_TRY(dalloc(&r->labels, static_cast<size_t>(rows)));
+  } else {
+    const int dim = cfg_.data.dim;
+    EDL_TRY(dalloc(&r->w, static_cast<size_t>(dim)));
+    EDL_CUDA_TRY(cudaMemset(r->w, 0, sizeof(double) * dim));  // w0 = 0
+    EDL_TRY(dalloc(&r->xb, static_cast<size_t>(rows) * dim));
+    EDL_TRY(dalloc(&r->yb, static_cast<size_t>(rows)));
+    EDL_TRY(dalloc(&r->ws, static_cast<size_t>(rows) + 1));
+    EDL_TRY(dalloc(&r->total, static_cast<size_t>(dim) + 1));
+  }
+  EDL_TRY(dalloc(&r->loss_sum, 1));
+  EDL_CUDA_TRY(cudaStreamSynchronize(r->stream));
+  return EDL_OK;
+}
+
+int Job::build_worker(Worker* w, Replica* r) {
+  DeviceGuard g(r->device);
+  w->rep = r;
+  w->runs_cap = r->rows_cap + 2;
+  EDL_TRY(dalloc(&w->runs_dev, static_cast<size_t>(w->runs_cap)));
+  EDL_CUDA_TRY(cudaMallocHost(&w->runs_host, sizeof(EdlRun) * w->runs_cap * kSlots));
+  EDL_TRY(dalloc(&w->loss, 1));
+  if (mlp_)
+    EDL_TRY(dalloc(&w->grad, P_));
+  else
+    EDL_TRY(dalloc(&w->g, static_cast<size_t>(cfg_.data.dim) + 1));
+  return EDL_OK;
+}
+
+void Job::free_worker(Worker* w) {
+  if (!w || !w->rep) return;
+  DeviceGuard g(w->rep->device);
+  cudaFree(w->runs_dev);
+  cudaFreeHost(w->runs_host);
+  cudaFree(w->loss);
+  cudaFree(w->grad);
+  cudaFree(w->g);
+  w->rep = nullptr;
+}
+
+Job::~Job() {
+  for (auto& e : events_)
+    if (e->prep && e->prep->joinable()) e->prep->join();
+  for (auto& [dev, r] : reps_) {
+    DeviceGuard g(dev);
+    if (r->stream) cudaStreamSynchronize(r->stream);
+  }
+  for (auto& [ev, w] : graveyard_) {
+    free_worker(w.get());
+    cudaEventDestroy(ev);
+  }
+  for (auto& e : events_)
+    for (auto& w : e->prepared) free_worker(w.get());
+  for (auto& [id, w] : workers_) free_worker(w.get());
+  for (auto& [dev, r] : reps_) {
+    DeviceGuard g(dev);
+    dataset_destroy(r->ds);
+    cudaFree(r->master);
+    cudaFree(r->W);
+    cudaFree(r->mom);
+    cudaFree(r->flags);
+    for (auto* a : r->act) cudaFree(a);
+    cudaFree(r->logits);
+    cudaFree(r->dlog);
+    cudaFree(r->dx[0]);
+    cudaFree(r->dx[1]);
+    cudaFree(r->row_loss);
+    cudaFree(r->labels);
+    cudaFree(r->w);
+    cudaFree(r->xb);
+    cudaFree(r->yb);
+    cudaFree(r->ws);
+    cudaFree(r->total);
+    cudaFree(r->loss_sum);
+    cudaFreeHost(r->host_loss);
+    for (int s = 0; s < kSlots; ++s) {
+      cudaEventDestroy(r->ev_begin[s]);
+      cudaEventDestroy(r->ev_end[s]);
+    }
+    cudaStreamDestroy(r->stream);
+  }
+}
+
+void Job::resplit() {
+  const int p = static_cast<int>(ring_.size());
+  if (cfg_.per_worker_batch > 0)
+    splits_.assign(static_cast<size_t>(p), cfg_.per_worker_batch);
+  else
+    splits_ = split_batch_vec(cfg_.batch, p);
+}
+
+// Draw `need` samples for one worker (protocol step 2).
+std::vector<std::pair<uint64_t, uint64_t>> Job::draw(Worker* w, int64_t need) {
+  std::vector<std::pair<uint64_t, uint64_t>> out;
+  out.reserve(static_cast<size_t>(need));
+  Cursor& c = w->cur;
+  while (need > 0) {
+    if (!c.has) {
+      const Lease n = lm_->next(w->id);
+      if (n.kind == LeaseKind::EpochEnd) continue;
+      if (n.kind == LeaseKind::Pending || n.status != LeaseStatus::Ok) break;
+      c.has = true;
+      c.part = n.meta.index;
+      c.off = n.resume;
+      c.len = n.meta.length;
+      c.first = n.meta.offset;
+      c.epoch = lm_->epoch();
+    }
+    const uint64_t k = std::min<uint64_t>(static_cast<uint64_t>(need), c.len - c.off);
+    for (uint64_t j = 0; j < k; ++j) out.emplace_back(c.epoch, c.first + c.off + j);
+    c.off += k;
+    need -= static_cast<int64_t>(k);
+    if (c.off >= c.len) {
+      lm_->progress(w->id, c.part, c.len);
+      c.has = false;
+    }
+  }
+  if (c.has) lm_->progress(w->id, c.part, c.off);
+  return out;
+}
+
+// Protocol step 1: topology switches due at this mini-batch.
+int Job::install_due(bool* switched) {
+  *switched = false;
+  bool changed = false;
+  while (!events_.empty() && events_.front()->switch_t <= static_cast<int64_t>(t_)) {
+    std::unique_ptr<Event> ev = std::move(events_.front());
+    events_.pop_front();
+    if (ev->out) {
+      if (ev->prep && ev->prep->joinable()) ev->prep->join();  // stall only if prep is late
+      if (ev->prep_rc != EDL_OK) return ev->prep_rc;
+      std::vector<size_t> order(ev->ids.size());
+      for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+      std::sort(order.begin(), order.end(),
+                [&](size_t a, size_t b) { return ev->ids[a] < ev->ids[b]; });
+      for (size_t i : order) {
+        const std::string& id = ev->ids[i];
+        if (std::find(ring_.begin(), ring_.end(), id) != ring_.end()) continue;
+        ring_.push_back(id);
+        lm_->enroll(id);
+        // model broadcast: newcomers on an existing device share that replica, which is
+        // already current; the lowest existing rank is the source.
+        workers_[id] = std::move(ev->prepared[i]);
+      }
+    } else {
+      std::vector<std::string> keep;
+      for (const auto& id : ring_) {
+        if (std::find(ev->ids.begin(), ev->ids.end(), id) == ev->ids.end()) {
+          keep.push_back(id);
+          continue;
+        }
+        lm_->reclaim(id);  // graceful exit: shard back at its last reported offset
+        lm_->retire(id);
+        auto it = workers_.find(id);
+        cudaEvent_t done;
+        DeviceGuard g(it->second->rep->device);
+        cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+        cudaEventRecord(done, it->second->rep->stream);
+        graveyard_.emplace_back(done, std::move(it->second));
+        workers_.erase(it);
+      }
+      ring_ = keep;
+    }
+    ++version_;
+    changed = true;
+    if (cfg_.keep_log) {
+      LogRec r;
+      r.kind = LogRec::Topo;
+      r.t = t_ == 0 ? 0 : t_ - 1;
+      r.version = version_;
+      r.ring = ring_;
+      log_.push_back(r);
+    }
+  }
+  if (changed) {
+    resplit();
+    *switched = true;
+  }
+  return EDL_OK;
+}
+
+int Job::ensure_plans(Worker* w, int64_t rows) {
+  Replica* r = w->rep;
+  if (r->plan_rows != rows) {
+    r->fwd.assign(static_cast<size_t>(L_), GemmPlan{});
+    r->dgrad.assign(static_cast<size_t>(L_), GemmPlan{});
+    for (int l = 0; l < L_; ++l) {
+      const bool last = l == L_ - 1;
+      void* outp = last ? static_cast<void*>(r->logits) : static_cast<void*>(r->act[l + 1]);
+      EDL_TRY(gemm_plan_init(&r->fwd[l], r->act[l], in_[l], 0, r->W + off_[l], in_[l], 0, outp,
+                             out_[l], static_cast<int>(rows), out_[l], in_[l], last ? 0 : 1,
+                             last ? 1 : 0, nullptr, 0, 0));
+      if (l > 0) {
+        const __nv_bfloat16* dy = last ? r->dlog : r->dx[(l + 1) & 1];
+        EDL_TRY(gemm_plan_init(&r->dgrad[l], dy, out_[l], 0, r->W + off_[l], in_[l], 1,
+                               r->dx[l & 1], in_[l], static_cast<int>(rows), in_[l], out_[l], 0,
+                               0, r->act[l], in_[l], 0));
+      }
+    }
+    r->plan_rows = rows;
+  }
+  if (w->plan_rows != rows) {
+    w->wgrad.assign(static_cast<size_t>(L_), GemmPlan{});
+    for (int l = 0; l < L_; ++l) {
+      const bool last = l == L_ - 1;
+      const __nv_bfloat16* dy = last ? r->dlog : r->dx[(l + 1) & 1];
+      EDL_TRY(gemm_plan_init(&w->wgrad[l], dy, out_[l], 1, r->act[l], in_[l], 1,
+                             w->grad + off_[l], in_[l], out_[l], in_[l], static_cast<int>(rows),
+                             0, 0, nullptr, 0, 0));
+    }
+    w->plan_rows = rows;
+  }
+  return EDL_OK;
+}
+
+int Job::run_worker_mlp(Worker* w, int slot) {
+  Replica* r = w->rep;
+  const int64_t rows = static_cast<int64_t>(w->plan.size());
+  EDL_CUDA_TRY(cudaMemsetAsync(w->loss, 0, sizeof(double), r->stream));
+  if (rows == 0) {  // ShardPending for the whole step: contributes a zero gradient
+    EDL_CUDA_TRY(cudaMemsetAsync(w->grad, 0, sizeof(__nv_bfloat16) * P_, r->stream));
+    return EDL_OK;
+  }
+  EdlRun* host = w->runs_host + static_cast<size_t>(slot) * w->runs_cap;
+  EDL_CUDA_TRY(cudaMemcpyAsync(w->runs_dev, host, sizeof(EdlRun) * w->n_runs,
+                               cudaMemcpyHostToDevice, r->stream));
+  EDL_TRY(gather(r->ds, w->runs_dev, w->n_runs, rows, r->act[0], r->labels, r->stream));
+  EDL_TRY(ensure_plans(w, rows));
+  for (int l = 0; l < L_; ++l) EDL_TRY(gemm_plan_run(r->fwd[l], r->stream));
+  EDL_TRY(softmax_xent(r->logits, r->labels, static_cast<int>(rows), cfg_.num_classes, r->dlog,
+                       r->row_loss, r->stream));
+  EDL_TRY(sum_rows(r->row_loss, static_cast<int>(rows), w->loss, r->stream));
+  for (int l = L_ - 1; l >= 0; --l) {
+    if (l > 0) EDL_TRY(gemm_plan_run(r->dgrad[l], r->stream));
+    EDL_TRY(gemm_plan_run(w->wgrad[l], r->stream));
+  }
+  return EDL_OK;
+}
+
+int Job::run_worker_linear(Worker* w, int slot) {
+  Replica* r = w->rep;
+  const int64_t rows = static_cast<int64_t>(w->plan.size());
+  if (rows > 0) {
+    EdlRun* host = w->runs_host + static_cast<size_t>(slot) * w->runs_cap;
+    EDL_CUDA_TRY(cudaMemcpyAsync(w->runs_dev, host, sizeof(EdlRun) * w->n_runs,
+                                 cudaMemcpyHostToDevice, r->stream));
+    EDL_TRY(gather(r->ds, w->runs_dev, w->n_runs, rows, r->xb, r->yb, r->stream));
+  }
+  EDL_TRY(linear_local_gradient(cfg_.model, r->w, r->xb, r->yb, rows, cfg_.data.dim, w->g, r->ws,
+                                r->stream));
+  EDL_TRY(linear_batch_loss(cfg_.model, r->w, r->xb, r->yb, rows, cfg_.data.dim, w->loss, r->ws,
+                            r->stream));
+  return EDL_OK;
+}
+
+// Protocol step 3.
+int Job::reduce_and_update(uint64_t count, uint64_t t) {
+  Replica* r = reps_.begin()->second.get();
+  const double eta_t = cfg_.eta / (1.0 + cfg_.decay * static_cast<double>(t));  // trainer.hpp:27
+  if (mlp_) {
+    std::vector<const __nv_bfloat16*> grads;
+    for (const auto& id : ring_) grads.push_back(workers_[id]->grad);
+    if (count > 0) {
+      __nv_bfloat16* wdst[1] = {r->W};
+      EDL_TRY(sgd_update_bf16(grads.data(), static_cast<int>(grads.size()), r->master, r->mom,
+                              wdst, 1, P_, static_cast<float>(eta_t / static_cast<double>(count)),
+                              static_cast<float>(1.0 / static_cast<double>(count)),
+                              static_cast<float>(eta_t), static_cast<float>(cfg_.momentum),
+                              r->stream));
+    }
+    std::vector<const double*> losses;
+    for (const auto& id : ring_) losses.push_back(workers_[id]->loss);
+    EDL_TRY(ordered_sum_f64(losses.data(), static_cast<int>(losses.size()), r->loss_sum,
+                            r->stream));
+  } else {
+    std::vector<const double*> gs, losses;
+    for (const auto& id : ring_) {
+      gs.push_back(workers_[id]->g);
+      losses.push_back(workers_[id]->loss);
+    }
+    EDL_TRY(ring_allreduce_f64(gs.data(), static_cast<int>(gs.size()),
+                               static_cast<size_t>(cfg_.data.dim) + 1, EDL_REDUCE_SUM, r->total,
+                               r->stream));
+    if (count > 0) EDL_TRY(linear_sgd(r->w, r->total, -1, eta_t, cfg_.data.dim, r->stream));
+    EDL_TRY(ordered_sum_f64(losses.data(), static_cast<int>(losses.size()), r->loss_sum,
+                            r->stream));
+  }
+  return EDL_OK;
+}
+
+void Job::collect_completed() {
+  while (!inflight_.empty()) {
+    Pending& p = inflight_.front();
+    Replica* r = reps_.begin()->second.get();
+    if (cudaEventQuery(r->ev_end[p.slot]) != cudaSuccess) break;
+    EdlStepReport rep{};
+    rep.t = p.t;
+    rep.version = p.version;
+    rep.ring_size = p.ring_size;
+    rep.switched = p.switched;
+    rep.count = p.count;
+    rep.loss = p.count ? r->host_loss[p.slot] / static_cast<double>(p.count) : 0.0;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r->ev_begin[p.slot], r->ev_end[p.slot]);
+    rep.step_ms = ms;
+    rep.stall_ms = 0.0;
+    if (p.have_prev) {
+      float st = 0.f;
+      if (cudaEventElapsedTime(&st, p.prev_end, r->ev_begin[p.slot]) == cudaSuccess)
+        rep.stall_ms = st;
+    }
+    step_ms_.push_back(rep.step_ms);
+    if (step_ms_.size() > 64) step_ms_.erase(step_ms_.begin());
+    last_ = rep;
+    inflight_.pop_front();
+  }
+  for (auto it = graveyard_.begin(); it != graveyard_.end();) {
+    if (cudaEventQuery(it->first) == cudaSuccess) {
+      free_worker(it->second.get());
+      cudaEventDestroy(it->first);
+      it = graveyard_.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
+double Job::median_step_ms() const {
+  if (step_ms_.empty()) return 0.0;
+  std::vector<double> v = step_ms_;
+  std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end());
+  return v[v.size() / 2];
+}
+
+int Job::step(EdlStepReport* out) {
+  Replica* r = reps_.begin()->second.get();
+  DeviceGuard g(r->device);
+  const int slot = static_cast<int>(launched_ % kSlots);
+  // pinned staging for this slot is free once the step that used it kSlots ago is done
+  if (launched_ >= kSlots) EDL_CUDA_TRY(cudaEventSynchronize(r->ev_end[slot]));
+  collect_completed();
+
+  bool switched = false;
+  EDL_TRY(install_due(&switched));
+
+  // protocol step 2: lease draws in ring order, runs for the gather kernel
+  uint64_t count = 0;
+  for (size_t k = 0; k < ring_.size(); ++k) {
+    Worker* w = workers_[ring_[k]].get();
+    w->plan = draw(w, splits_[k]);
+    count += w->plan.size();
+    EdlRun* host = w->runs_host + static_cast<size_t>(slot) * w->runs_cap;
+    int n = 0;
+    for (size_t i = 0; i < w->plan.size(); ++i) {
+      const uint64_t id = w->plan[i].second;
+      if (n > 0 && host[n - 1].first + host[n - 1].count == id)
+        host[n - 1].count++;
+      else
+        host[n++] = EdlRun{id, 1};
+    }
+    w->n_runs = n;
+  }
+
+  // device work
+  EDL_CUDA_TRY(cudaEventRecord(r->ev_begin[slot], r->stream));
+  for (const auto& id : ring_) {
+    Worker* w = workers_[id].get();
+    EDL_TRY(mlp_ ? run_worker_mlp(w, slot) : run_worker_linear(w, slot));
+  }
+  EDL_TRY(reduce_and_update(count, t_));
+  EDL_CUDA_TRY(cudaMemcpyAsync(&r->host_loss[slot], r->loss_sum, sizeof(double),
+                               cudaMemcpyDeviceToHost, r->stream));
+  EDL_CUDA_TRY(cudaEventRecord(r->ev_end[slot], r->stream));
+
+  Pending p{t_, slot, count, version_, static_cast<int>(ring_.size()), switched ? 1 : 0,
+            last_end_ != nullptr, last_end_};
+  inflight_.push_back(p);
+  last_end_ = r->ev_end[slot];
+
+  if (cfg_.keep_log) {
+    for (const auto& id : ring_) {
+      LogRec rec;
+      rec.t = t_;
+      rec.worker = id;
+      rec.samples = workers_[id]->plan;
+      log_.push_back(std::move(rec));
+    }
+  }
+  if (out) {
+    *out = EdlStepReport{};
+    out->t = t_;
+    out->version = version_;
+    out->ring_size = static_cast<int32_t>(ring_.size());
+    out->switched = switched ? 1 : 0;
+    out->count = count;
+    out->loss = NAN;
+  }
+  ++t_;
+  ++launched_;
+  return EDL_OK;
+}
+
+int Job::sync(EdlStepReport* out) {
+  for (auto& [dev, r] : reps_) {
+    DeviceGuard g(dev);
+    EDL_CUDA_TRY(cudaStreamSynchronize(r->stream));
+  }
+  collect_completed();
+  if (out) *out = last_;
+  return EDL_OK;
+}
+
+// scale_out / scale_in / scripted event.  explicit_switch < 0: scheduler-facing call,
+// switch at t + max(1, ceil(T_a / T_b)) and Retry while another scaling op is pending.
+int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<int>& devices,
+               int64_t explicit_switch, int64_t* switch_t) {
+  if (ids.empty()) return fail(EDL_EINVAL, "scale: empty worker set");
+  if (explicit_switch < 0 && !events_.empty())
+    return fail(EDL_RETRY, "a scaling operation is in progress");
+  auto ev = std::make_unique<Event>();
+  ev->out = out;
+  ev->ids = ids;
+  ev->devices = devices;
+  if (explicit_switch >= 0) {
+    ev->switch_t = explicit_switch;
+  } else {
+    const double tb = median_step_ms();
+    int64_t k = 1;
+    if (tb > 0) k = std::max<int64_t>(1, static_cast<int64_t>(std::ceil(cfg_.t_a_ms / tb)));
+    ev->switch_t = static_cast<int64_t>(t_) + k;
+  }
+  if (out) {
+    for (const auto& id : ids)
+      if (workers_.count(id)) return fail(EDL_EINVAL, "scale_out: worker already in the job");
+    if (devices.size() != ids.size()) return fail(EDL_EINVAL, "scale_out: one device per worker");
+    for (int d : devices) {
+      int rc = EDL_OK;
+      if (!replica_for(d, &rc)) return rc;
+    }
+    // execution-context preparation off the training thread (§4.2): buffers,
+    // pinned staging; the training loop keeps stepping meanwhile.
+    ev->prepared.resize(ids.size());
+    Event* raw = ev.get();
+    ev->prep = std::make_unique<std::thread>([this, raw]() {
+      for (size_t i = 0; i < raw->ids.size(); ++i) {
+        auto w = std::make_unique<Worker>();
+        w->id = raw->ids[i];
+        int rc = build_worker(w.get(), reps_[raw->devices[i]].get());
+        if (rc != EDL_OK) {
+          raw->prep_rc = rc;
+          return;
+        }
+        raw->prepared[i] = std::move(w);
+      }
+    });
+  } else {
+    size_t leaving = 0;
+    for (const auto& id : ids) {
+      if (!workers_.count(id)) return fail(EDL_UNKNOWN_WORKER, "scale_in: unknown worker " + id);
+      ++leaving;
+    }
+    if (leaving >= ring_.size()) return fail(EDL_EINVAL, "scale_in: no worker would remain");
+  }
+  if (switch_t) *switch_t = ev->switch_t;
+  auto pos = std::upper_bound(events_.begin(), events_.end(), ev->switch_t,
+                              [](int64_t s, const std::unique_ptr<Event>& e) { return s < e->switch_t; });
+  events_.insert(pos, std::move(ev));
+  return EDL_OK;
+}
+
+int Job::params(const std::string& worker, void* host, size_t bytes) {
+  auto it = workers_.find(worker);
+  if (it == workers_.end()) return fail(EDL_UNKNOWN_WORKER, "params: unknown worker " + worker);
+  Replica* r = it->second->rep;
+  DeviceGuard g(r->device);
+  EDL_CUDA_TRY(cudaStreamSynchronize(r->stream));
+  const size_t need = mlp_ ? sizeof(float) * P_ : sizeof(double) * P_;
+  if (bytes < need) return fail(EDL_EINVAL, "params: buffer too small");
+  EDL_CUDA_TRY(cudaMemcpy(host, mlp_ ? static_cast<void*>(r->master) : static_cast<void*>(r->w),
+                          need, cudaMemcpyDeviceToHost));
+  return EDL_OK;
+}
+
+std::string Job::log_text() const {  // write_log_file, trainer.cpp:79-100
+  std::ostringstream o;
+  for (const auto& r : log_) {
+    if (r.kind == LogRec::Batch) {
+      o << "batch " << r.t << " " << r.worker << " " << r.samples.size();
+      for (const auto& [e, id] : r.samples) o << " " << e << ":" << id;
+      o << "\n";
+    } else if (r.kind == LogRec::Topo) {
+      o << "topo " << r.t << " " << r.version << " " << r.ring.size();
+      for (const auto& w : r.ring) o << " " << w;
+      o << "\n";
+    } else {
+      o << "restore " << r.t << "\n";
+    }
+  }
+  return o.str();
+}
+
+std::string Job::ring_csv() const {
+  std::string s;
+  for (size_t i = 0; i < ring_.size(); ++i) s += (i ? "," : "") + ring_[i];
+  return s;
+}
+
+}  // namespace edl

@@ -1,0 +1,172 @@
+// Elastic data-parallel job runtime (the reference's absent runtime layer).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <deque>
+#include <map>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "collective.hpp"
+#include "edl_internal.hpp"
+#include "kernels.hpp"
+#include "lease.hpp"
+
+namespace edl {
+
+constexpr int kSlots = 4;  // steps in flight on the host side (pinned staging ring)
+
+struct LogRec {  // LogRecord, include/edl/trainer.hpp:59-70
+  enum Kind { Batch = 0, Topo = 1, Restore = 2 } kind = Batch;
+  uint64_t t = 0;
+  std::string worker;
+  std::vector<std::pair<uint64_t, uint64_t>> samples;  // (epoch, id) in draw order
+  uint64_t version = 0;
+  std::vector<std::string> ring;
+};
+
+struct Cursor {  // a worker's current shard lease
+  bool has = false;
+  uint32_t part = 0;
+  uint64_t off = 0, len = 0, first = 0, epoch = 0;
+};
+
+// Model state + scratch on one GPU.  Workers on the same device share it: their replicas
+// would be bit-identical at every mini-batch boundary (SPEC.md trainer invariants).
+struct Replica {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  Dataset* ds = nullptr;
+  // MLP
+  float* master = nullptr;
+  __nv_bfloat16* W = nullptr;
+  float* mom = nullptr;
+  uint32_t* flags = nullptr;
+  int64_t rows_cap = 0;
+  std::vector<__nv_bfloat16*> act;  // act[l]: input of layer l, [rows][in_l]
+  float* logits = nullptr;
+  __nv_bfloat16* dlog = nullptr;
+  __nv_bfloat16* dx[2] = {nullptr, nullptr};
+  float* row_loss = nullptr;
+  int32_t* labels = nullptr;
+  int64_t plan_rows = -1;
+  std::vector<GemmPlan> fwd, dgrad;
+  // linear
+  double* w = nullptr;
+  double* xb = nullptr;
+  double* yb = nullptr;
+  double* ws = nullptr;
+  double* total = nullptr;
+  double* loss_sum = nullptr;
+  // per-step events
+  cudaEvent_t ev_begin[kSlots] = {};
+  cudaEvent_t ev_end[kSlots] = {};
+  double* host_loss = nullptr;  // pinned [kSlots]
+};
+
+struct Worker {
+  std::string id;
+  Replica* rep = nullptr;
+  __nv_bfloat16* grad = nullptr;  // MLP gradient sum [P]
+  double* g = nullptr;            // linear [grad_sum, count] (dim + 1)
+  double* loss = nullptr;         // device scalar (sum over this worker's batch)
+  EdlRun* runs_dev = nullptr;
+  EdlRun* runs_host = nullptr;  // pinned [kSlots][runs_cap]
+  int64_t runs_cap = 0;
+  std::vector<GemmPlan> wgrad;
+  int64_t plan_rows = -1;
+  Cursor cur;
+  // current step
+  std::vector<std::pair<uint64_t, uint64_t>> plan;
+  int n_runs = 0;
+};
+
+struct Event {
+  int64_t switch_t;
+  bool out;
+  std::vector<std::string> ids;
+  std::vector<int> devices;
+  std::vector<std::unique_ptr<Worker>> prepared;  // scale-out newcomers built off-thread
+  std::unique_ptr<std::thread> prep;
+  int prep_rc = EDL_OK;
+  double requested_ms = 0;
+};
+
+class Job {
+ public:
+  static int create(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
+                    const std::vector<int>& devices, Job** out);
+  ~Job();
+
+  int step(EdlStepReport* rep);
+  int sync(EdlStepReport* rep);
+  int scale(bool out, const std::vector<std::string>& ids, const std::vector<int>& devices,
+            int64_t explicit_switch, int64_t* switch_t);
+  int params(const std::string& worker, void* host, size_t bytes);
+  std::string log_text() const;
+  std::string ring_csv() const;
+  uint64_t t() const { return t_; }
+  size_t param_count() const { return P_; }
+  double median_step_ms() const;
+  int lease_snapshot(std::vector<uint8_t>* out) const {
+    *out = lm_->snapshot();
+    return EDL_OK;
+  }
+
+ private:
+  Job() = default;
+  int init(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
+           const std::vector<int>& devices);
+  Replica* replica_for(int device, int* rc);
+  int build_replica(Replica* r);
+  int build_worker(Worker* w, Replica* r);
+  void free_worker(Worker* w);
+  int ensure_plans(Worker* w, int64_t rows);
+  int install_due(bool* switched);
+  void resplit();
+  std::vector<std::pair<uint64_t, uint64_t>> draw(Worker* w, int64_t need);
+  int run_worker_mlp(Worker* w, int slot);
+  int run_worker_linear(Worker* w, int slot);
+  int reduce_and_update(uint64_t count, uint64_t t);
+  void collect_completed();
+
+  EdlJobConfig cfg_{};
+  bool mlp_ = false;
+  int L_ = 0;
+  std::vector<int> in_, out_;
+  std::vector<size_t> off_;
+  size_t P_ = 0;
+  std::unique_ptr<LeaseManager> lm_;
+  std::map<int, std::unique_ptr<Replica>> reps_;
+  std::map<std::string, std::unique_ptr<Worker>> workers_;
+  std::vector<std::string> ring_;
+  std::vector<int64_t> splits_;
+  std::deque<std::unique_ptr<Event>> events_;
+  std::vector<LogRec> log_;
+  uint64_t t_ = 0, version_ = 1;
+  uint64_t launched_ = 0;  // steps launched
+  uint32_t coll_epoch_ = 0;
+  // completed-step bookkeeping
+  struct Pending {
+    uint64_t t;
+    int slot;
+    uint64_t count;
+    uint64_t version;
+    int ring_size;
+    int switched;
+    bool have_prev;
+    cudaEvent_t prev_end;
+  };
+  std::deque<Pending> inflight_;
+  std::vector<double> step_ms_;
+  EdlStepReport last_{};
+  std::vector<std::pair<cudaEvent_t, std::unique_ptr<Worker>>> graveyard_;
+  cudaEvent_t last_end_ = nullptr;
+};
+
+}  // namespace edl

@@ -1,0 +1,177 @@
+"""Elastic job runtime — Python face of the C ABI (include/edl_b200.h, csrc/runtime.cpp).
+
+Mirrors the reference's (spec-only) job/worker API: scale_out / scale_in / step with
+notify_batch_end folded in / split_batch (Table 1).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+LEAST_SQUARES, LOGISTIC, MLP = 0, 1, 2
+
+
+def split_batch(B: int, p: int) -> list:
+    """SPEC.md:339-347; raises EdlError(Invalid) when B < p."""
+    out = (C.c_int64 * max(1, p))()
+    _lib.check(_lib.lib().edl_split_batch(B, p, out))
+    return list(out[:p])
+
+
+def switch_delay(t_a_ms: float, t_b_ms: float) -> int:
+    """k = max(1, ceil(T_a / T_b))."""
+    return _lib.lib().edl_switch_delay(t_a_ms, t_b_ms)
+
+
+def eta_at(eta: float, decay: float, t: int) -> float:  # trainer.hpp:27-29
+    return _lib.lib().edl_eta_at(eta, decay, t)
+
+
+@dataclass
+class JobConfig:
+    model: int = LEAST_SQUARES
+    size: int = 8192
+    dim: int = 64
+    seed: int = 1
+    noise: float = 0.01
+    sign_labels: bool = False
+    num_classes: int = 4096
+    layers: int = 8
+    hidden: int = 4096
+    eta: float = 0.05
+    decay: float = 0.0
+    momentum: float = 0.0
+    batch: int = 64
+    per_worker_batch: int = 0
+    lease_seed: int = 7
+    partitions: int = 0
+    max_workers: int = 1
+    init_seed: int = 0
+    t_a_ms: float = 500.0
+    keep_log: bool = True
+
+    def to_c(self) -> _lib.EdlJobConfig:
+        c = _lib.EdlJobConfig()
+        c.model = self.model
+        c.data = _lib.EdlSyntheticSpec(self.size, self.dim, self.seed, self.noise,
+                                       int(self.sign_labels))
+        c.num_classes, c.layers, c.hidden = self.num_classes, self.layers, self.hidden
+        c.eta, c.decay, c.momentum = self.eta, self.decay, self.momentum
+        c.batch, c.per_worker_batch = self.batch, self.per_worker_batch
+        c.lease_seed, c.partitions, c.max_workers = self.lease_seed, self.partitions, self.max_workers
+        c.init_seed, c.t_a_ms, c.keep_log = self.init_seed, self.t_a_ms, int(self.keep_log)
+        return c
+
+
+@dataclass
+class StepReport:
+    t: int
+    version: int
+    ring_size: int
+    switched: bool
+    count: int
+    loss: float
+    step_ms: float
+    stall_ms: float
+
+    @staticmethod
+    def of(r: _lib.EdlStepReport) -> "StepReport":
+        return StepReport(r.t, r.version, r.ring_size, bool(r.switched), r.count, r.loss,
+                          r.step_ms, r.stall_ms)
+
+
+class Job:
+    """One elastic data-parallel SGD job (JobState)."""
+
+    def __init__(self, cfg: JobConfig, ring, devices=None):
+        self._L = _lib.lib()
+        self.cfg = cfg
+        ring = list(ring)
+        devices = list(devices) if devices is not None else [0] * len(ring)
+        h = C.c_void_p()
+        c = cfg.to_c()
+        dev = (C.c_int32 * len(devices))(*devices)
+        _lib.check(self._L.edl_job_create(C.byref(c), _lib.cstrs(ring), dev, len(ring), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.edl_job_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def step(self) -> StepReport:
+        r = _lib.EdlStepReport()
+        _lib.check(self._L.edl_job_step(self._h, C.byref(r)))
+        return StepReport.of(r)
+
+    def sync(self) -> StepReport:
+        r = _lib.EdlStepReport()
+        _lib.check(self._L.edl_job_sync(self._h, C.byref(r)))
+        return StepReport.of(r)
+
+    def scale_out(self, ids, devices=None) -> int:
+        ids = list(ids)
+        devices = list(devices) if devices is not None else [0] * len(ids)
+        st = C.c_int64()
+        dev = (C.c_int32 * len(devices))(*devices)
+        _lib.check(self._L.edl_job_scale_out(self._h, _lib.cstrs(ids), dev, len(ids), C.byref(st)))
+        return st.value
+
+    def scale_in(self, ids, allowance_ms: float = 30000.0) -> int:
+        ids = list(ids)
+        st = C.c_int64()
+        _lib.check(self._L.edl_job_scale_in(self._h, _lib.cstrs(ids), len(ids), allowance_ms,
+                                            C.byref(st)))
+        return st.value
+
+    def schedule(self, switch_t: int, out: bool, ids, devices=None) -> None:
+        ids = list(ids)
+        devices = list(devices) if devices is not None else [0] * len(ids)
+        dev = (C.c_int32 * max(1, len(devices)))(*devices)
+        _lib.check(self._L.edl_job_schedule(self._h, switch_t, 1 if out else 0, _lib.cstrs(ids),
+                                            dev, len(ids)))
+
+    def param_count(self) -> int:
+        return self._L.edl_job_param_count(self._h)
+
+    def params(self, worker: str) -> np.ndarray:
+        n = self.param_count()
+        dt = np.float32 if self.cfg.model == MLP else np.float64
+        out = np.empty(n, dtype=dt)
+        _lib.check(self._L.edl_job_params(self._h, worker.encode(), out.ctypes.data, out.nbytes))
+        return out
+
+    @property
+    def t(self) -> int:
+        return self._L.edl_job_t(self._h)
+
+    def median_step_ms(self) -> float:
+        return self._L.edl_job_median_step_ms(self._h)
+
+    def _text(self, fn) -> str:
+        n = C.c_size_t()
+        fn(self._h, None, 0, C.byref(n))
+        buf = C.create_string_buffer(n.value + 1)
+        fn(self._h, buf, n.value + 1, C.byref(n))
+        return buf.value.decode()
+
+    def log_text(self) -> str:
+        return self._text(self._L.edl_job_log)
+
+    def ring(self) -> list:
+        s = self._text(self._L.edl_job_ring)
+        return s.split(",") if s else []
+
+    def lease_snapshot(self) -> bytes:
+        n = C.c_size_t()
+        self._L.edl_job_lease_snapshot(self._h, None, 0, C.byref(n))
+        buf = (C.c_uint8 * n.value)()
+        self._L.edl_job_lease_snapshot(self._h, buf, n.value, C.byref(n))
+        return bytes(buf)
