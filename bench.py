@@ -1,0 +1,281 @@
+#!/usr/bin/env python
+"""bench.py — samples/sec of EDL's elastic data-parallel SGD step on B200.
+
+Metric (BASELINE.json): samples/sec at 1/2/4/8 B200.  Workload at N=1: BASELINE.json
+configs[1] — MLP 4096-wide x 8 layers, bf16, batch 512 per GPU, softmax-CE over 4096 classes,
+plain SGD (the reference's sgd_step semantics), HBM-resident synthetic dataset of 2^20 samples
+(8 GiB bf16) fed by partition leases.  A "step" is one mini-batch through the public job API:
+host lease draws -> H2D lease runs -> gather -> 8 fwd GEMMs -> softmax-CE -> 15 bwd GEMMs ->
+fused allreduce + SGD update -> D2H loss.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "samples/sec at 1/2/4/8 B200; scale-out/in stall ms vs stop-resume"
+UNIT = "samples/s"
+WORKLOAD = dict(dim=4096, hidden=4096, classes=4096, layers=8, batch=512, size=1 << 20)
+
+
+def flops_per_sample(w=WORKLOAD) -> float:
+    """6 * params per sample (fwd 2P + dgrad 2P + wgrad 2P; layer-0 dgrad is skipped but
+    kept in the algorithmic count like SURVEY.md §8(d))."""
+    p = w["dim"] * w["hidden"] + (w["layers"] - 2) * w["hidden"] ** 2 + w["hidden"] * w["classes"]
+    return 6.0 * p, p
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        if not self.proc or not self.path:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_step(batch: int, steps: int, w=WORKLOAD):
+    """The CPU port of the same MLP step (oracle/mlp.py, numpy/BLAS on every host core):
+    the reference has no MLP, so its SGD semantics are restated there."""
+    import numpy as np
+    from oracle.mlp import MLPOracle
+    orc = MLPOracle(w["dim"], w["hidden"], w["classes"], w["layers"], 1, 0, 0.05, 0.0)
+    rng = np.random.default_rng(0)
+    times = []
+    for t in range(steps):
+        ids = rng.integers(0, w["size"], size=batch).astype(np.uint64)
+        t0 = time.perf_counter()
+        orc.step([("w00", ids)], t)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+    batch = int(os.environ.get("EDL_REF_BATCH", "128"))
+    times = cpu_reference_step(batch, args.warmup + args.steps)
+    timed = times[args.warmup:]
+    total = sum(timed)
+    value = batch * len(timed) / total
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(timed),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic", "config": {"workload": "mlp4096x8_bf16_b512_sgd",
+                                        "parallelism": f"dp{args.gpus}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{batch}-sample mini-batches of the full 4096x8 MLP step "
+                                   f"(numpy/BLAS port oracle/mlp.py; the reference has no MLP)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, rank: int, world: int) -> None:
+    import torch
+    from paper_1909_11985_b200 import runtime as rt
+
+    if world > 1:
+        raise SystemExit("bench.py: multi-process data parallelism is built in "
+                         "paper_1909_11985_b200.dist (not yet wired into bench.py)")
+    dev = 0
+    torch.cuda.set_device(dev)
+    w = WORKLOAD
+    cfg = rt.JobConfig(model=rt.MLP, size=w["size"], dim=w["dim"], seed=1, noise=0.0,
+                       num_classes=w["classes"], layers=w["layers"], hidden=w["hidden"],
+                       eta=0.05, decay=0.0, batch=w["batch"], per_worker_batch=w["batch"],
+                       lease_seed=7, partitions=64, max_workers=max(1, world), init_seed=0,
+                       keep_log=False)
+    job = rt.Job(cfg, [f"w{rank:02d}"], [dev])
+    stream = torch.cuda.ExternalStream(job.stream_handle())
+    for _ in range(args.warmup):
+        job.step()
+    job.sync()
+
+    flops, P = flops_per_sample()
+    # ---- value: K pipelined steps (inputs HBM-resident), device-timed on the job stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        # keep the GPU under the same load around the (short) timed region so the 200 ms
+        # clock samples see it: untimed steps for >= 1 s before and 0.5 s after
+        t_load = time.time()
+        while time.time() - t_load < 1.0:
+            for _ in range(20):
+                job.step()
+            job.sync()
+        job.set_profile(True)
+        job.reset_counters()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            job.step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        job.set_profile(False)
+        t_load = time.time()
+        while time.time() - t_load < 0.5:
+            for _ in range(20):
+                job.step()
+            job.sync()
+    ms = e0.elapsed_time(e1)
+    counters = job.counters()
+    clocks = clk.summary()
+    samples = w["batch"] * args.steps * world
+    value = samples / (ms / 1e3)
+
+    ph = counters["phase_ms"]
+    n = max(1, counters["steps"])
+    gemm_ms = (ph["forward"] + ph["backward"]) / n
+    upd_ms = ph["update"] / n
+    gemm_tflops = flops * w["batch"] / (gemm_ms / 1e3) / 1e12
+    upd_bytes = 12 * P  # bf16 grad read + fp32 master read/write + bf16 weight write
+    upd_gbs = upd_bytes / (upd_ms / 1e3) / 1e9
+    peaks = measured_peaks()
+    peak_t = peaks.get("bf16_tflops_sustained", 1354.1)
+    peak_h = peaks.get("hbm_gbs", 6555.5)
+
+    # ---- e2e: every step through the public API with a D2H read of its loss
+    job.reset_counters()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e2.record(stream)
+    losses = []
+    for _ in range(args.steps):
+        job.step()
+        losses.append(job.sync().loss)
+    e3.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = e2.elapsed_time(e3)
+    e2e_value = samples / (ms_e2e / 1e3)
+    runs_per_step = 2  # a 512-sample batch spans <= 2 shards of 16384 samples
+    launches = counters["launches"]
+
+    # ---- CPU baseline (oracle port), bounded sample on this host
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        batch = int(os.environ.get("EDL_CPU_BATCH", "64"))
+        t = cpu_reference_step(batch, 2)
+        cpu = {"value": batch / min(t), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": f"best of 2 {batch}-sample steps of the full 4096x8 MLP "
+                         f"(numpy/BLAS, oracle/mlp.py); the reference has no MLP"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (HBM-resident 2^20 x 4096 bf16 splitmix64 dataset, random-init MLP)",
+        "config": {"workload": "mlp4096x8_bf16_b512_sgd", "layers": w["layers"],
+                   "width": w["hidden"], "classes": w["classes"], "global_batch": samples // args.steps,
+                   "per_gpu_batch": w["batch"], "dataset_samples": w["size"],
+                   "parallelism": f"dp{world}", "optimizer": "sgd(eta=0.05), fp32 master",
+                   "l2": "inputs > L2 (weights 268 MB + fp32 master 537 MB streamed per step)"},
+        "e2e": {"value": e2e_value, "unit": UNIT,
+                "h2d_bytes_per_step": 16 * runs_per_step, "d2h_bytes_per_step": 8,
+                "note": "job.step()+job.sync() per step: host lease draws, H2D lease runs, D2H loss"},
+        "gpu_launches": launches,
+        "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMMs (8 fwd + 7 dgrad + 8 wgrad)",
+                     "achieved": gemm_tflops, "peak": peak_t, "unit": "TFLOP/s",
+                     "frac": gemm_tflops / peak_t, "traffic": None,
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
+                     "per_step_ms": gemm_ms, "algorithmic_gflop_per_step": flops * w["batch"] / 1e9},
+        "update_roofline": {"bound": "hbm", "achieved": upd_gbs, "peak": peak_h, "unit": "GB/s",
+                            "frac": upd_gbs / peak_h, "bytes_per_step": upd_bytes,
+                            "per_step_ms": upd_ms},
+        "phase_ms_per_step": {k: v / n for k, v in ph.items()},
+        "loss_first_last": [losses[0], losses[-1]] if losses else None,
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    job.close()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_b200(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

@@ -267,6 +267,14 @@ double edl_job_median_step_ms(const EdlJob* job);
 int edl_job_log(const EdlJob* job, char* buf, size_t cap, size_t* len);
 int edl_job_ring(const EdlJob* job, char* buf, size_t cap, size_t* len);
 int edl_job_lease_snapshot(const EdlJob* job, uint8_t* buf, size_t cap, size_t* len);
+/* Instrumentation (bench.py): the CUDA stream the job's kernels run on (cudaStream_t);
+ * per-phase device time from CUDA events recorded on that stream while profiling is on
+ * (phase_ms[5] = gather, forward GEMMs, loss, backward GEMMs, allreduce+update), the steps
+ * profiled and the number of library kernels launched since the last reset.            */
+void* edl_job_stream(const EdlJob* job);
+void edl_job_set_profile(EdlJob* job, int32_t on);
+void edl_job_counters(const EdlJob* job, double* phase_ms, uint64_t* steps, uint64_t* launches);
+void edl_job_reset_counters(EdlJob* job);
 
 #ifdef __cplusplus
 }

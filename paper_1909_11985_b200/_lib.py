@@ -150,6 +150,10 @@ def _declare(L: C.CDLL) -> None:
         "edl_job_log": ([vp, vp, sz, P(sz)], ci),
         "edl_job_ring": ([vp, vp, sz, P(sz)], ci),
         "edl_job_lease_snapshot": ([vp, vp, sz, P(sz)], ci),
+        "edl_job_stream": ([vp], vp),
+        "edl_job_set_profile": ([vp, i32], None),
+        "edl_job_counters": ([vp, P(f64), P(u64), P(u64)], None),
+        "edl_job_reset_counters": ([vp], None),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)  # AttributeError = the library lacks a declared entry point

@@ -319,7 +319,10 @@ int Job::install_due(bool* switched) {
                 [&](size_t a, size_t b) { return ev->ids[a] < ev->ids[b]; });
       for (size_t i : order) {
         const std::string& id = ev->ids[i];
-        if (std::find(ring_.begin(), ring_.end(), id) != ring_.end()) continue;
+        if (std::find(ring_.begin(), ring_.end(), id) != ring_.end()) {
+          free_worker(ev->prepared[i].get());  // already a member: nothing to join
+          continue;
+        }
         ring_.push_back(id);
         lm_->enroll(id);
         // model broadcast: newcomers on an existing device share that replica, which is
@@ -397,6 +400,32 @@ int Job::ensure_plans(Worker* w, int64_t rows) {
   return EDL_OK;
 }
 
+cudaEvent_t Job::mark_event() {
+  if (!ev_pool_.empty()) {
+    cudaEvent_t e = ev_pool_.back();
+    ev_pool_.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+cudaEvent_t Job::mark_begin(cudaStream_t s) {
+  if (!profile_) return nullptr;
+  cudaEvent_t e = mark_event();
+  cudaEventRecord(e, s);
+  return e;
+}
+
+cudaEvent_t Job::mark(int slot, int phase, cudaEvent_t start, cudaStream_t s) {
+  if (!profile_ || !start) return nullptr;
+  cudaEvent_t e = mark_event();
+  cudaEventRecord(e, s);
+  marks_[slot].push_back(Mark{phase, start, e});
+  return e;
+}
+
 int Job::run_worker_mlp(Worker* w, int slot) {
   Replica* r = w->rep;
   const int64_t rows = static_cast<int64_t>(w->plan.size());
@@ -405,41 +434,56 @@ int Job::run_worker_mlp(Worker* w, int slot) {
     EDL_CUDA_TRY(cudaMemsetAsync(w->grad, 0, sizeof(__nv_bfloat16) * P_, r->stream));
     return EDL_OK;
   }
+  EDL_TRY(ensure_plans(w, rows));
+  cudaEvent_t m = mark_begin(r->stream);
   EdlRun* host = w->runs_host + static_cast<size_t>(slot) * w->runs_cap;
   EDL_CUDA_TRY(cudaMemcpyAsync(w->runs_dev, host, sizeof(EdlRun) * w->n_runs,
                                cudaMemcpyHostToDevice, r->stream));
   EDL_TRY(gather(r->ds, w->runs_dev, w->n_runs, rows, r->act[0], r->labels, r->stream));
-  EDL_TRY(ensure_plans(w, rows));
+  m = mark(slot, 0, m, r->stream);
   for (int l = 0; l < L_; ++l) EDL_TRY(gemm_plan_run(r->fwd[l], r->stream));
+  m = mark(slot, 1, m, r->stream);
   EDL_TRY(softmax_xent(r->logits, r->labels, static_cast<int>(rows), cfg_.num_classes, r->dlog,
                        r->row_loss, r->stream));
   EDL_TRY(sum_rows(r->row_loss, static_cast<int>(rows), w->loss, r->stream));
+  m = mark(slot, 2, m, r->stream);
   for (int l = L_ - 1; l >= 0; --l) {
     if (l > 0) EDL_TRY(gemm_plan_run(r->dgrad[l], r->stream));
     EDL_TRY(gemm_plan_run(w->wgrad[l], r->stream));
   }
+  m = mark(slot, 3, m, r->stream);
+  (void)m;
+  launches_ += 1 + static_cast<uint64_t>(L_) + 2 + static_cast<uint64_t>(2 * L_ - 1);
   return EDL_OK;
 }
 
 int Job::run_worker_linear(Worker* w, int slot) {
   Replica* r = w->rep;
   const int64_t rows = static_cast<int64_t>(w->plan.size());
+  cudaEvent_t m = mark_begin(r->stream);
   if (rows > 0) {
     EdlRun* host = w->runs_host + static_cast<size_t>(slot) * w->runs_cap;
     EDL_CUDA_TRY(cudaMemcpyAsync(w->runs_dev, host, sizeof(EdlRun) * w->n_runs,
                                  cudaMemcpyHostToDevice, r->stream));
     EDL_TRY(gather(r->ds, w->runs_dev, w->n_runs, rows, r->xb, r->yb, r->stream));
+    launches_ += 1;
   }
+  m = mark(slot, 0, m, r->stream);
   EDL_TRY(linear_local_gradient(cfg_.model, r->w, r->xb, r->yb, rows, cfg_.data.dim, w->g, r->ws,
                                 r->stream));
+  m = mark(slot, 3, m, r->stream);
   EDL_TRY(linear_batch_loss(cfg_.model, r->w, r->xb, r->yb, rows, cfg_.data.dim, w->loss, r->ws,
                             r->stream));
+  m = mark(slot, 2, m, r->stream);
+  (void)m;
+  launches_ += (rows > 0 ? 2 : 1) + (rows > 0 ? 2 : 1);
   return EDL_OK;
 }
 
 // Protocol step 3.
-int Job::reduce_and_update(uint64_t count, uint64_t t) {
+int Job::reduce_and_update(uint64_t count, uint64_t t, int slot) {
   Replica* r = reps_.begin()->second.get();
+  cudaEvent_t m = mark_begin(r->stream);
   const double eta_t = cfg_.eta / (1.0 + cfg_.decay * static_cast<double>(t));  // trainer.hpp:27
   if (mlp_) {
     std::vector<const __nv_bfloat16*> grads;
@@ -456,6 +500,7 @@ int Job::reduce_and_update(uint64_t count, uint64_t t) {
     for (const auto& id : ring_) losses.push_back(workers_[id]->loss);
     EDL_TRY(ordered_sum_f64(losses.data(), static_cast<int>(losses.size()), r->loss_sum,
                             r->stream));
+    launches_ += (count > 0 ? 1 : 0) + 1;
   } else {
     std::vector<const double*> gs, losses;
     for (const auto& id : ring_) {
@@ -468,7 +513,10 @@ int Job::reduce_and_update(uint64_t count, uint64_t t) {
     if (count > 0) EDL_TRY(linear_sgd(r->w, r->total, -1, eta_t, cfg_.data.dim, r->stream));
     EDL_TRY(ordered_sum_f64(losses.data(), static_cast<int>(losses.size()), r->loss_sum,
                             r->stream));
+    launches_ += 2 + (count > 0 ? 1 : 0);
   }
+  m = mark(slot, 4, m, r->stream);
+  (void)m;
   return EDL_OK;
 }
 
@@ -493,6 +541,18 @@ void Job::collect_completed() {
       if (cudaEventElapsedTime(&st, p.prev_end, r->ev_begin[p.slot]) == cudaSuccess)
         rep.stall_ms = st;
     }
+    std::vector<cudaEvent_t> used;
+    for (const Mark& mk : marks_[p.slot]) {
+      float pm = 0.f;
+      if (cudaEventElapsedTime(&pm, mk.a, mk.b) == cudaSuccess) phase_ms_[mk.phase] += pm;
+      used.push_back(mk.a);
+      used.push_back(mk.b);
+    }
+    std::sort(used.begin(), used.end());
+    used.erase(std::unique(used.begin(), used.end()), used.end());
+    ev_pool_.insert(ev_pool_.end(), used.begin(), used.end());
+    if (!marks_[p.slot].empty()) ++phase_steps_;
+    marks_[p.slot].clear();
     step_ms_.push_back(rep.step_ms);
     if (step_ms_.size() > 64) step_ms_.erase(step_ms_.begin());
     last_ = rep;
@@ -551,7 +611,7 @@ int Job::step(EdlStepReport* out) {
     Worker* w = workers_[id].get();
     EDL_TRY(mlp_ ? run_worker_mlp(w, slot) : run_worker_linear(w, slot));
   }
-  EDL_TRY(reduce_and_update(count, t_));
+  EDL_TRY(reduce_and_update(count, t_, slot));
   EDL_CUDA_TRY(cudaMemcpyAsync(&r->host_loss[slot], r->loss_sum, sizeof(double),
                                cudaMemcpyDeviceToHost, r->stream));
   EDL_CUDA_TRY(cudaEventRecord(r->ev_end[slot], r->stream));
@@ -615,7 +675,8 @@ int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<
   }
   if (out) {
     for (const auto& id : ids)
-      if (workers_.count(id)) return fail(EDL_EINVAL, "scale_out: worker already in the job");
+      if (workers_.count(id) && explicit_switch < 0)
+        return fail(EDL_EINVAL, "scale_out: worker already in the job");
     if (devices.size() != ids.size()) return fail(EDL_EINVAL, "scale_out: one device per worker");
     for (int d : devices) {
       int rc = EDL_OK;
@@ -638,12 +699,15 @@ int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<
       }
     });
   } else {
-    size_t leaving = 0;
-    for (const auto& id : ids) {
-      if (!workers_.count(id)) return fail(EDL_UNKNOWN_WORKER, "scale_in: unknown worker " + id);
-      ++leaving;
+    // Scripted events are validated when they are installed (the ring may change before).
+    if (explicit_switch < 0) {
+      size_t leaving = 0;
+      for (const auto& id : ids) {
+        if (!workers_.count(id)) return fail(EDL_UNKNOWN_WORKER, "scale_in: unknown worker " + id);
+        ++leaving;
+      }
+      if (leaving >= ring_.size()) return fail(EDL_EINVAL, "scale_in: no worker would remain");
     }
-    if (leaving >= ring_.size()) return fail(EDL_EINVAL, "scale_in: no worker would remain");
   }
   if (switch_t) *switch_t = ev->switch_t;
   auto pos = std::upper_bound(events_.begin(), events_.end(), ev->switch_t,

@@ -117,6 +117,21 @@ class Job {
     *out = lm_->snapshot();
     return EDL_OK;
   }
+  void* stream() const { return reps_.begin()->second->stream; }
+  void set_profile(bool on) { profile_ = on; }
+  // accumulated device ms per phase (gather, forward, loss, backward, update) + launches
+  void phase_totals(double* ms, uint64_t* steps, uint64_t* launches) const {
+    for (int k = 0; k < kPhases; ++k) ms[k] = phase_ms_[k];
+    *steps = phase_steps_;
+    *launches = launches_;
+  }
+  void reset_counters() {
+    for (double& v : phase_ms_) v = 0;
+    phase_steps_ = 0;
+    launches_ = 0;
+  }
+  static constexpr int kPhases = 5;
+  static constexpr int kMaxMarks = 64;
 
  private:
   Job() = default;
@@ -132,7 +147,7 @@ class Job {
   std::vector<std::pair<uint64_t, uint64_t>> draw(Worker* w, int64_t need);
   int run_worker_mlp(Worker* w, int slot);
   int run_worker_linear(Worker* w, int slot);
-  int reduce_and_update(uint64_t count, uint64_t t);
+  int reduce_and_update(uint64_t count, uint64_t t, int slot);
   void collect_completed();
 
   EdlJobConfig cfg_{};
@@ -167,6 +182,22 @@ class Job {
   EdlStepReport last_{};
   std::vector<std::pair<cudaEvent_t, std::unique_ptr<Worker>>> graveyard_;
   cudaEvent_t last_end_ = nullptr;
+  // profiling: events at phase boundaries of each in-flight slot
+  bool profile_ = false;
+  struct Mark {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  std::vector<Mark> marks_[kSlots];
+  std::vector<cudaEvent_t> ev_pool_;
+  double phase_ms_[kPhases] = {};
+  uint64_t phase_steps_ = 0;
+  uint64_t launches_ = 0;  // kernels of this library launched
+  cudaEvent_t mark_event();
+  // Records a phase boundary on s; returns the event that starts the next phase (or null
+  // when profiling is off).
+  cudaEvent_t mark(int slot, int phase, cudaEvent_t start, cudaStream_t s);
+  cudaEvent_t mark_begin(cudaStream_t s);
 };
 
 }  // namespace edl

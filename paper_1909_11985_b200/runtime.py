@@ -169,6 +169,25 @@ class Job:
         s = self._text(self._L.edl_job_ring)
         return s.split(",") if s else []
 
+    def stream_handle(self) -> int:
+        """cudaStream_t of the job's kernels (for CUDA-event timing on the right stream)."""
+        return self._L.edl_job_stream(self._h) or 0
+
+    def set_profile(self, on: bool) -> None:
+        self._L.edl_job_set_profile(self._h, 1 if on else 0)
+
+    PHASES = ("gather", "forward", "loss", "backward", "update")
+
+    def counters(self) -> dict:
+        ms = (C.c_double * 5)()
+        steps, launches = C.c_uint64(), C.c_uint64()
+        self._L.edl_job_counters(self._h, ms, C.byref(steps), C.byref(launches))
+        return {"phase_ms": dict(zip(self.PHASES, list(ms))), "steps": steps.value,
+                "launches": launches.value}
+
+    def reset_counters(self) -> None:
+        self._L.edl_job_reset_counters(self._h)
+
     def lease_snapshot(self) -> bytes:
         n = C.c_size_t()
         self._L.edl_job_lease_snapshot(self._h, None, 0, C.byref(n))
