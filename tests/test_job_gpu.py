@@ -128,7 +128,7 @@ def test_mlp_elastic_vs_numpy_oracle(momentum):
     from paper_1909_11985_b200 import runtime as rt
     dim, hidden, classes, layers = 64, 128, 64, 3
     spec = {"size": 3000, "dim": dim, "seed": 5, "noise": 0.0, "sign_labels": False}
-    B, steps, eta, decay = 96, 12, 0.5, 0.01
+    B, steps, eta, decay = 96, 12, 0.1, 0.01
     events = [(4, True, ["w01"]), (9, False, ["w00"])]
     cfg = rt.JobConfig(model=rt.MLP, size=spec["size"], dim=dim, seed=5, noise=0.0,
                        num_classes=classes, layers=layers, hidden=hidden, eta=eta, decay=decay,
