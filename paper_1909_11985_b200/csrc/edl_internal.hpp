@@ -33,8 +33,8 @@ struct EpiParams {
 };
 // Pre-encoded launch (TMA descriptors built once; launching costs one kernel launch).
 struct GemmPlan {
-  CUtensorMap ta, tb;
-  int M = 0, N = 0, K = 0, a_mn = 0, b_mn = 0, bn = 0;
+  CUtensorMap ta, tb, tc;
+  int M = 0, N = 0, K = 0, a_mn = 0, b_mn = 0, bn = 0, cg = 1;
   EpiParams ep{};
 };
 int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B, int ldb,

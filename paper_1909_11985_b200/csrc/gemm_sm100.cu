@@ -45,7 +45,14 @@ struct Cfg {
   static constexpr uint32_t kBBytesMN = kBBoxes * kMnBlockBytes;  // MN-major B tile
   static constexpr uint32_t kBSlot = (kBBytesK > kBBytesMN ? kBBytesK : kBBytesMN);
   static constexpr uint32_t kStageBytes = kABytes + ((kBSlot + 1023) / 1024) * 1024;
-  static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+#ifndef EDL_GEMM_SMEM_KB
+#define EDL_GEMM_SMEM_KB 200
+#endif
+#ifndef EDL_GEMM_MAX_STAGES
+#define EDL_GEMM_MAX_STAGES 8
+#endif
+  static constexpr int kFit = (EDL_GEMM_SMEM_KB * 1024) / kStageBytes;
+  static constexpr int kStages = kFit > EDL_GEMM_MAX_STAGES ? EDL_GEMM_MAX_STAGES : kFit;
   static constexpr uint32_t kAccCols = BN;  // fp32 columns per accumulator
   static constexpr uint32_t kTmemCols = (2 * BN <= 32)    ? 32
                                         : (2 * BN <= 64)  ? 64
@@ -103,15 +110,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      const uint32_t tx = C::kABytes + (B_MN ? C::kBBytesMN : C::kBBytesK);
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile % m_tiles) * BM;
-        const int n0 = (tile / m_tiles) * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t tx = C::kABytes + (B_MN ? C::kBBytesMN : C::kBBytesK);
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int m0 = (tile % m_tiles) * BM;
+      const int n0 = (tile / m_tiles) * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (elect_one()) {
           uint8_t* sa = smem + stage * C::kStageBytes;
           uint8_t* sb = sa + C::kABytes;
           mbar_arrive_expect_tx(&full_bar[stage], tx);
@@ -129,47 +136,52 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {
             tma_load_2d(sb, &tmap_b, &full_bar[stage], kb * BK, n0);
           }
-          if (++stage == C::kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
+        }
+        __syncwarp();
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, A_MN, B_MN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int local = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+    constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, A_MN, B_MN);
+    const uint32_t s0 = smem_u32(smem);
+    const uint64_t a0 = A_MN ? smem_desc_sw128(s0, kMnBlockBytes, 1024) : smem_desc_sw128(s0, 16, 1024);
+    const uint64_t b0 = B_MN ? smem_desc_sw128(s0 + C::kABytes, kMnBlockBytes, 1024)
+                             : smem_desc_sw128(s0 + C::kABytes, 16, 1024);
+    constexpr uint32_t kStepA = A_MN ? 2048 : 32, kStepB = B_MN ? 2048 : 32;
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    // one fixed issuing lane: tcgen05.commit only tracks the MMAs of the executing thread
+    const bool issuer = elect_one();
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * C::kAccCols;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * C::kAccCols;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
-          tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
-          const uint32_t sb = sa + C::kABytes;
+        const uint64_t so = static_cast<uint64_t>(stage * C::kStageBytes) >> 4;
+        if (issuer) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t da = A_MN ? smem_desc_sw128(sa + k * 2048, kMnBlockBytes, 1024)
-                                     : smem_desc_sw128(sa + k * 32, 16, 1024);
-            const uint64_t db = B_MN ? smem_desc_sw128(sb + k * 2048, kMnBlockBytes, 1024)
-                                     : smem_desc_sw128(sb + k * 32, 16, 1024);
-            umma_bf16(d_tmem, da, db, idesc, (kb | k) != 0 ? 1u : 0u);
-          }
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(d_tmem, a0 + so + ((k * kStepA) >> 4), b0 + so + ((k * kStepB) >> 4), idesc,
+                      (kb | k) != 0 ? 1u : 0u);
           umma_commit(&empty_bar[stage]);
-          if (++stage == C::kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
-        umma_commit(&tfull_bar[acc]);
+        __syncwarp();
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
+      if (issuer) umma_commit(&tfull_bar[acc]);
+      __syncwarp();
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -256,6 +268,301 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------ CTA-pair kernel
+// cta_group::2 variant: a cluster of 2 CTAs (one TPC) computes a 256 x BN tile with
+// M=256 UMMAs issued by the pair leader.  Each CTA stages its own 128 rows of A and BN/2
+// rows of B, so each SM's shared memory feeds half the operand bytes per MMA that the
+// 1-SM kernel needs (the 1-SM kernel is shared-memory-bound at BN=128).  The epilogue
+// goes TMEM -> registers -> 128B-swizzled smem -> TMA bulk-tensor store (coalesced,
+// asynchronous); the two accumulator buffers let tile i's epilogue overlap tile i+1's MMAs.
+constexpr int kEpiChunkBytes = 32 * 128;  // one warp's 32 rows x 128 B staging box
+
+#ifdef EDL_GEMM_TRACE
+// [cta][0] mma wait-full cycles, [1] mma wait-tempty, [2] mma loop total, [3] producer
+// wait-empty, [4] producer total, [5] epilogue wait-tfull (warp 2), [6] epilogue total
+__device__ unsigned long long g_gemm_trace[296][8];
+#define TRACE_T0(v) const unsigned long long v = clock64()
+#define TRACE_ADD(slot, t0) atomicAdd(&g_gemm_trace[blockIdx.x][slot], clock64() - (t0))
+#else
+#define TRACE_T0(v)
+#define TRACE_ADD(slot, t0)
+#endif
+
+template <int BN>
+struct Cfg2 {
+  static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "2-SM tiles: BN multiple of 64");
+  static constexpr int kHalfN = BN / 2;
+  static constexpr uint32_t kABytes = 128 * BK * 2;                      // 16 KB
+  static constexpr int kBBoxesMN = (kHalfN + 63) / 64;  // MN-major B: 64-column TMA boxes
+  static constexpr uint32_t kBBytesK = static_cast<uint32_t>(kHalfN) * BK * 2;  // per CTA
+  static constexpr uint32_t kBBytesMN = kBBoxesMN * kMnBlockBytes;
+  static constexpr uint32_t kBSlot = kBBytesK > kBBytesMN ? kBBytesK : kBBytesMN;
+  static constexpr uint32_t kStageBytes = kABytes + ((kBSlot + 1023) / 1024) * 1024;
+  static constexpr uint32_t kEpiBytes = 4 * 2 * kEpiChunkBytes;         // 4 warps x 2 buffers
+#ifndef EDL_GEMM2_MAX_STAGES
+#define EDL_GEMM2_MAX_STAGES 6
+#endif
+  static constexpr int kFit = (224 * 1024 - kEpiBytes) / kStageBytes;
+  static constexpr int kStages = kFit > EDL_GEMM2_MAX_STAGES ? EDL_GEMM2_MAX_STAGES : kFit;
+  // N <= 128: two interleaved accumulators per tile (even / odd K-steps) so consecutive
+  // MMAs are independent; a dependent M=256 MMA chain is latency-bound below N = 256.
+  static constexpr int kSplit = 1;
+  static constexpr uint32_t kAccCols = BN * kSplit;
+  static constexpr uint32_t kTmemCols = (2 * kAccCols <= 256) ? 256 : 512;
+  static constexpr uint32_t kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 256;
+};
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                         const __grid_constant__ CUtensorMap tmap_b,
+                         const __grid_constant__ CUtensorMap tmap_c, int M, int N, int K,
+                         EpiParams ep) {
+  using C = Cfg2<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* epi = smem + C::kStages * C::kStageBytes;  // 1024-aligned staging
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(epi + C::kEpiBytes);
+  uint64_t* empty_bar = full_bar + C::kStages;
+  uint64_t* tfull_bar = empty_bar + C::kStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x / 2, n_pairs = gridDim.x / 2;
+  const int m_tiles = (M + 255) / 256;
+  const int n_tiles = (N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmap_a);
+    prefetch_tmap(&tmap_b);
+    prefetch_tmap(&tmap_c);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 8);  // lane 0 of the 4 epilogue warps of both CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_2sm<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised before any remote arrive / TMA
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // Producer and MMA loops run warp-uniform (all 32 lanes wait on the barriers; elect.sync
+  // picks the issuing lane) so descriptors and coordinates stay in uniform registers and
+  // each UTCHMMA / UTMALDG issues without a per-instruction R2UR waterfall.
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    int stage = 0;
+    uint32_t phase = 0;
+    // both CTAs' bytes (full boxes, OOB included) are counted on the leader's barrier
+    const uint32_t tx = 2 * (C::kABytes + (B_MN ? C::kBBytesMN : C::kBBytesK));
+    TRACE_T0(t_prod);
+    for (int tile = pair; tile < num_tiles; tile += n_pairs) {
+      const int m0 = (tile % m_tiles) * 256 + static_cast<int>(rank) * 128;
+      const int n0 = (tile / m_tiles) * BN + static_cast<int>(rank) * C::kHalfN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        TRACE_T0(t_w);
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        TRACE_ADD(3, t_w);
+        if (elect_one()) {
+          uint8_t* sa = smem + stage * C::kStageBytes;
+          uint8_t* sb = sa + C::kABytes;
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], tx);
+          if (A_MN) {
+            tma_load_2d_2sm(sa, &tmap_a, &full_bar[stage], m0, kb * BK);
+            tma_load_2d_2sm(sa + kMnBlockBytes, &tmap_a, &full_bar[stage], m0 + 64, kb * BK);
+          } else {
+            tma_load_2d_2sm(sa, &tmap_a, &full_bar[stage], kb * BK, m0);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < C::kBBoxesMN; ++j)
+              tma_load_2d_2sm(sb + j * kMnBlockBytes, &tmap_b, &full_bar[stage], n0 + 64 * j,
+                              kb * BK);
+          } else {
+            tma_load_2d_2sm(sb, &tmap_b, &full_bar[stage], kb * BK, n0);
+          }
+        }
+        __syncwarp();
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    TRACE_ADD(4, t_prod);
+  } else if (warp == 1) {
+    if (leader) {
+      // ------------------------------------------------------------ MMA issuer (pair leader)
+      constexpr uint32_t idesc = idesc_bf16_f32(256, BN, A_MN, B_MN);
+      // descriptors of stage 0 / k = 0; stage s, k-step k add (s*stage + k*step) >> 4 to the
+      // 14-bit start-address field (smem offsets < 256 KB never carry out of it)
+      const uint32_t s0 = smem_u32(smem);
+      const uint64_t a0 = A_MN ? smem_desc_sw128(s0, kMnBlockBytes, 1024) : smem_desc_sw128(s0, 16, 1024);
+      const uint64_t b0 = B_MN ? smem_desc_sw128(s0 + C::kABytes, kMnBlockBytes, 1024)
+                               : smem_desc_sw128(s0 + C::kABytes, 16, 1024);
+      constexpr uint32_t kStepA = A_MN ? 2048 : 32, kStepB = B_MN ? 2048 : 32;
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      // one fixed issuing lane: tcgen05.commit only tracks the MMAs of the executing thread
+      const bool issuer = elect_one();
+      TRACE_T0(t_mma);
+      for (int tile = pair; tile < num_tiles; tile += n_pairs, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        TRACE_T0(t_te);
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        TRACE_ADD(1, t_te);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * C::kAccCols;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          TRACE_T0(t_f);
+          mbar_wait(&full_bar[stage], phase);
+          TRACE_ADD(0, t_f);
+          tc_fence_after();
+          const uint64_t so = static_cast<uint64_t>(stage * C::kStageBytes) >> 4;
+          if (issuer) {
+  #pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16_2sm(d_tmem, a0 + so + ((k * kStepA) >> 4), b0 + so + ((k * kStepB) >> 4),
+                            idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_commit_2sm(&empty_bar[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (issuer) umma_commit_2sm(&tfull_bar[acc], 0x3);
+        __syncwarp();
+      }
+      TRACE_ADD(2, t_mma);
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int q = warp & 3;  // TMEM lane quarter
+    uint8_t* stage_buf = epi + q * 2 * kEpiChunkBytes;
+    int buf = 0;
+    int local = 0;
+    for (int tile = pair; tile < num_tiles; tile += n_pairs, ++local) {
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      const int row0 = (tile % m_tiles) * 256 + static_cast<int>(rank) * 128 + q * 32;
+      const int n0 = (tile / m_tiles) * BN;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = row0 + lane;
+      const uint32_t t_row =
+          tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::kAccCols;
+      const int cw = ep.out_f32 ? 32 : 64;  // columns per 128-byte staging row
+#pragma unroll 1
+      for (int c = 0; c < BN; c += cw) {
+        float v[64];
+        {
+          uint32_t r[32];
+          tmem_ld32(t_row + c, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          if (!ep.out_f32) {
+            tmem_ld32(t_row + c + 32, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[32 + j] = __uint_as_float(r[j]);
+          }
+          if (C::kSplit == 2) {  // fold the odd-K accumulator
+            tmem_ld32(t_row + BN + c, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += __uint_as_float(r[j]);
+            if (!ep.out_f32) {
+              tmem_ld32(t_row + BN + c + 32, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[32 + j] += __uint_as_float(r[j]);
+            }
+          }
+        }
+        if (ep.relu) {
+#pragma unroll
+          for (int j = 0; j < 64; ++j) v[j] = fmaxf(v[j], 0.0f);
+        }
+        if (ep.mask && row < M) {
+          const __nv_bfloat16* mrow = ep.mask + static_cast<size_t>(row) * ep.ldm + n0 + c;
+          if (n0 + c + 64 <= N) {
+#pragma unroll
+            for (int j8 = 0; j8 < 8; ++j8) {
+              const uint4 mv = __ldg(reinterpret_cast<const uint4*>(mrow + j8 * 8));
+              const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&mv);
+#pragma unroll
+              for (int t = 0; t < 8; ++t)
+                if (!(__bfloat162float(mb[t]) > 0.0f)) v[j8 * 8 + t] = 0.0f;
+            }
+          } else {
+            for (int j = 0; j < 64 && n0 + c + j < N; ++j)
+              if (!(__bfloat162float(mrow[j]) > 0.0f)) v[j] = 0.0f;
+          }
+        }
+        // staging buffer reuse: the TMA store issued two chunks ago must have read it
+        if (lane == 0) tma_store_wait_read<1>();
+        __syncwarp();
+        uint8_t* sbuf = stage_buf + buf * kEpiChunkBytes + lane * 128;
+        if (ep.out_f32) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint4 o = make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                                       __float_as_uint(v[4 * j + 2]),
+                                       __float_as_uint(v[4 * j + 3]));
+            *reinterpret_cast<uint4*>(sbuf + ((j ^ (lane & 7)) << 4)) = o;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint4 o;
+            o.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
+            o.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
+            o.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
+            o.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
+            *reinterpret_cast<uint4*>(sbuf + ((j ^ (lane & 7)) << 4)) = o;
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmap_c, stage_buf + buf * kEpiChunkBytes, n0 + c, row0);
+          tma_store_commit();
+        }
+        buf ^= 1;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(&tempty_bar[acc], 0);
+    }
+    if (lane == 0) tma_store_wait<0>();
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2sm<C::kTmemCols>(tmem_base);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -278,18 +585,26 @@ EncodeTiledFn encode_fn() {
 
 // Row-major bf16 matrix [rows][cols] with leading dimension ld (elements); box = 64 cols x
 // box_rows rows, 128-byte swizzle.
-int make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
-              uint32_t box_rows) {
+int make_tmap_t(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                uint32_t box_cols, uint32_t box_rows, bool f32) {
   auto fn = encode_fn();
   if (!fn) return EDL_ECUDA;
+  const uint64_t esz = f32 ? 4 : 2;
   cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {ld * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint64_t strides[1] = {ld * esz};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult r = fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? EDL_OK : EDL_ECUDA;
+}
+
+// Row-major bf16 operand [rows][cols]: box = 64 cols (one 128-byte swizzle row) x box_rows.
+int make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+              uint32_t box_rows) {
+  return make_tmap_t(m, base, rows, cols, ld, 64, box_rows, false);
 }
 
 int num_sms() {
@@ -321,7 +636,43 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
   return EDL_OK;
 }
 
+template <int BN, bool A_MN, bool B_MN>
+int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream) {
+  using Cf = Cfg2<BN>;
+  auto kern = gemm_bf16_2sm_kernel<BN, A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    EDL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Cf::kSmemBytes));
+    attr_set = true;
+  }
+  const int tiles = ((p.M + 255) / 256) * ((p.N + BN - 1) / BN);
+  const int pairs = num_sms() / 2;
+  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  kern<<<grid, kThreads, Cf::kSmemBytes, stream>>>(p.ta, p.tb, p.tc, p.M, p.N, p.K, p.ep);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
+
 }  // namespace
+
+// CTA-pair N tile: fill the 74 TPCs evenly, preferring wide tiles (less smem traffic/MAC).
+int gemm_pick_bn_2sm(int M, int N) {
+  const int pairs = num_sms() / 2;
+  int best = 128;
+  double best_eff = -1;
+  for (int bn : {256, 192, 128}) {
+    const long tiles = static_cast<long>((M + 255) / 256) * ((N + bn - 1) / bn);
+    const long waves = (tiles + pairs - 1) / pairs;
+    const double eff = static_cast<double>(M) * N / (static_cast<double>(waves) * pairs * 256 * bn) *
+                       (bn == 256 ? 1.0 : bn == 192 ? 0.97 : 0.93);
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = bn;
+    }
+  }
+  return best;
+}
 
 // Picks the N tile so the output-tile count fills the 148 SMs as evenly as possible.
 int gemm_pick_bn(int M, int N, bool b_mn) {
@@ -350,7 +701,38 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B,
                    const void* mask, int ldm, int bn) {
   if (M <= 0 || N <= 0 || K <= 0) return fail(EDL_EINVAL, "gemm: empty shape");
   if ((lda * 2) % 16 || (ldb * 2) % 16) return fail(EDL_EINVAL, "gemm: 16-byte row alignment");
-  if (bn <= 0) bn = gemm_pick_bn(M, N, b_mn != 0);
+  // bn: 0 = auto, 1..256 = 1-SM kernel with that N tile, 1000 + x = CTA-pair kernel, N tile x
+  int cg = 1;
+  if (bn >= 1000) {
+    cg = 2;
+    bn -= 1000;
+  } else if (bn <= 0) {
+    if (M >= 256 && (ldc * (out_f32 ? 4 : 2)) % 16 == 0) {
+      cg = 2;
+      bn = gemm_pick_bn_2sm(M, N);
+    } else {
+      bn = gemm_pick_bn(M, N, b_mn != 0);
+    }
+  }
+  p->cg = cg;
+  if (cg == 2) {
+    if (bn != 128 && bn != 192 && bn != 256) return fail(EDL_EINVAL, "gemm: 2-SM N tile");
+    int rc = a_mn ? make_tmap(&p->ta, A, K, M, lda, 64) : make_tmap(&p->ta, A, M, K, lda, 128);
+    if (rc) return fail(rc, "gemm: tensor map A");
+    rc = b_mn ? make_tmap(&p->tb, B, K, N, ldb, 64) : make_tmap(&p->tb, B, N, K, ldb, bn / 2);
+    if (rc) return fail(rc, "gemm: tensor map B");
+    rc = make_tmap_t(&p->tc, Cout, M, N, ldc, out_f32 ? 32 : 64, 32, out_f32 != 0);
+    if (rc) return fail(rc, "gemm: tensor map C");
+    if (mask && out_f32) return fail(EDL_EINVAL, "gemm: mask needs a bf16 output");
+    p->M = M;
+    p->N = N;
+    p->K = K;
+    p->a_mn = a_mn;
+    p->b_mn = b_mn;
+    p->bn = bn;
+    p->ep = EpiParams{Cout, static_cast<const __nv_bfloat16*>(mask), ldc, ldm, relu, out_f32};
+    return EDL_OK;
+  }
   int rc = a_mn ? make_tmap(&p->ta, A, K, M, lda, 64) : make_tmap(&p->ta, A, M, K, lda, BM);
   if (rc) return fail(rc, "gemm: tensor map A");
   rc = b_mn ? make_tmap(&p->tb, B, K, N, ldb, 64) : make_tmap(&p->tb, B, N, K, ldb, bn);
@@ -367,6 +749,22 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B,
 
 int gemm_plan_run(const GemmPlan& p, cudaStream_t stream) {
   const int a_mn = p.a_mn, b_mn = p.b_mn;
+  if (p.cg == 2) {
+#define EDL_GEMM2_CASE(BNV)                                                          \
+  case BNV:                                                                          \
+    if (!a_mn && !b_mn) return launch_gemm_2sm<BNV, false, false>(p, stream);        \
+    if (!a_mn && b_mn) return launch_gemm_2sm<BNV, false, true>(p, stream);          \
+    if (a_mn && !b_mn) return launch_gemm_2sm<BNV, true, false>(p, stream);          \
+    return launch_gemm_2sm<BNV, true, true>(p, stream);
+    switch (p.bn) {
+      EDL_GEMM2_CASE(128)
+      EDL_GEMM2_CASE(192)
+      EDL_GEMM2_CASE(256)
+      default:
+        return fail(EDL_EINVAL, "gemm: unsupported 2-SM N tile");
+    }
+#undef EDL_GEMM2_CASE
+  }
 #define EDL_GEMM_CASE(BNV)                                                                  \
   case BNV:                                                                                 \
     if (!a_mn && !b_mn) return launch_gemm<BNV, false, false>(p.ta, p.tb, p.M, p.N, p.K, p.ep, stream); \
@@ -399,3 +797,15 @@ int gemm_bf16(const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn
 }
 
 }  // namespace edl
+
+#ifdef EDL_GEMM_TRACE
+extern "C" int edl_debug_gemm_trace(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, edl::g_gemm_trace, sizeof(edl::g_gemm_trace));
+  if (reset) {
+    static unsigned long long zero[296][8];
+    cudaMemcpyToSymbol(edl::g_gemm_trace, zero, sizeof(zero));
+  }
+  return 0;
+}
+#endif

@@ -1,0 +1,32 @@
+import ctypes as C, sys, os, torch
+sys.path.insert(0, '.')
+from paper_1909_11985_b200 import _lib
+L = _lib.lib()
+tag = os.environ.get("EDL_LIB_PATH", "default").split('/')[-2]
+def timed(fn, it=40):
+    for _ in range(3): fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(it): fn()
+    g.replay(); torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / it
+def bench(a_mn, b_mn, M, N, K, bn):
+    A = (torch.randn(K, M) if a_mn else torch.randn(M, K)).to(torch.bfloat16).cuda()
+    B = (torch.randn(K, N) if b_mn else torch.randn(N, K)).to(torch.bfloat16).cuda()
+    out = torch.empty(M, N, dtype=torch.bfloat16, device='cuda')
+    args = (A.data_ptr(), A.shape[1], a_mn, B.data_ptr(), B.shape[1], b_mn, out.data_ptr(), N, M, N, K, 0, 0, None, 0, bn)
+    us = timed(lambda: L.edl_gemm_bf16(*args, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    real = bn - 1000 if bn >= 1000 else bn
+    bm = 256 if bn >= 1000 else 128
+    tiles = ((M+bm-1)//bm)*((N+real-1)//real); sms = min(tiles*(2 if bn>=1000 else 1), 148)
+    mac_clk = M*N*K/(us*1e-6)/sms/1.965e9
+    print(f"[{tag}] a{a_mn}b{b_mn} M={M} N={N} K={K} bn={bn} sms={sms}: {us:.1f} us {2*M*N*K/us/1e6:.0f} TF/s per-SM {100*mac_clk/4096:.0f}%", flush=True)
+for bn in (1128, 1256):
+    bench(0, 0, 512, 4096, 4096, bn)
+    bench(0, 0, 512, 4096, 16384, bn)
+    bench(0, 0, 1024, 4096, 4096, bn)
+bench(1, 1, 4096, 4096, 512, 1256)
+bench(1, 1, 4096, 4096, 2048, 1256)

@@ -28,10 +28,15 @@ def _ref(A, a_mn, B, b_mn):
     return a @ b
 
 
+# bn: 0 = auto (CTA-pair kernel when M >= 256), 1..256 = 1-SM kernel with that N tile,
+# 1000 + x = CTA-pair (cta_group::2) kernel with N tile x
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("M,N,K,bn", [(128, 128, 64, 128), (256, 256, 512, 0),
                                       (512, 4096, 4096, 0), (512, 4096, 4096, 128),
-                                      (384, 448, 320, 112), (4096, 1024, 512, 256)])
+                                      (384, 448, 320, 112), (4096, 1024, 512, 256),
+                                      (256, 256, 128, 1128), (512, 512, 256, 1256),
+                                      (384, 320, 200, 1192), (4096, 1024, 512, 1128),
+                                      (512, 4096, 4096, 1256)])
 def test_gemm_layouts(a_mn, b_mn, M, N, K, bn):
     torch.manual_seed(0)
     A = (torch.randn(K, M) if a_mn else torch.randn(M, K)).to(torch.bfloat16).cuda()
@@ -43,12 +48,13 @@ def test_gemm_layouts(a_mn, b_mn, M, N, K, bn):
     assert err <= 1e-3 * scale + 1e-3, (err, scale)
 
 
-def test_gemm_relu_mask_bf16():
+@pytest.mark.parametrize("bn", [0, 128, 1128, 1256])
+def test_gemm_relu_mask_bf16(bn):
     torch.manual_seed(1)
     M, N, K = 512, 1024, 768
     A = torch.randn(M, K).to(torch.bfloat16).cuda()
     B = torch.randn(N, K).to(torch.bfloat16).cuda()
     mask = torch.randn(M, N).to(torch.bfloat16).cuda()
-    out = _gemm(A, 0, B, 0, M, N, K, relu=1, mask=mask)
+    out = _gemm(A, 0, B, 0, M, N, K, relu=1, mask=mask, bn=bn)
     ref = torch.relu(_ref(A, 0, B, 0)) * (mask.float() > 0)
     assert torch.allclose(out.float(), ref.bfloat16().float(), rtol=2e-2, atol=2e-1)
