@@ -276,6 +276,13 @@ void edl_job_set_profile(EdlJob* job, int32_t on);
 void edl_job_counters(const EdlJob* job, double* phase_ms, uint64_t* steps, uint64_t* launches);
 void edl_job_reset_counters(EdlJob* job);
 
+/* Weight-gradient GEMM with sgd_step (trainer.cpp:56-61) fused into its epilogue, for a job
+ * with a single replica: dW[M][N] = dy^T x (dy row-major [K][ld_dy], x row-major [K][ld_x]),
+ * then master -= scale * bf16(dW) and W (bf16) <- master.  No gradient buffer is written. */
+int edl_gemm_wgrad_sgd(const void* dy, int32_t ld_dy, const void* x, int32_t ld_x,
+                       float* master, void* W, int32_t ldw, int32_t M, int32_t N, int32_t K,
+                       float scale, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -154,6 +154,7 @@ def _declare(L: C.CDLL) -> None:
         "edl_job_set_profile": ([vp, i32], None),
         "edl_job_counters": ([vp, P(f64), P(u64), P(u64)], None),
         "edl_job_reset_counters": ([vp], None),
+        "edl_gemm_wgrad_sgd": ([vp, i32, vp, i32, vp, vp, i32, i32, i32, i32, C.c_float, vp], ci),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)  # AttributeError = the library lacks a declared entry point

@@ -30,17 +30,26 @@ struct EpiParams {
   int ldm;
   int relu;     // apply max(0, x)
   int out_f32;  // store fp32 instead of bf16
+  // fused SGD epilogue (weight-gradient GEMM): master[M][N] -= scale * bf16(acc);
+  // C (bf16) <- master.  Set per launch by gemm_plan_run(plan, stream, scale).
+  int sgd;
+  float scale;
 };
 // Pre-encoded launch (TMA descriptors built once; launching costs one kernel launch).
 struct GemmPlan {
-  CUtensorMap ta, tb, tc;
+  CUtensorMap ta, tb, tc, tm;  // tm: fp32 master (fused-SGD plans)
   int M = 0, N = 0, K = 0, a_mn = 0, b_mn = 0, bn = 0, cg = 1;
   EpiParams ep{};
 };
 int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B, int ldb,
                    int b_mn, void* C, int ldc, int M, int N, int K, int relu, int out_f32,
                    const void* mask, int ldm, int bn);
-int gemm_plan_run(const GemmPlan& p, cudaStream_t stream);
+int gemm_plan_run(const GemmPlan& p, cudaStream_t stream, float sgd_scale = 0.f);
+// Weight-gradient GEMM with the SGD step fused into its epilogue (CTA-pair kernel, one
+// replica): dW = A^T-major x B^T-major as for wgrad, then master -= scale * bf16(dW) and
+// W (bf16) <- master, with no gradient buffer round trip through HBM.
+int gemm_plan_init_sgd(GemmPlan* p, const void* A, int lda, int a_mn, const void* B, int ldb,
+                       int b_mn, float* master, __nv_bfloat16* W, int ldw, int M, int N, int K);
 int gemm_pick_bn(int M, int N, bool b_mn);
 int gemm_bf16(const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
               int ldc, int M, int N, int K, int relu, int out_f32, const void* mask, int ldm,

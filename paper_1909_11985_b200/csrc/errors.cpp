@@ -43,3 +43,13 @@ int edl_gemm_bf16(const void* A, int32_t lda, int32_t a_mn, const void* B, int32
 }
 
 }  // extern "C"
+
+extern "C" int edl_gemm_wgrad_sgd(const void* dy, int32_t ld_dy, const void* x, int32_t ld_x,
+                                  float* master, void* W, int32_t ldw, int32_t M, int32_t N,
+                                  int32_t K, float scale, void* stream) {
+  edl::GemmPlan p;
+  int rc = edl::gemm_plan_init_sgd(&p, dy, ld_dy, 1, x, ld_x, 1, master,
+                                   static_cast<__nv_bfloat16*>(W), ldw, M, N, K);
+  if (rc) return rc;
+  return edl::gemm_plan_run(p, static_cast<cudaStream_t>(stream), scale);
+}

@@ -288,7 +288,7 @@ __device__ unsigned long long g_gemm_trace[296][8];
 #define TRACE_ADD(slot, t0)
 #endif
 
-template <int BN>
+template <int BN, bool kSgd = false>
 struct Cfg2 {
   static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "2-SM tiles: BN multiple of 64");
   static constexpr int kHalfN = BN / 2;
@@ -298,7 +298,11 @@ struct Cfg2 {
   static constexpr uint32_t kBBytesMN = kBBoxesMN * kMnBlockBytes;
   static constexpr uint32_t kBSlot = kBBytesK > kBBytesMN ? kBBytesK : kBBytesMN;
   static constexpr uint32_t kStageBytes = kABytes + ((kBSlot + 1023) / 1024) * 1024;
-  static constexpr uint32_t kEpiBytes = 4 * 2 * kEpiChunkBytes;         // 4 warps x 2 buffers
+  // epilogue staging per warp x 2 buffers: plain 4 KB; fused SGD 8 KB master + 4 KB bf16 W
+  static constexpr uint32_t kSgdBufBytes = 3 * kEpiChunkBytes;
+  static constexpr int kSgdBufs = 2;  // master prefetch distance: 1 chunk per warp
+  static constexpr uint32_t kEpiBytes =
+      kSgd ? 4 * kSgdBufs * kSgdBufBytes : 4 * 2 * kEpiChunkBytes;
 #ifndef EDL_GEMM2_MAX_STAGES
 #define EDL_GEMM2_MAX_STAGES 6
 #endif
@@ -309,16 +313,17 @@ struct Cfg2 {
   static constexpr int kSplit = 1;
   static constexpr uint32_t kAccCols = BN * kSplit;
   static constexpr uint32_t kTmemCols = (2 * kAccCols <= 256) ? 256 : 512;
-  static constexpr uint32_t kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 256;
+  static constexpr uint32_t kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 512;
 };
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool kSgd>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                          const __grid_constant__ CUtensorMap tmap_b,
-                         const __grid_constant__ CUtensorMap tmap_c, int M, int N, int K,
+                         const __grid_constant__ CUtensorMap tmap_c,
+                         const __grid_constant__ CUtensorMap tmap_m, int M, int N, int K,
                          EpiParams ep) {
-  using C = Cfg2<BN>;
+  using C = Cfg2<BN, kSgd>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -327,7 +332,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* tfull_bar = empty_bar + C::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* sgd_bar = tempty_bar + 2;  // fused SGD: master-load barriers per epilogue warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgd_bar + 16);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -351,6 +357,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 8);  // lane 0 of the 4 epilogue warps of both CTAs
     }
+    for (int a = 0; a < 16; ++a) mbar_init(&sgd_bar[a], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_2sm<C::kTmemCols>(tmem_slot);
@@ -452,6 +459,121 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       TRACE_ADD(2, t_mma);
     }
+  } else if (kSgd) {
+    // ------------------------------------------------------------ fused SGD epilogue
+    // Per warp (32 rows of the CTA's 128) and 64-column chunk: TMA-load the fp32 master
+    // chunk (prefetched one chunk ahead, across tiles), fold master -= scale * bf16(acc) in
+    // place in swizzled smem, then TMA-store master and the bf16 working weights.
+    // HBM per parameter: 4 B master read + 4 B master write + 2 B weight write.
+    const int q = warp & 3;
+    constexpr int kChunks = BN / 64;
+    constexpr int NB = C::kSgdBufs;
+    uint8_t* wbase = epi + q * NB * C::kSgdBufBytes;
+    uint64_t* mb = sgd_bar + q * NB;
+    auto coords = [&](int j, int* r0, int* c0) -> bool {
+      const int t = pair + (j / kChunks) * n_pairs;
+      if (t >= num_tiles) return false;
+      *r0 = (t % m_tiles) * 256 + static_cast<int>(rank) * 128 + q * 32;
+      *c0 = (t / m_tiles) * BN + (j % kChunks) * 64;
+      return true;
+    };
+    auto prefetch = [&](int j) {
+      int r0, c0;
+      if (!coords(j, &r0, &c0)) return;
+      uint8_t* dst = wbase + (j % NB) * C::kSgdBufBytes;
+      mbar_arrive_expect_tx(&mb[j % NB], 2 * kEpiChunkBytes);
+      tma_load_2d(dst, &tmap_m, &mb[j % NB], c0, r0);
+      tma_load_2d(dst + kEpiChunkBytes, &tmap_m, &mb[j % NB], c0 + 32, r0);
+    };
+    if (lane == 0)
+      for (int p0 = 0; p0 < NB - 1; ++p0) prefetch(p0);
+    int j = 0;
+    int local = 0;
+    TRACE_T0(t_epi);
+    for (int tile = pair; tile < num_tiles; tile += n_pairs, ++local) {
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      TRACE_T0(t_tf);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      if (lane == 0) TRACE_ADD(5, t_tf);
+      tc_fence_after();
+      const uint32_t t_row =
+          tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::kAccCols;
+#pragma unroll 1
+      for (int cc = 0; cc < kChunks; ++cc, ++j) {
+        const int b = j % NB;
+        if (lane == 0) {
+          TRACE_T0(t_wr);
+          tma_store_wait_read<0>();  // chunk j-1's stores have read the buffer refilled next
+          TRACE_ADD(6, t_wr);
+          prefetch(j + NB - 1);
+        }
+        float g[64];
+        {
+          uint32_t r[32];
+          tmem_ld32(t_row + cc * 64, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) g[e] = __uint_as_float(r[e]);
+          tmem_ld32(t_row + cc * 64 + 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) g[32 + e] = __uint_as_float(r[e]);
+        }
+        // same numerics as the unfused path: the gradient is rounded to bf16 first
+#pragma unroll
+        for (int e = 0; e < 64; ++e) g[e] = __bfloat162float(__float2bfloat16_rn(g[e]));
+        TRACE_T0(t_ml);
+        mbar_wait(&mb[b], (j / NB) & 1);
+        if (lane == 0) TRACE_ADD(7, t_ml);
+        uint8_t* buf = wbase + b * C::kSgdBufBytes;
+        uint8_t* wrow = buf + 2 * kEpiChunkBytes + lane * 128;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint8_t* mrow = buf + h * kEpiChunkBytes + lane * 128;
+#pragma unroll
+          for (int k4 = 0; k4 < 8; ++k4) {
+            float4* pm = reinterpret_cast<float4*>(mrow + ((k4 ^ (lane & 7)) << 4));
+            float4 m = *pm;
+            const float* gg = &g[h * 32 + k4 * 4];
+            m.x = __fsub_rn(m.x, __fmul_rn(ep.scale, gg[0]));
+            m.y = __fsub_rn(m.y, __fmul_rn(ep.scale, gg[1]));
+            m.z = __fsub_rn(m.z, __fmul_rn(ep.scale, gg[2]));
+            m.w = __fsub_rn(m.w, __fmul_rn(ep.scale, gg[3]));
+            *pm = m;
+            g[h * 32 + k4 * 4 + 0] = m.x;  // reuse g for the new weights
+            g[h * 32 + k4 * 4 + 1] = m.y;
+            g[h * 32 + k4 * 4 + 2] = m.z;
+            g[h * 32 + k4 * 4 + 3] = m.w;
+          }
+        }
+#pragma unroll
+        for (int j8 = 0; j8 < 8; ++j8) {
+          uint4 o;
+          o.x = pack_bf16(g[8 * j8 + 0], g[8 * j8 + 1]);
+          o.y = pack_bf16(g[8 * j8 + 2], g[8 * j8 + 3]);
+          o.z = pack_bf16(g[8 * j8 + 4], g[8 * j8 + 5]);
+          o.w = pack_bf16(g[8 * j8 + 6], g[8 * j8 + 7]);
+          *reinterpret_cast<uint4*>(wrow + ((j8 ^ (lane & 7)) << 4)) = o;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          int r0, c0;
+          coords(j, &r0, &c0);
+          tma_store_2d(&tmap_m, buf, c0, r0);
+          tma_store_2d(&tmap_m, buf + kEpiChunkBytes, c0 + 32, r0);
+          tma_store_2d(&tmap_c, buf + 2 * kEpiChunkBytes, c0, r0);
+          tma_store_commit();
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(&tempty_bar[acc], 0);
+    }
+    if (lane == 0) tma_store_wait<0>();
+    if (lane == 0) TRACE_ADD(4, t_epi);  // note: slot 4 shared with producer total
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int q = warp & 3;  // TMEM lane quarter
@@ -636,10 +758,10 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
   return EDL_OK;
 }
 
-template <int BN, bool A_MN, bool B_MN>
-int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream) {
-  using Cf = Cfg2<BN>;
-  auto kern = gemm_bf16_2sm_kernel<BN, A_MN, B_MN>;
+template <int BN, bool A_MN, bool B_MN, bool kSgd = false>
+int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream, float scale = 0.f) {
+  using Cf = Cfg2<BN, kSgd>;
+  auto kern = gemm_bf16_2sm_kernel<BN, A_MN, B_MN, kSgd>;
   static bool attr_set = false;
   if (!attr_set) {
     EDL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -649,7 +771,9 @@ int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream) {
   const int tiles = ((p.M + 255) / 256) * ((p.N + BN - 1) / BN);
   const int pairs = num_sms() / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
-  kern<<<grid, kThreads, Cf::kSmemBytes, stream>>>(p.ta, p.tb, p.tc, p.M, p.N, p.K, p.ep);
+  EpiParams ep = p.ep;
+  ep.scale = scale;
+  kern<<<grid, kThreads, Cf::kSmemBytes, stream>>>(p.ta, p.tb, p.tc, p.tm, p.M, p.N, p.K, ep);
   EDL_CUDA_TRY(cudaGetLastError());
   return EDL_OK;
 }
@@ -730,7 +854,8 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B,
     p->a_mn = a_mn;
     p->b_mn = b_mn;
     p->bn = bn;
-    p->ep = EpiParams{Cout, static_cast<const __nv_bfloat16*>(mask), ldc, ldm, relu, out_f32};
+    p->ep = EpiParams{Cout, static_cast<const __nv_bfloat16*>(mask), ldc, ldm, relu, out_f32, 0, 0.f};
+    p->tm = p->tc;
     return EDL_OK;
   }
   int rc = a_mn ? make_tmap(&p->ta, A, K, M, lda, 64) : make_tmap(&p->ta, A, M, K, lda, BM);
@@ -743,12 +868,30 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B,
   p->a_mn = a_mn;
   p->b_mn = b_mn;
   p->bn = bn;
-  p->ep = EpiParams{Cout, static_cast<const __nv_bfloat16*>(mask), ldc, ldm, relu, out_f32};
+  p->ep = EpiParams{Cout, static_cast<const __nv_bfloat16*>(mask), ldc, ldm, relu, out_f32, 0, 0.f};
   return EDL_OK;
 }
 
-int gemm_plan_run(const GemmPlan& p, cudaStream_t stream) {
+int gemm_plan_init_sgd(GemmPlan* p, const void* A, int lda, int a_mn, const void* B, int ldb,
+                       int b_mn, float* master, __nv_bfloat16* W, int ldw, int M, int N, int K) {
+  if (!a_mn || !b_mn) return fail(EDL_EINVAL, "fused SGD: weight-gradient layout (MN-major A/B)");
+  if (M <= 0 || N <= 0 || K <= 0 || (ldw * 2) % 16) return fail(EDL_EINVAL, "fused SGD: shape");
+  int rc = gemm_plan_init(p, A, lda, a_mn, B, ldb, b_mn, W, ldw, M, N, K, 0, 0, nullptr, 0,
+                          1000 + 128);
+  if (rc) return rc;
+  rc = make_tmap_t(&p->tm, master, M, N, ldw, 32, 32, true);
+  if (rc) return fail(rc, "fused SGD: tensor map master");
+  p->ep.sgd = 1;
+  return EDL_OK;
+}
+
+int gemm_plan_run(const GemmPlan& p, cudaStream_t stream, float sgd_scale) {
   const int a_mn = p.a_mn, b_mn = p.b_mn;
+  if (p.ep.sgd) {
+    if (p.cg != 2 || p.bn != 128 || !a_mn || !b_mn)
+      return fail(EDL_EINVAL, "gemm: fused SGD plans are CTA-pair, N tile 128, MN-major A/B");
+    return launch_gemm_2sm<128, true, true, true>(p, stream, sgd_scale);
+  }
   if (p.cg == 2) {
 #define EDL_GEMM2_CASE(BNV)                                                          \
   case BNV:                                                                          \

@@ -397,6 +397,17 @@ int Job::ensure_plans(Worker* w, int64_t rows) {
     }
     w->plan_rows = rows;
   }
+  if (fused_update_ && w->sgd_plan_rows != rows) {
+    w->wgrad_sgd.assign(static_cast<size_t>(L_), GemmPlan{});
+    for (int l = 0; l < L_; ++l) {
+      const bool last = l == L_ - 1;
+      const __nv_bfloat16* dy = last ? r->dlog : r->dx[(l + 1) & 1];
+      EDL_TRY(gemm_plan_init_sgd(&w->wgrad_sgd[l], dy, out_[l], 1, r->act[l], in_[l], 1,
+                                 r->master + off_[l], r->W + off_[l], in_[l], out_[l], in_[l],
+                                 static_cast<int>(rows)));
+    }
+    w->sgd_plan_rows = rows;
+  }
   return EDL_OK;
 }
 
@@ -449,7 +460,10 @@ int Job::run_worker_mlp(Worker* w, int slot) {
   m = mark(slot, 2, m, r->stream);
   for (int l = L_ - 1; l >= 0; --l) {
     if (l > 0) EDL_TRY(gemm_plan_run(r->dgrad[l], r->stream));
-    EDL_TRY(gemm_plan_run(w->wgrad[l], r->stream));
+    if (fused_update_)
+      EDL_TRY(gemm_plan_run(w->wgrad_sgd[l], r->stream, step_scale_));  // dW + sgd_step
+    else
+      EDL_TRY(gemm_plan_run(w->wgrad[l], r->stream));
   }
   m = mark(slot, 3, m, r->stream);
   (void)m;
@@ -488,7 +502,7 @@ int Job::reduce_and_update(uint64_t count, uint64_t t, int slot) {
   if (mlp_) {
     std::vector<const __nv_bfloat16*> grads;
     for (const auto& id : ring_) grads.push_back(workers_[id]->grad);
-    if (count > 0) {
+    if (count > 0 && !fused_update_) {
       __nv_bfloat16* wdst[1] = {r->W};
       EDL_TRY(sgd_update_bf16(grads.data(), static_cast<int>(grads.size()), r->master, r->mom,
                               wdst, 1, P_, static_cast<float>(eta_t / static_cast<double>(count)),
@@ -604,6 +618,12 @@ int Job::step(EdlStepReport* out) {
     }
     w->n_runs = n;
   }
+
+  // one ring member, plain SGD: no collective, the update runs inside the wgrad GEMMs
+  fused_update_ = mlp_ && ring_.size() == 1 && cfg_.momentum == 0.0 && reps_.size() == 1;
+  if (count > 0)
+    step_scale_ = static_cast<float>(
+        cfg_.eta / (1.0 + cfg_.decay * static_cast<double>(t_)) / static_cast<double>(count));
 
   // device work
   EDL_CUDA_TRY(cudaEventRecord(r->ev_begin[slot], r->stream));

@@ -79,7 +79,9 @@ struct Worker {
   EdlRun* runs_host = nullptr;  // pinned [kSlots][runs_cap]
   int64_t runs_cap = 0;
   std::vector<GemmPlan> wgrad;
+  std::vector<GemmPlan> wgrad_sgd;  // fused weight-gradient + SGD (single-member ring)
   int64_t plan_rows = -1;
+  int64_t sgd_plan_rows = -1;
   Cursor cur;
   // current step
   std::vector<std::pair<uint64_t, uint64_t>> plan;
@@ -152,6 +154,10 @@ class Job {
 
   EdlJobConfig cfg_{};
   bool mlp_ = false;
+  // Single ring member + plain SGD: the update is fused into the weight-gradient GEMMs
+  // (there is nothing to all-reduce); set per step.
+  bool fused_update_ = false;
+  float step_scale_ = 0.f;
   int L_ = 0;
   std::vector<int> in_, out_;
   std::vector<size_t> off_;
