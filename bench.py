@@ -144,49 +144,77 @@ def run_b200(args, rank: int, world: int) -> None:
     import torch
     from paper_1909_11985_b200 import runtime as rt
 
+    dist = None
     if world > 1:
-        raise SystemExit("bench.py: multi-process data parallelism is built in "
-                         "paper_1909_11985_b200.dist (not yet wired into bench.py)")
-    dev = 0
-    torch.cuda.set_device(dev)
+        # plumbing only (handle exchange, barriers, max-over-ranks timing); the gradient
+        # exchange itself is the fused NVLink peer-memory kernel, not a library collective
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
     w = WORKLOAD
     cfg = rt.JobConfig(model=rt.MLP, size=w["size"], dim=w["dim"], seed=1, noise=0.0,
                        num_classes=w["classes"], layers=w["layers"], hidden=w["hidden"],
                        eta=0.05, decay=0.0, batch=w["batch"], per_worker_batch=w["batch"],
-                       lease_seed=7, partitions=64, max_workers=max(1, world), init_seed=0,
+                       lease_seed=7, partitions=0, max_workers=max(1, world), init_seed=0,
                        keep_log=False)
-    job = rt.Job(cfg, [f"w{rank:02d}"], [dev])
+    ring = [f"w{r:02d}" for r in range(world)]
+    job = rt.Job(cfg, ring, [local if r == rank else -1 for r in range(world)])
+    if dist is not None:
+        blobs = [None] * world
+        dist.all_gather_object(blobs, job.export_handles())
+        for r, b in enumerate(blobs):
+            if r != rank:
+                job.import_handles(b)
+        dist.barrier()
     stream = torch.cuda.ExternalStream(job.stream_handle())
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     for _ in range(args.warmup):
         job.step()
     job.sync()
+    barrier()
 
     flops, P = flops_per_sample()
     # ---- value: K pipelined steps (inputs HBM-resident), device-timed on the job stream
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clk:
+    with ClockSampler(local) as clk:
         # keep the GPU under the same load around the (short) timed region so the 200 ms
         # clock samples see it: untimed steps for >= 1 s before and 0.5 s after
         t_load = time.time()
-        while time.time() - t_load < 1.0:
+        n_pre = 0
+        while max_over_ranks(time.time() - t_load) < 1.0:
             for _ in range(20):
                 job.step()
             job.sync()
+            n_pre += 1
         job.set_profile(True)
         job.reset_counters()
-        torch.cuda.synchronize()
+        barrier()
         e0.record(stream)
         for _ in range(args.steps):
             job.step()
         e1.record(stream)
         torch.cuda.synchronize()
         job.set_profile(False)
+        barrier()
         t_load = time.time()
-        while time.time() - t_load < 0.5:
+        while max_over_ranks(time.time() - t_load) < 0.5:
             for _ in range(20):
                 job.step()
             job.sync()
-    ms = e0.elapsed_time(e1)
+    ms = max_over_ranks(e0.elapsed_time(e1))
     counters = job.counters()
     clocks = clk.summary()
     samples = w["batch"] * args.steps * world
@@ -197,16 +225,26 @@ def run_b200(args, rank: int, world: int) -> None:
     gemm_ms = (ph["forward"] + ph["backward"]) / n
     upd_ms = ph["update"] / n
     gemm_tflops = flops * w["batch"] / (gemm_ms / 1e3) / 1e12
-    upd_bytes = 12 * P  # bf16 grad read + fp32 master read/write + bf16 weight write
-    upd_gbs = upd_bytes / (upd_ms / 1e3) / 1e9
     peaks = measured_peaks()
     peak_t = peaks.get("bf16_tflops_sustained", 1354.1)
     peak_h = peaks.get("hbm_gbs", 6555.5)
+    if world == 1:
+        # update fused into the weight-gradient GEMM epilogues: 4 B master read + 4 B
+        # master write + 2 B bf16 weight write per parameter, inside the backward phase
+        upd = {"bound": "hbm", "where": "fused into wgrad GEMM epilogue (backward phase)",
+               "bytes_per_step": 10 * P}
+    else:
+        nv = 2.0 * (world - 1) / world * 2 * P  # bf16 RS + AG bytes per GPU per direction
+        upd = {"bound": "nvlink", "achieved": nv / (upd_ms / 1e3) / 1e9, "peak": 770.0,
+               "unit": "GB/s", "frac": nv / (upd_ms / 1e3) / 1e9 / 770.0,
+               "bytes_per_step": nv, "per_step_ms": upd_ms,
+               "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction",
+               "kernel": "fused reduce-scatter + sharded SGD + all-gather over NVLink P2P"}
 
     # ---- e2e: every step through the public API with a D2H read of its loss
     job.reset_counters()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
+    barrier()
     e2.record(stream)
     losses = []
     for _ in range(args.steps):
@@ -214,14 +252,14 @@ def run_b200(args, rank: int, world: int) -> None:
         losses.append(job.sync().loss)
     e3.record(stream)
     torch.cuda.synchronize()
-    ms_e2e = e2.elapsed_time(e3)
+    ms_e2e = max_over_ranks(e2.elapsed_time(e3))
     e2e_value = samples / (ms_e2e / 1e3)
-    runs_per_step = 2  # a 512-sample batch spans <= 2 shards of 16384 samples
+    runs_per_step = 2  # a 512-sample batch spans <= 2 shards of >= 4096 samples
     launches = counters["launches"]
 
-    # ---- CPU baseline (oracle port), bounded sample on this host
+    # ---- CPU baseline (oracle port), bounded sample on this host, rank 0 at N=1 only
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         batch = int(os.environ.get("EDL_CPU_BATCH", "64"))
         t = cpu_reference_step(batch, 2)
         cpu = {"value": batch / min(t), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
@@ -234,22 +272,23 @@ def run_b200(args, rank: int, world: int) -> None:
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (HBM-resident 2^20 x 4096 bf16 splitmix64 dataset, random-init MLP)",
         "config": {"workload": "mlp4096x8_bf16_b512_sgd", "layers": w["layers"],
-                   "width": w["hidden"], "classes": w["classes"], "global_batch": samples // args.steps,
-                   "per_gpu_batch": w["batch"], "dataset_samples": w["size"],
-                   "parallelism": f"dp{world}", "optimizer": "sgd(eta=0.05), fp32 master",
+                   "width": w["hidden"], "classes": w["classes"],
+                   "global_batch": samples // args.steps, "per_gpu_batch": w["batch"],
+                   "dataset_samples": w["size"], "parallelism": f"dp{world}",
+                   "optimizer": "sgd(eta=0.05), fp32 master",
                    "l2": "inputs > L2 (weights 268 MB + fp32 master 537 MB streamed per step)"},
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": 16 * runs_per_step, "d2h_bytes_per_step": 8,
-                "note": "job.step()+job.sync() per step: host lease draws, H2D lease runs, D2H loss"},
+                "note": "job.step()+job.sync() per step: host lease draws, H2D lease runs, "
+                        "D2H loss"},
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMMs (8 fwd + 7 dgrad + 8 wgrad)",
                      "achieved": gemm_tflops, "peak": peak_t, "unit": "TFLOP/s",
                      "frac": gemm_tflops / peak_t, "traffic": None,
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
-                     "per_step_ms": gemm_ms, "algorithmic_gflop_per_step": flops * w["batch"] / 1e9},
-        "update_roofline": {"bound": "hbm", "achieved": upd_gbs, "peak": peak_h, "unit": "GB/s",
-                            "frac": upd_gbs / peak_h, "bytes_per_step": upd_bytes,
-                            "per_step_ms": upd_ms},
+                     "per_step_ms": gemm_ms,
+                     "algorithmic_gflop_per_step": flops * w["batch"] / 1e9},
+        "update_roofline": upd,
         "phase_ms_per_step": {k: v / n for k, v in ph.items()},
         "loss_first_last": [losses[0], losses[-1]] if losses else None,
         "clocks": clocks,
@@ -257,7 +296,11 @@ def run_b200(args, rank: int, world: int) -> None:
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
     job.close()
+    if dist is not None:
+        dist.destroy_process_group()
 
 
 def main() -> None:

@@ -221,6 +221,7 @@ typedef struct {
   uint64_t init_seed;        /* MLP weight init seed                                       */
   double t_a_ms;             /* switch allowance T_a, default 500             */
   int32_t keep_log;          /* record the assignment log                                  */
+  int32_t dry_run;           /* host protocol only (leases, ring, log): no device work      */
 } EdlJobConfig;
 
 typedef struct {
@@ -272,6 +273,16 @@ int edl_job_lease_snapshot(const EdlJob* job, uint8_t* buf, size_t cap, size_t* 
  * (phase_ms[5] = gather, forward GEMMs, loss, backward GEMMs, allreduce+update), the steps
  * profiled and the number of library kernels launched since the last reset.            */
 void* edl_job_stream(const EdlJob* job);
+/* Multi-process data parallelism (one process per GPU, e.g. torchrun): every process
+ * creates the job with the full ring, device = its GPU for its own worker and -1 for
+ * workers hosted elsewhere; exports a blob of CUDA IPC handles (gradients, weights, flags,
+ * losses), ships it to the others by any side channel and imports every peer's blob.
+ * The per-step allreduce + update then runs as one kernel per GPU over NVLink peer memory. */
+int edl_job_export(const EdlJob* job, uint8_t* buf, size_t cap, size_t* len);
+int edl_job_import(EdlJob* job, const uint8_t* blob, size_t len);
+/* Collective: all-gather the sharded fp32 master so every replica holds all of it
+ * (before edl_job_params / checkpoints in multi-process jobs).                          */
+int edl_job_gather_master(EdlJob* job);
 void edl_job_set_profile(EdlJob* job, int32_t on);
 void edl_job_counters(const EdlJob* job, double* phase_ms, uint64_t* steps, uint64_t* launches);
 void edl_job_reset_counters(EdlJob* job);

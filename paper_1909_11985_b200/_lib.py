@@ -85,7 +85,7 @@ class EdlJobConfig(C.Structure):
                 ("decay", C.c_double), ("momentum", C.c_double), ("batch", C.c_int64),
                 ("per_worker_batch", C.c_int64), ("lease_seed", C.c_uint64),
                 ("partitions", C.c_int32), ("max_workers", C.c_int32), ("init_seed", C.c_uint64),
-                ("t_a_ms", C.c_double), ("keep_log", C.c_int32)]
+                ("t_a_ms", C.c_double), ("keep_log", C.c_int32), ("dry_run", C.c_int32)]
 
 
 class EdlStepReport(C.Structure):
@@ -154,6 +154,9 @@ def _declare(L: C.CDLL) -> None:
         "edl_job_set_profile": ([vp, i32], None),
         "edl_job_counters": ([vp, P(f64), P(u64), P(u64)], None),
         "edl_job_reset_counters": ([vp], None),
+        "edl_job_export": ([vp, vp, sz, P(sz)], ci),
+        "edl_job_import": ([vp, vp, sz], ci),
+        "edl_job_gather_master": ([vp], ci),
         "edl_gemm_wgrad_sgd": ([vp, i32, vp, i32, vp, vp, i32, i32, i32, i32, C.c_float, vp], ci),
     }
     for name, (args, res) in sig.items():

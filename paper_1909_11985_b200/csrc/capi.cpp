@@ -269,6 +269,7 @@ void edl_job_config_default(EdlJobConfig* c) {
   c->init_seed = 0;
   c->t_a_ms = 500.0;
   c->keep_log = 1;
+  c->dry_run = 0;
 }
 
 int edl_job_create(const EdlJobConfig* cfg, const char* const* ring, const int32_t* devices,
@@ -356,4 +357,20 @@ void edl_job_counters(const EdlJob* job, double* phase_ms, uint64_t* steps, uint
   job->job->phase_totals(phase_ms, steps, launches);
 }
 void edl_job_reset_counters(EdlJob* job) { job->job->reset_counters(); }
+int edl_job_export(const EdlJob* job, uint8_t* buf, size_t cap, size_t* len) {
+  return guarded([&]() -> int {
+    std::vector<uint8_t> b;
+    const int rc = job->job->export_handles(&b);
+    if (rc != EDL_OK) return rc;
+    if (len) *len = b.size();
+    if (buf) std::memcpy(buf, b.data(), b.size() < cap ? b.size() : cap);
+    return EDL_OK;
+  });
+}
+int edl_job_import(EdlJob* job, const uint8_t* blob, size_t len) {
+  return guarded([&]() -> int { return job->job->import_handles(blob, len); });
+}
+int edl_job_gather_master(EdlJob* job) {
+  return guarded([&]() -> int { return job->job->gather_master(); });
+}
 }  // extern "C"

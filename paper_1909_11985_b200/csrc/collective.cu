@@ -42,19 +42,30 @@ __device__ __forceinline__ uint32_t* flag_slot(uint32_t* base, int phase, int bl
   return base + (static_cast<size_t>(phase) * kCollMaxBlocks + block) * kCollMaxReplicas + src;
 }
 
-__device__ void cross_replica_barrier(const CollArgs& a, int phase) {
+// CTA b of this replica signals CTA b of every peer, then waits for theirs.  After phase 0
+// every peer's earlier kernels (its weight-gradient GEMMs) have completed; after phase 1
+// every peer has finished this kernel's reads of our memory and writes into it.
+__device__ void cross_replica_barrier(uint32_t* const* flags, int me, int n_rep, uint32_t epoch,
+                                      int phase) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
-    for (int r = 0; r < a.n_rep; ++r)
-      if (r != a.me) st_release_sys(flag_slot(a.flags[r], phase, blockIdx.x, a.me), a.epoch);
-    for (int r = 0; r < a.n_rep; ++r) {
-      if (r == a.me) continue;
-      const uint32_t* f = flag_slot(a.flags[a.me], phase, blockIdx.x, r);
-      while (static_cast<int32_t>(ld_acquire_sys(f) - a.epoch) < 0) __nanosleep(64);
+    for (int r = 0; r < n_rep; ++r)
+      if (r != me) st_release_sys(flag_slot(flags[r], phase, blockIdx.x, me), epoch);
+    for (int r = 0; r < n_rep; ++r) {
+      if (r == me) continue;
+      const uint32_t* f = flag_slot(flags[me], phase, blockIdx.x, r);
+      const uint64_t t0 = clock64();
+      while (static_cast<int32_t>(ld_acquire_sys(f) - epoch) < 0) {
+        __nanosleep(32);
+        if (clock64() - t0 > (1ull << 36)) __trap();  // a peer died: fail, don't hang
+      }
     }
   }
   __syncthreads();
+}
+__device__ __forceinline__ void cross_replica_barrier(const CollArgs& a, int phase) {
+  cross_replica_barrier(a.flags, a.me, a.n_rep, a.epoch, phase);
 }
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
@@ -71,7 +82,12 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
 template <bool kMomentum>
 __global__ void __launch_bounds__(256) allreduce_sgd_kernel(CollArgs a) {
   if (a.n_rep > 1) cross_replica_barrier(a, 0);
-  const size_t lo = a.lo8, hi = a.hi8;
+  if (a.loss_out && blockIdx.x == 0 && threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int k = 0; k < a.n_loss; ++k) acc = __dadd_rn(acc, *a.losses[k]);
+    *a.loss_out = acc;
+  }
+  const size_t lo = a.lo8, hi = a.update ? a.hi8 : a.lo8;
   for (size_t i = lo + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < hi;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     float gs[8];
@@ -113,7 +129,53 @@ __global__ void __launch_bounds__(256) allreduce_sgd_kernel(CollArgs a) {
 
 __global__ void barrier_kernel(CollArgs a) { cross_replica_barrier(a, 0); }
 
+// One CTA: barrier, ring-order f64 reduction of every member's [grad_sum, count] (chunk c =
+// [c*len/n, (c+1)*len/n) folds ranks c, c+1, ... left to right, allreduce.cpp:132-148),
+// ordered loss sum, barrier, then sgd_step on the local replica (trainer.cpp:56-61).
+__global__ void linear_allreduce_sgd_kernel(LinearCollArgs a) {
+  if (a.n_rep > 1) cross_replica_barrier(a.flags, a.me, a.n_rep, a.epoch, 0);
+  const int n = a.n_src;
+  const size_t len = static_cast<size_t>(a.dim) + 1;
+  for (size_t i = threadIdx.x; i < len; i += blockDim.x) {
+    int c = 0;
+    while (c + 1 < n && len * static_cast<size_t>(c + 1) / static_cast<size_t>(n) <= i) ++c;
+    double acc = a.g[c][i];
+    for (int k = 1; k < n; ++k) acc = __dadd_rn(acc, a.g[(c + k) % n][i]);
+    a.total[i] = acc;
+  }
+  if (threadIdx.x == 0 && a.loss_out) {
+    double acc = 0.0;
+    for (int k = 0; k < n; ++k) acc = __dadd_rn(acc, *a.losses[k]);
+    *a.loss_out = acc;
+  }
+  __syncthreads();
+  if (a.n_rep > 1) cross_replica_barrier(a.flags, a.me, a.n_rep, a.epoch, 1);
+  const double count = a.total[a.dim];
+  if (count == 0.0) return;
+  const double sc = __ddiv_rn(a.eta, count);
+  for (int i = threadIdx.x; i < a.dim; i += blockDim.x)
+    a.w[i] = __dsub_rn(a.w[i], __dmul_rn(sc, a.total[i]));
+}
+
+__global__ void __launch_bounds__(256) master_allgather_kernel(CollArgs a) {
+  cross_replica_barrier(a, 0);
+  const float4* src = reinterpret_cast<const float4*>(a.master);
+  for (size_t i = a.lo8 * 2 + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+       i < a.hi8 * 2; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const float4 v = src[i];
+    for (int d = 0; d < a.n_dst; ++d)
+      if (d != a.me) reinterpret_cast<float4*>(a.m_dst[d])[i] = v;
+  }
+  cross_replica_barrier(a, 1);
+}
+
 }  // namespace
+
+int master_allgather(const CollArgs& a, cudaStream_t s) {
+  master_allgather_kernel<<<coll_blocks(), 256, 0, s>>>(a);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
 
 int coll_blocks() { return 148 * 4; }
 
@@ -126,6 +188,13 @@ int allreduce_sgd(const CollArgs& a, cudaStream_t s) {
     allreduce_sgd_kernel<true><<<blocks, 256, 0, s>>>(a);
   else
     allreduce_sgd_kernel<false><<<blocks, 256, 0, s>>>(a);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
+
+int linear_allreduce_sgd(const LinearCollArgs& a, cudaStream_t s) {
+  if (a.n_src < 1 || a.n_src > kCollMaxSources) return fail(EDL_EINVAL, "linear allreduce: sources");
+  linear_allreduce_sgd_kernel<<<1, 256, 0, s>>>(a);
   EDL_CUDA_TRY(cudaGetLastError());
   return EDL_OK;
 }

@@ -84,6 +84,7 @@ int Job::init(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
   if (cfg.per_worker_batch <= 0 && cfg.batch < static_cast<int64_t>(ring.size()))
     return fail(EDL_EINVAL, "split_batch: B < p");
   mlp_ = cfg.model == EDL_MODEL_MLP;
+  dry_ = cfg.dry_run != 0;
   if (mlp_) {
     L_ = cfg.layers;
     if (L_ < 1 || cfg.hidden <= 0 || cfg.num_classes <= 0) return fail(EDL_EINVAL, "job: MLP shape");
@@ -105,16 +106,35 @@ int Job::init(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
   std::ostringstream loc;
   loc << "synthetic:" << cfg.data.seed << ":" << cfg.data.size;  // dataset.cpp:56-58
   lm_ = std::make_unique<LeaseManager>(cfg.data.size, parts, cfg.lease_seed, loc.str());
+  int first_local = -1;
   for (size_t i = 0; i < ring.size(); ++i) {
-    int rc = EDL_OK;
-    Replica* r = replica_for(devices[i], &rc);
-    if (!r) return rc;
-    auto w = std::make_unique<Worker>();
-    EDL_TRY(build_worker(w.get(), r));
-    w->id = ring[i];
     if (workers_.count(ring[i])) return fail(EDL_EINVAL, "job: duplicate worker id");
+    auto w = std::make_unique<Worker>();
+    w->id = ring[i];
+    if (devices[i] < 0) {
+      w->remote = true;  // hosted by a peer process; buffers arrive via import_handles
+    } else {
+      int rc = EDL_OK;
+      Replica* r = replica_for(devices[i], &rc);
+      if (!r) return rc;
+      EDL_TRY(build_worker(w.get(), r));
+      if (first_local < 0) first_local = static_cast<int>(i);
+    }
     lm_->enroll(ring[i]);
     workers_[ring[i]] = std::move(w);
+  }
+  if (first_local < 0) return fail(EDL_EINVAL, "job: no local worker (device >= 0) in the ring");
+  my_rank_ = first_local;
+  {
+    Replica* r = reps_.begin()->second.get();
+    PeerRep me;
+    me.rank = my_rank_;
+    me.device = r->device;
+    me.local = true;
+    me.W = r->W;
+    me.master = r->master;
+    me.flags = r->flags;
+    peers_.push_back(me);
   }
   ring_ = ring;
   version_ = 1;
@@ -148,6 +168,8 @@ Replica* Job::replica_for(int device, int* rc) {
 }
 
 int Job::build_replica(Replica* r) {
+  r->rows_cap = cfg_.per_worker_batch > 0 ? cfg_.per_worker_batch : cfg_.batch;
+  if (dry_) return EDL_OK;
   DeviceGuard g(r->device);
   EDL_CUDA_TRY(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
   for (int s = 0; s < kSlots; ++s) {
@@ -198,8 +220,9 @@ int Job::build_replica(Replica* r) {
 }
 
 int Job::build_worker(Worker* w, Replica* r) {
-  DeviceGuard g(r->device);
   w->rep = r;
+  if (dry_) return EDL_OK;
+  DeviceGuard g(r->device);
   w->runs_cap = r->rows_cap + 2;
   EDL_TRY(dalloc(&w->runs_dev, static_cast<size_t>(w->runs_cap)));
   EDL_CUDA_TRY(cudaMallocHost(&w->runs_host, sizeof(EdlRun) * w->runs_cap * kSlots));
@@ -212,7 +235,7 @@ int Job::build_worker(Worker* w, Replica* r) {
 }
 
 void Job::free_worker(Worker* w) {
-  if (!w || !w->rep) return;
+  if (!w || !w->rep || w->remote || dry_) return;
   DeviceGuard g(w->rep->device);
   cudaFree(w->runs_dev);
   cudaFreeHost(w->runs_host);
@@ -223,6 +246,12 @@ void Job::free_worker(Worker* w) {
 }
 
 Job::~Job() {
+  if (dry_) {
+    for (auto& e : events_)
+      if (e->prep && e->prep->joinable()) e->prep->join();
+    return;
+  }
+  for (void* p : ipc_mapped_) cudaIpcCloseMemHandle(p);
   for (auto& e : events_)
     if (e->prep && e->prep->joinable()) e->prep->join();
   for (auto& [dev, r] : reps_) {
@@ -339,6 +368,10 @@ int Job::install_due(bool* switched) {
         lm_->reclaim(id);  // graceful exit: shard back at its last reported offset
         lm_->retire(id);
         auto it = workers_.find(id);
+        if (dry_ || it->second->remote) {
+          workers_.erase(it);
+          continue;
+        }
         cudaEvent_t done;
         DeviceGuard g(it->second->rep->device);
         cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
@@ -499,35 +532,57 @@ int Job::reduce_and_update(uint64_t count, uint64_t t, int slot) {
   Replica* r = reps_.begin()->second.get();
   cudaEvent_t m = mark_begin(r->stream);
   const double eta_t = cfg_.eta / (1.0 + cfg_.decay * static_cast<double>(t));  // trainer.hpp:27
+  const int n_rep = static_cast<int>(peers_.size());
+  if (n_rep > 1 && !peers_ready())
+    return fail(EDL_EINVAL, "job: peer handles missing (call edl_job_import for every peer)");
+  if (ring_.size() > static_cast<size_t>(kCollMaxSources))
+    return fail(EDL_EINVAL, "job: ring larger than the collective supports");
+  const int me = rep_index();
   if (mlp_) {
-    std::vector<const __nv_bfloat16*> grads;
-    for (const auto& id : ring_) grads.push_back(workers_[id]->grad);
-    if (count > 0 && !fused_update_) {
-      __nv_bfloat16* wdst[1] = {r->W};
-      EDL_TRY(sgd_update_bf16(grads.data(), static_cast<int>(grads.size()), r->master, r->mom,
-                              wdst, 1, P_, static_cast<float>(eta_t / static_cast<double>(count)),
-                              static_cast<float>(1.0 / static_cast<double>(count)),
-                              static_cast<float>(eta_t), static_cast<float>(cfg_.momentum),
-                              r->stream));
-    }
-    std::vector<const double*> losses;
-    for (const auto& id : ring_) losses.push_back(workers_[id]->loss);
-    EDL_TRY(ordered_sum_f64(losses.data(), static_cast<int>(losses.size()), r->loss_sum,
-                            r->stream));
-    launches_ += (count > 0 ? 1 : 0) + 1;
-  } else {
-    std::vector<const double*> gs, losses;
+    // one fused kernel per replica: [barrier] ordered loss sum, reduce-scatter of the bf16
+    // gradients of every ring member, sharded SGD on the fp32 master, all-gather of the
+    // bf16 weights into every replica [barrier]
+    CollArgs a;
     for (const auto& id : ring_) {
-      gs.push_back(workers_[id]->g);
-      losses.push_back(workers_[id]->loss);
+      a.grads[a.n_src++] = workers_[id]->grad;
+      a.losses[a.n_loss++] = workers_[id]->loss;
     }
-    EDL_TRY(ring_allreduce_f64(gs.data(), static_cast<int>(gs.size()),
-                               static_cast<size_t>(cfg_.data.dim) + 1, EDL_REDUCE_SUM, r->total,
-                               r->stream));
-    if (count > 0) EDL_TRY(linear_sgd(r->w, r->total, -1, eta_t, cfg_.data.dim, r->stream));
-    EDL_TRY(ordered_sum_f64(losses.data(), static_cast<int>(losses.size()), r->loss_sum,
-                            r->stream));
-    launches_ += 2 + (count > 0 ? 1 : 0);
+    for (const auto& p : peers_) {
+      a.w_dst[a.n_dst++] = p.W;
+      a.flags[&p - peers_.data()] = p.flags;
+    }
+    a.me = me;
+    a.n_rep = n_rep;
+    a.epoch = ++coll_epoch_;
+    shard_range(P_ / 8, n_rep, me, &a.lo8, &a.hi8);
+    a.master = r->master;
+    a.mom = r->mom;
+    a.scale = count ? static_cast<float>(eta_t / static_cast<double>(count)) : 0.f;
+    a.inv_count = count ? static_cast<float>(1.0 / static_cast<double>(count)) : 0.f;
+    a.eta = static_cast<float>(eta_t);
+    a.mu = static_cast<float>(cfg_.momentum);
+    a.update = (count > 0 && !fused_update_) ? 1 : 0;
+    a.loss_out = r->loss_sum;
+    EDL_TRY(allreduce_sgd(a, r->stream));
+    launches_ += 1;
+  } else {
+    LinearCollArgs a;
+    for (const auto& id : ring_) {
+      a.g[a.n_src] = workers_[id]->g;
+      a.losses[a.n_src] = workers_[id]->loss;
+      ++a.n_src;
+    }
+    for (const auto& p : peers_) a.flags[&p - peers_.data()] = p.flags;
+    a.me = me;
+    a.n_rep = n_rep;
+    a.epoch = ++coll_epoch_;
+    a.dim = cfg_.data.dim;
+    a.total = r->total;
+    a.w = r->w;
+    a.eta = eta_t;
+    a.loss_out = r->loss_sum;
+    EDL_TRY(linear_allreduce_sgd(a, r->stream));
+    launches_ += 1;
   }
   m = mark(slot, 4, m, r->stream);
   (void)m;
@@ -590,7 +645,43 @@ double Job::median_step_ms() const {
   return v[v.size() / 2];
 }
 
+// Host-only mini-batch (EdlJobConfig::dry_run): the full control protocol — topology
+// installs, lease draws, assignment log — without device work.  Lets every process of a
+// multi-process job (or a CPU test) replay the leader's decisions.
+int Job::step_dry(EdlStepReport* out) {
+  bool switched = false;
+  EDL_TRY(install_due(&switched));
+  uint64_t count = 0;
+  for (size_t k = 0; k < ring_.size(); ++k) {
+    Worker* w = workers_[ring_[k]].get();
+    w->plan = draw(w, splits_[k]);
+    count += w->plan.size();
+  }
+  if (cfg_.keep_log) {
+    for (const auto& id : ring_) {
+      LogRec rec;
+      rec.t = t_;
+      rec.worker = id;
+      rec.samples = workers_[id]->plan;
+      log_.push_back(std::move(rec));
+    }
+  }
+  EdlStepReport rep{};
+  rep.t = t_;
+  rep.version = version_;
+  rep.ring_size = static_cast<int32_t>(ring_.size());
+  rep.switched = switched ? 1 : 0;
+  rep.count = count;
+  rep.loss = NAN;
+  last_ = rep;
+  if (out) *out = rep;
+  ++t_;
+  ++launched_;
+  return EDL_OK;
+}
+
 int Job::step(EdlStepReport* out) {
+  if (dry_) return step_dry(out);
   Replica* r = reps_.begin()->second.get();
   DeviceGuard g(r->device);
   const int slot = static_cast<int>(launched_ % kSlots);
@@ -605,8 +696,9 @@ int Job::step(EdlStepReport* out) {
   uint64_t count = 0;
   for (size_t k = 0; k < ring_.size(); ++k) {
     Worker* w = workers_[ring_[k]].get();
-    w->plan = draw(w, splits_[k]);
+    w->plan = draw(w, splits_[k]);  // every process replays every member's draw
     count += w->plan.size();
+    if (w->remote) continue;
     EdlRun* host = w->runs_host + static_cast<size_t>(slot) * w->runs_cap;
     int n = 0;
     for (size_t i = 0; i < w->plan.size(); ++i) {
@@ -629,6 +721,7 @@ int Job::step(EdlStepReport* out) {
   EDL_CUDA_TRY(cudaEventRecord(r->ev_begin[slot], r->stream));
   for (const auto& id : ring_) {
     Worker* w = workers_[id].get();
+    if (w->remote) continue;  // computed by its own process
     EDL_TRY(mlp_ ? run_worker_mlp(w, slot) : run_worker_linear(w, slot));
   }
   EDL_TRY(reduce_and_update(count, t_, slot));
@@ -665,6 +758,10 @@ int Job::step(EdlStepReport* out) {
 }
 
 int Job::sync(EdlStepReport* out) {
+  if (dry_) {
+    if (out) *out = last_;
+    return EDL_OK;
+  }
   for (auto& [dev, r] : reps_) {
     DeviceGuard g(dev);
     EDL_CUDA_TRY(cudaStreamSynchronize(r->stream));
@@ -771,6 +868,170 @@ std::string Job::ring_csv() const {
   std::string s;
   for (size_t i = 0; i < ring_.size(); ++i) s += (i ? "," : "") + ring_[i];
   return s;
+}
+
+// ------------------------------------------------------------------ multi-process plumbing
+// One process per GPU: every process hosts its own replica + worker(s) and replays the
+// lease protocol for the whole ring; the per-step exchange goes through CUDA IPC mappings
+// of the peers' gradient / weight / flag / loss buffers (NVLink peer memory), so no NCCL
+// call sits on the data path.
+
+int Job::rep_index() const {
+  for (size_t i = 0; i < peers_.size(); ++i)
+    if (peers_[i].local) return static_cast<int>(i);
+  return 0;
+}
+
+bool Job::peers_ready() const {
+  for (const auto& [id, w] : workers_)
+    if (w->remote && !w->imported) return false;
+  return true;
+}
+
+namespace {
+constexpr uint32_t kBlobMagic = 0x48444c45;  // "EDLH"
+struct BlobW {
+  std::vector<uint8_t> b;
+  bool dry = false;  // dry-run jobs publish the layout without device handles
+  template <class T>
+  void pod(const T& v) {
+    const auto* p = reinterpret_cast<const uint8_t*>(&v);
+    b.insert(b.end(), p, p + sizeof(T));
+  }
+  void text(const std::string& s) {
+    pod<uint32_t>(static_cast<uint32_t>(s.size()));
+    b.insert(b.end(), s.begin(), s.end());
+  }
+  int handle(const void* ptr) {
+    cudaIpcMemHandle_t h{};
+    const uint8_t has = ptr != nullptr && !dry;
+    pod(has);
+    if (has) EDL_CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void*>(ptr)));
+    pod(h);
+    return EDL_OK;
+  }
+};
+struct BlobR {
+  const uint8_t* p;
+  size_t n, at = 0;
+  bool ok = true;
+  template <class T>
+  T pod() {
+    T v{};
+    if (at + sizeof(T) > n) {
+      ok = false;
+      return v;
+    }
+    std::memcpy(&v, p + at, sizeof(T));
+    at += sizeof(T);
+    return v;
+  }
+  std::string text() {
+    const uint32_t k = pod<uint32_t>();
+    if (at + k > n) {
+      ok = false;
+      return {};
+    }
+    std::string s(reinterpret_cast<const char*>(p + at), k);
+    at += k;
+    return s;
+  }
+};
+}  // namespace
+
+int Job::export_handles(std::vector<uint8_t>* out) const {
+  const Replica* r = reps_.begin()->second.get();
+  DeviceGuard g(dry_ ? 0 : r->device);
+  BlobW w;
+  w.dry = dry_;
+  w.pod(kBlobMagic);
+  w.pod<int32_t>(my_rank_);
+  w.pod<int32_t>(r->device);
+  w.pod<uint64_t>(P_);
+  EDL_TRY(w.handle(r->W));
+  EDL_TRY(w.handle(r->master));
+  EDL_TRY(w.handle(r->flags));
+  uint32_t n = 0;
+  for (const auto& [id, wk] : workers_) n += wk->remote ? 0 : 1;
+  w.pod(n);
+  for (const auto& [id, wk] : workers_) {
+    if (wk->remote) continue;
+    w.text(id);
+    EDL_TRY(w.handle(wk->grad));
+    EDL_TRY(w.handle(wk->g));
+    EDL_TRY(w.handle(wk->loss));
+  }
+  *out = std::move(w.b);
+  return EDL_OK;
+}
+
+int Job::import_handles(const uint8_t* blob, size_t len) {
+  Replica* r = reps_.begin()->second.get();
+  DeviceGuard g(dry_ ? 0 : r->device);
+  BlobR rd{blob, len};
+  if (rd.pod<uint32_t>() != kBlobMagic) return fail(EDL_EINVAL, "import: not an edl handle blob");
+  PeerRep peer;
+  peer.rank = rd.pod<int32_t>();
+  peer.device = rd.pod<int32_t>();
+  if (rd.pod<uint64_t>() != P_) return fail(EDL_SHAPE_MISMATCH, "import: model shape differs");
+  auto open = [&](void** dst) -> int {
+    const uint8_t has = rd.pod<uint8_t>();
+    const cudaIpcMemHandle_t h = rd.pod<cudaIpcMemHandle_t>();
+    *dst = nullptr;
+    if (!has || !rd.ok) return EDL_OK;
+    EDL_CUDA_TRY(cudaIpcOpenMemHandle(dst, h, cudaIpcMemLazyEnablePeerAccess));
+    ipc_mapped_.push_back(*dst);
+    return EDL_OK;
+  };
+  void* p = nullptr;
+  EDL_TRY(open(&p));
+  peer.W = static_cast<__nv_bfloat16*>(p);
+  EDL_TRY(open(&p));
+  peer.master = static_cast<float*>(p);
+  EDL_TRY(open(&p));
+  peer.flags = static_cast<uint32_t*>(p);
+  const uint32_t n = rd.pod<uint32_t>();
+  for (uint32_t i = 0; i < n && rd.ok; ++i) {
+    const std::string id = rd.text();
+    auto it = workers_.find(id);
+    if (it == workers_.end() || !it->second->remote)
+      return fail(EDL_UNKNOWN_WORKER, "import: " + id + " is not a remote member of this ring");
+    Worker* w = it->second.get();
+    w->imported = true;
+    EDL_TRY(open(&p));
+    w->grad = static_cast<__nv_bfloat16*>(p);
+    EDL_TRY(open(&p));
+    w->g = static_cast<double*>(p);
+    EDL_TRY(open(&p));
+    w->loss = static_cast<double*>(p);
+  }
+  if (!rd.ok) return fail(EDL_ETRUNCATED, "import: truncated handle blob");
+  if (peers_.size() >= static_cast<size_t>(kCollMaxReplicas))
+    return fail(EDL_EINVAL, "import: too many replicas");
+  peers_.push_back(peer);
+  std::sort(peers_.begin(), peers_.end(),
+            [](const PeerRep& a, const PeerRep& b) { return a.rank < b.rank; });
+  return EDL_OK;
+}
+
+int Job::gather_master() {
+  Replica* r = reps_.begin()->second.get();
+  DeviceGuard g(r->device);
+  if (!mlp_ || peers_.size() < 2) return EDL_OK;
+  CollArgs a;
+  for (const auto& p : peers_) {
+    a.m_dst[a.n_dst] = p.master;
+    a.flags[a.n_dst] = p.flags;
+    ++a.n_dst;
+  }
+  a.me = rep_index();
+  a.n_rep = static_cast<int>(peers_.size());
+  a.epoch = ++coll_epoch_;
+  shard_range(P_ / 8, a.n_rep, a.me, &a.lo8, &a.hi8);
+  a.master = r->master;
+  EDL_TRY(master_allgather(a, r->stream));
+  EDL_CUDA_TRY(cudaStreamSynchronize(r->stream));
+  return EDL_OK;
 }
 
 }  // namespace edl

@@ -71,6 +71,8 @@ struct Replica {
 
 struct Worker {
   std::string id;
+  bool remote = false;    // hosted by another process; buffers below are IPC-mapped
+  bool imported = false;  // remote worker whose handles have been imported
   Replica* rep = nullptr;
   __nv_bfloat16* grad = nullptr;  // MLP gradient sum [P]
   double* g = nullptr;            // linear [grad_sum, count] (dim + 1)
@@ -99,6 +101,17 @@ struct Event {
   double requested_ms = 0;
 };
 
+// A replica as seen by every process: pointers valid in this process (local allocations
+// or CUDA IPC mappings of a peer process's allocations over NVLink).
+struct PeerRep {
+  int rank = 0;  // replica order (smallest initial ring index of its workers)
+  int device = -1;
+  bool local = false;
+  __nv_bfloat16* W = nullptr;
+  float* master = nullptr;
+  uint32_t* flags = nullptr;
+};
+
 class Job {
  public:
   static int create(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
@@ -120,6 +133,12 @@ class Job {
     return EDL_OK;
   }
   void* stream() const { return reps_.begin()->second->stream; }
+  // multi-process data parallelism (one process per GPU): CUDA IPC handle exchange
+  int export_handles(std::vector<uint8_t>* out) const;
+  int import_handles(const uint8_t* blob, size_t len);
+  bool peers_ready() const;
+  // all-gather of the sharded fp32 master across replicas (collective: every process calls)
+  int gather_master();
   void set_profile(bool on) { profile_ = on; }
   // accumulated device ms per phase (gather, forward, loss, backward, update) + launches
   void phase_totals(double* ms, uint64_t* steps, uint64_t* launches) const {
@@ -150,10 +169,12 @@ class Job {
   int run_worker_mlp(Worker* w, int slot);
   int run_worker_linear(Worker* w, int slot);
   int reduce_and_update(uint64_t count, uint64_t t, int slot);
+  int step_dry(EdlStepReport* out);
   void collect_completed();
 
   EdlJobConfig cfg_{};
   bool mlp_ = false;
+  bool dry_ = false;  // host protocol only (EdlJobConfig::dry_run)
   // Single ring member + plain SGD: the update is fused into the weight-gradient GEMMs
   // (there is nothing to all-reduce); set per step.
   bool fused_update_ = false;
@@ -163,6 +184,10 @@ class Job {
   std::vector<size_t> off_;
   size_t P_ = 0;
   std::unique_ptr<LeaseManager> lm_;
+  std::vector<PeerRep> peers_;  // sorted by rank; includes the local replica
+  int my_rank_ = 0;
+  std::vector<void*> ipc_mapped_;
+  int rep_index() const;
   std::map<int, std::unique_ptr<Replica>> reps_;
   std::map<std::string, std::unique_ptr<Worker>> workers_;
   std::vector<std::string> ring_;

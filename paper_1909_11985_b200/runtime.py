@@ -54,6 +54,7 @@ class JobConfig:
     init_seed: int = 0
     t_a_ms: float = 500.0
     keep_log: bool = True
+    dry_run: bool = False
 
     def to_c(self) -> _lib.EdlJobConfig:
         c = _lib.EdlJobConfig()
@@ -65,6 +66,7 @@ class JobConfig:
         c.batch, c.per_worker_batch = self.batch, self.per_worker_batch
         c.lease_seed, c.partitions, c.max_workers = self.lease_seed, self.partitions, self.max_workers
         c.init_seed, c.t_a_ms, c.keep_log = self.init_seed, self.t_a_ms, int(self.keep_log)
+        c.dry_run = int(self.dry_run)
         return c
 
 
@@ -187,6 +189,21 @@ class Job:
 
     def reset_counters(self) -> None:
         self._L.edl_job_reset_counters(self._h)
+
+    def export_handles(self) -> bytes:
+        """CUDA IPC handles of this process's replica and workers (multi-process jobs)."""
+        n = C.c_size_t()
+        _lib.check(self._L.edl_job_export(self._h, None, 0, C.byref(n)))
+        buf = (C.c_uint8 * max(1, n.value))()
+        _lib.check(self._L.edl_job_export(self._h, buf, n.value, C.byref(n)))
+        return bytes(buf[:n.value])
+
+    def import_handles(self, blob: bytes) -> None:
+        buf = (C.c_uint8 * max(1, len(blob))).from_buffer_copy(blob or b"\0")
+        _lib.check(self._L.edl_job_import(self._h, buf, len(blob)))
+
+    def gather_master(self) -> None:
+        _lib.check(self._L.edl_job_gather_master(self._h))
 
     def lease_snapshot(self) -> bytes:
         n = C.c_size_t()
