@@ -120,7 +120,12 @@ def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
     import numpy as np  # noqa: F401
-    batch = int(os.environ.get("EDL_REF_BATCH", "128"))
+    # size each step's sample so the whole --warmup + --steps run stays near 2 minutes
+    probe = cpu_reference_step(16, 1)[0]
+    per_sample = probe / 16
+    budget = float(os.environ.get("EDL_REF_BUDGET_S", "120"))
+    batch = int(max(8, min(512, budget / (args.warmup + args.steps) / per_sample)))
+    batch = int(os.environ.get("EDL_REF_BATCH", batch))
     times = cpu_reference_step(batch, args.warmup + args.steps)
     timed = times[args.warmup:]
     total = sum(timed)
@@ -284,7 +289,11 @@ def run_b200(args, rank: int, world: int) -> None:
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMMs (8 fwd + 7 dgrad + 8 wgrad)",
                      "achieved": gemm_tflops, "peak": peak_t, "unit": "TFLOP/s",
-                     "frac": gemm_tflops / peak_t, "traffic": None,
+                     "frac": gemm_tflops / peak_t,
+                     # DRAM read + write per GEMM launch (mean of the 23 GEMM launches of one
+                     # mini-batch, ncu --set full, profiles/r01_ncu_full.md); algorithmic
+                     # bytes: fwd/dgrad ~40 MB (W once), wgrad+sgd 168 MB (master RMW + W)
+                     "traffic": 67.46e6, "traffic_source": "profiles/r01_ncu_full.md",
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                      "per_step_ms": gemm_ms,
                      "algorithmic_gflop_per_step": flops * w["batch"] / 1e9},
