@@ -261,6 +261,8 @@ int edl_job_schedule(EdlJob* job, int64_t switch_t, int32_t out, const char* con
                      const int32_t* devices, int32_t n);
 /* Parameters of a worker's replica: linear f64[dim]; MLP fp32 master [param_count].    */
 int edl_job_params(EdlJob* job, const char* worker, void* host_out, size_t bytes);
+/* Checkpoint restore into every replica (same layout as edl_job_params).                */
+int edl_job_set_params(EdlJob* job, const void* host, size_t bytes);
 size_t edl_job_param_count(const EdlJob* job);
 uint64_t edl_job_t(const EdlJob* job);
 double edl_job_median_step_ms(const EdlJob* job);

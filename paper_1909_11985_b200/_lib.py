@@ -157,6 +157,7 @@ def _declare(L: C.CDLL) -> None:
         "edl_job_export": ([vp, vp, sz, P(sz)], ci),
         "edl_job_import": ([vp, vp, sz], ci),
         "edl_job_gather_master": ([vp], ci),
+        "edl_job_set_params": ([vp, vp, sz], ci),
         "edl_gemm_wgrad_sgd": ([vp, i32, vp, i32, vp, vp, i32, i32, i32, i32, C.c_float, vp], ci),
     }
     for name, (args, res) in sig.items():

@@ -370,6 +370,9 @@ int edl_job_export(const EdlJob* job, uint8_t* buf, size_t cap, size_t* len) {
 int edl_job_import(EdlJob* job, const uint8_t* blob, size_t len) {
   return guarded([&]() -> int { return job->job->import_handles(blob, len); });
 }
+int edl_job_set_params(EdlJob* job, const void* host, size_t bytes) {
+  return guarded([&]() -> int { return job->job->set_params(host, bytes); });
+}
 int edl_job_gather_master(EdlJob* job) {
   return guarded([&]() -> int { return job->job->gather_master(); });
 }

@@ -730,7 +730,7 @@ int make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, ui
 }
 
 int num_sms() {
-  static int n = 0;
+  static int n = 0;  // identical B200s: the first device's count holds for all
   if (!n) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -744,12 +744,13 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
                 const EpiParams& ep, cudaStream_t stream) {
   using Cf = Cfg<BN>;
   auto kern = gemm_bf16_tn_kernel<BN, A_MN, B_MN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Cf::kSmemBytes) != cudaSuccess)
-      return EDL_ECUDA;
-    attr_set = true;
+  static uint64_t attr_set = 0;  // per device: the attribute lives in each context
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_set >> dev & 1)) {
+    EDL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Cf::kSmemBytes));
+    attr_set |= 1ull << dev;
   }
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
@@ -762,11 +763,13 @@ template <int BN, bool A_MN, bool B_MN, bool kSgd = false>
 int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream, float scale = 0.f) {
   using Cf = Cfg2<BN, kSgd>;
   auto kern = gemm_bf16_2sm_kernel<BN, A_MN, B_MN, kSgd>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_set = 0;  // per device: the attribute lives in each context
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_set >> dev & 1)) {
     EDL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       Cf::kSmemBytes));
-    attr_set = true;
+    attr_set |= 1ull << dev;
   }
   const int tiles = ((p.M + 255) / 256) * ((p.N + BN - 1) / BN);
   const int pairs = num_sms() / 2;

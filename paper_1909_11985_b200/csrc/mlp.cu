@@ -158,3 +158,20 @@ int sgd_update_bf16(const __nv_bfloat16* const* grads, int n_src, float* master,
 }
 
 }  // namespace edl
+
+namespace edl {
+namespace {
+__global__ void master_to_bf16_kernel(const float* __restrict__ m, __nv_bfloat16* __restrict__ w,
+                                      size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    w[i] = __float2bfloat16_rn(m[i]);
+}
+}  // namespace
+
+int master_to_bf16(const float* master, __nv_bfloat16* w, size_t n, cudaStream_t s) {
+  master_to_bf16_kernel<<<148 * 8, 256, 0, s>>>(master, w, n);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
+}  // namespace edl

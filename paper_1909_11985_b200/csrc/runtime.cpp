@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <set>
 #include <sstream>
 
 namespace edl {
@@ -134,10 +135,12 @@ int Job::init(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
     me.W = r->W;
     me.master = r->master;
     me.flags = r->flags;
+    me.rep = r;
     peers_.push_back(me);
   }
   ring_ = ring;
   version_ = 1;
+  rebuild_peers();
   resplit();
   if (cfg_.keep_log) {
     LogRec r;
@@ -153,18 +156,71 @@ int Job::init(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
 Replica* Job::replica_for(int device, int* rc) {
   auto it = reps_.find(device);
   if (it != reps_.end()) return it->second.get();
-  if (!reps_.empty()) {
-    *rc = fail(EDL_EINVAL, "job: one GPU per process in this build (multi-GPU runs use one "
-                           "process per GPU)");
-    return nullptr;
-  }
   auto r = std::make_unique<Replica>();
   r->device = device;
   *rc = build_replica(r.get());
+  if (*rc == EDL_OK) *rc = enable_peers(r.get());
   if (*rc != EDL_OK) return nullptr;
   Replica* raw = r.get();
   reps_[device] = std::move(r);
   return raw;
+}
+
+// NVLink peer access between a new replica's GPU and every other replica's, both ways.
+int Job::enable_peers(Replica* a) {
+  if (dry_) return EDL_OK;
+  for (auto& [dev, r] : reps_) {
+    if (r.get() == a || dev == a->device) continue;
+    for (int pass = 0; pass < 2; ++pass) {
+      const int from = pass ? dev : a->device, to = pass ? a->device : dev;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, from, to);
+      if (!can) return fail(EDL_ECUDA, "GPUs " + std::to_string(from) + " and " +
+                                           std::to_string(to) + " have no peer access");
+      DeviceGuard g(from);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+      cudaGetLastError();  // clear "already enabled"
+    }
+  }
+  return EDL_OK;
+}
+
+Replica* Job::primary() const {
+  for (const auto& id : ring_) {
+    auto it = workers_.find(id);
+    if (it != workers_.end() && !it->second->remote && it->second->rep) return it->second->rep;
+  }
+  return reps_.empty() ? nullptr : reps_.begin()->second.get();
+}
+
+// Single-process jobs: replicas ordered by their first ring member; replicas without
+// members (all their workers left) drop out of the collective.  Multi-process jobs keep the
+// static order fixed at import time.
+void Job::rebuild_peers() {
+  for (const auto& p : peers_)
+    if (!p.local) return;
+  std::vector<PeerRep> v;
+  for (auto& [dev, r] : reps_) {
+    int first = -1;
+    for (size_t i = 0; i < ring_.size() && first < 0; ++i) {
+      auto it = workers_.find(ring_[i]);
+      if (it != workers_.end() && it->second->rep == r.get()) first = static_cast<int>(i);
+    }
+    if (first < 0) continue;
+    PeerRep p;
+    p.rank = first;
+    p.device = dev;
+    p.local = true;
+    p.W = r->W;
+    p.master = r->master;
+    p.flags = r->flags;
+    p.rep = r.get();
+    v.push_back(p);
+  }
+  std::sort(v.begin(), v.end(), [](const PeerRep& a, const PeerRep& b) { return a.rank < b.rank; });
+  if (!v.empty()) peers_ = v;
 }
 
 int Job::build_replica(Replica* r) {
@@ -175,7 +231,9 @@ int Job::build_replica(Replica* r) {
   for (int s = 0; s < kSlots; ++s) {
     EDL_CUDA_TRY(cudaEventCreate(&r->ev_begin[s]));
     EDL_CUDA_TRY(cudaEventCreate(&r->ev_end[s]));
+    EDL_CUDA_TRY(cudaEventCreateWithFlags(&r->ev_done[s], cudaEventDisableTiming));
   }
+  EDL_CUDA_TRY(cudaEventCreateWithFlags(&r->ev_sync, cudaEventDisableTiming));
   EDL_CUDA_TRY(cudaMallocHost(&r->host_loss, sizeof(double) * kSlots));
   EDL_TRY(dataset_create(cfg_.data, mlp_ ? EDL_DTYPE_BF16 : EDL_DTYPE_F64,
                          mlp_ ? cfg_.num_classes : 0, &r->ds));
@@ -245,15 +303,45 @@ void Job::free_worker(Worker* w) {
   w->rep = nullptr;
 }
 
-Job::~Job() {
-  if (dry_) {
-    for (auto& e : events_)
-      if (e->prep && e->prep->joinable()) e->prep->join();
-    return;
+void Job::free_replica(Replica* r) {
+  if (!r || dry_) return;
+  DeviceGuard g(r->device);
+  if (r->stream) cudaStreamSynchronize(r->stream);
+  dataset_destroy(r->ds);
+  cudaFree(r->master);
+  cudaFree(r->W);
+  cudaFree(r->mom);
+  cudaFree(r->flags);
+  for (auto* a : r->act) cudaFree(a);
+  cudaFree(r->logits);
+  cudaFree(r->dlog);
+  cudaFree(r->dx[0]);
+  cudaFree(r->dx[1]);
+  cudaFree(r->row_loss);
+  cudaFree(r->labels);
+  cudaFree(r->w);
+  cudaFree(r->xb);
+  cudaFree(r->yb);
+  cudaFree(r->ws);
+  cudaFree(r->total);
+  cudaFree(r->loss_sum);
+  cudaFreeHost(r->host_loss);
+  for (int s = 0; s < kSlots; ++s) {
+    cudaEventDestroy(r->ev_begin[s]);
+    cudaEventDestroy(r->ev_end[s]);
+    cudaEventDestroy(r->ev_done[s]);
   }
-  for (void* p : ipc_mapped_) cudaIpcCloseMemHandle(p);
+  cudaEventDestroy(r->ev_sync);
+  cudaStreamDestroy(r->stream);
+  r->ds = nullptr;
+  r->stream = nullptr;
+}
+
+Job::~Job() {
   for (auto& e : events_)
     if (e->prep && e->prep->joinable()) e->prep->join();
+  if (dry_) return;
+  for (void* p : ipc_mapped_) cudaIpcCloseMemHandle(p);
   for (auto& [dev, r] : reps_) {
     DeviceGuard g(dev);
     if (r->stream) cudaStreamSynchronize(r->stream);
@@ -262,36 +350,12 @@ Job::~Job() {
     free_worker(w.get());
     cudaEventDestroy(ev);
   }
-  for (auto& e : events_)
+  for (auto& e : events_) {
     for (auto& w : e->prepared) free_worker(w.get());
-  for (auto& [id, w] : workers_) free_worker(w.get());
-  for (auto& [dev, r] : reps_) {
-    DeviceGuard g(dev);
-    dataset_destroy(r->ds);
-    cudaFree(r->master);
-    cudaFree(r->W);
-    cudaFree(r->mom);
-    cudaFree(r->flags);
-    for (auto* a : r->act) cudaFree(a);
-    cudaFree(r->logits);
-    cudaFree(r->dlog);
-    cudaFree(r->dx[0]);
-    cudaFree(r->dx[1]);
-    cudaFree(r->row_loss);
-    cudaFree(r->labels);
-    cudaFree(r->w);
-    cudaFree(r->xb);
-    cudaFree(r->yb);
-    cudaFree(r->ws);
-    cudaFree(r->total);
-    cudaFree(r->loss_sum);
-    cudaFreeHost(r->host_loss);
-    for (int s = 0; s < kSlots; ++s) {
-      cudaEventDestroy(r->ev_begin[s]);
-      cudaEventDestroy(r->ev_end[s]);
-    }
-    cudaStreamDestroy(r->stream);
+    for (auto& r : e->new_reps) free_replica(r.get());
   }
+  for (auto& [id, w] : workers_) free_worker(w.get());
+  for (auto& [dev, r] : reps_) free_replica(r.get());
 }
 
 void Job::resplit() {
@@ -339,9 +403,36 @@ int Job::install_due(bool* switched) {
   while (!events_.empty() && events_.front()->switch_t <= static_cast<int64_t>(t_)) {
     std::unique_ptr<Event> ev = std::move(events_.front());
     events_.pop_front();
+    // the fp32 master is sharded across GPUs; make every replica whole before the
+    // membership (and with it the sharding) changes
+    EDL_TRY(consolidate_master());
     if (ev->out) {
       if (ev->prep && ev->prep->joinable()) ev->prep->join();  // stall only if prep is late
       if (ev->prep_rc != EDL_OK) return ev->prep_rc;
+      Replica* src = primary();  // lowest existing ring member's replica
+      std::set<Replica*> live;     // replicas currently in the collective (model is current)
+      for (const auto& p : peers_)
+        if (p.local) live.insert(p.rep);
+      for (auto& nr : ev->new_reps) {
+        Replica* dst = nr.get();
+        auto have = reps_.find(dst->device);
+        if (have != reps_.end()) {
+          // an earlier event already brought this GPU in: join its replica instead
+          for (auto& w : ev->prepared)
+            if (w && w->rep == dst) w->rep = have->second.get();
+          free_replica(dst);
+          continue;
+        }
+        reps_[dst->device] = std::move(nr);
+      }
+      // model broadcast to every replica that is not in the collective yet (new GPUs, or
+      // GPUs whose members all left earlier and whose model is stale)
+      std::set<Replica*> sent;
+      for (auto& w : ev->prepared) {
+        if (!w || live.count(w->rep) || sent.count(w->rep)) continue;
+        EDL_TRY(broadcast_model(src, w->rep));
+        sent.insert(w->rep);
+      }
       std::vector<size_t> order(ev->ids.size());
       for (size_t i = 0; i < order.size(); ++i) order[i] = i;
       std::sort(order.begin(), order.end(),
@@ -354,8 +445,6 @@ int Job::install_due(bool* switched) {
         }
         ring_.push_back(id);
         lm_->enroll(id);
-        // model broadcast: newcomers on an existing device share that replica, which is
-        // already current; the lowest existing rank is the source.
         workers_[id] = std::move(ev->prepared[i]);
       }
     } else {
@@ -391,6 +480,7 @@ int Job::install_due(bool* switched) {
       r.ring = ring_;
       log_.push_back(r);
     }
+    rebuild_peers();
   }
   if (changed) {
     resplit();
@@ -472,6 +562,8 @@ cudaEvent_t Job::mark(int slot, int phase, cudaEvent_t start, cudaStream_t s) {
 
 int Job::run_worker_mlp(Worker* w, int slot) {
   Replica* r = w->rep;
+  DeviceGuard dg(r->device);
+  const bool prof = profile_ && r == primary();
   const int64_t rows = static_cast<int64_t>(w->plan.size());
   EDL_CUDA_TRY(cudaMemsetAsync(w->loss, 0, sizeof(double), r->stream));
   if (rows == 0) {  // ShardPending for the whole step: contributes a zero gradient
@@ -479,7 +571,7 @@ int Job::run_worker_mlp(Worker* w, int slot) {
     return EDL_OK;
   }
   EDL_TRY(ensure_plans(w, rows));
-  cudaEvent_t m = mark_begin(r->stream);
+  cudaEvent_t m = prof ? mark_begin(r->stream) : nullptr;
   EdlRun* host = w->runs_host + static_cast<size_t>(slot) * w->runs_cap;
   EDL_CUDA_TRY(cudaMemcpyAsync(w->runs_dev, host, sizeof(EdlRun) * w->n_runs,
                                cudaMemcpyHostToDevice, r->stream));
@@ -506,8 +598,9 @@ int Job::run_worker_mlp(Worker* w, int slot) {
 
 int Job::run_worker_linear(Worker* w, int slot) {
   Replica* r = w->rep;
+  DeviceGuard dg(r->device);
   const int64_t rows = static_cast<int64_t>(w->plan.size());
-  cudaEvent_t m = mark_begin(r->stream);
+  cudaEvent_t m = (profile_ && r == primary()) ? mark_begin(r->stream) : nullptr;
   if (rows > 0) {
     EdlRun* host = w->runs_host + static_cast<size_t>(slot) * w->runs_cap;
     EDL_CUDA_TRY(cudaMemcpyAsync(w->runs_dev, host, sizeof(EdlRun) * w->n_runs,
@@ -529,70 +622,128 @@ int Job::run_worker_linear(Worker* w, int slot) {
 
 // Protocol step 3.
 int Job::reduce_and_update(uint64_t count, uint64_t t, int slot) {
-  Replica* r = reps_.begin()->second.get();
-  cudaEvent_t m = mark_begin(r->stream);
   const double eta_t = cfg_.eta / (1.0 + cfg_.decay * static_cast<double>(t));  // trainer.hpp:27
   const int n_rep = static_cast<int>(peers_.size());
   if (n_rep > 1 && !peers_ready())
     return fail(EDL_EINVAL, "job: peer handles missing (call edl_job_import for every peer)");
   if (ring_.size() > static_cast<size_t>(kCollMaxSources))
     return fail(EDL_EINVAL, "job: ring larger than the collective supports");
-  const int me = rep_index();
-  if (mlp_) {
-    // one fused kernel per replica: [barrier] ordered loss sum, reduce-scatter of the bf16
-    // gradients of every ring member, sharded SGD on the fp32 master, all-gather of the
-    // bf16 weights into every replica [barrier]
-    CollArgs a;
-    for (const auto& id : ring_) {
-      a.grads[a.n_src++] = workers_[id]->grad;
-      a.losses[a.n_loss++] = workers_[id]->loss;
+  Replica* prim = primary();
+  cudaEvent_t m = mark_begin(prim->stream);
+  const uint32_t epoch = ++coll_epoch_;  // one collective per mini-batch, same on every GPU
+  for (int me = 0; me < n_rep; ++me) {
+    if (!peers_[me].local) continue;  // launched by its own process
+    Replica* r = peers_[me].rep;
+    DeviceGuard dg(r->device);
+    if (mlp_) {
+      // one fused kernel per replica: [barrier] ordered loss sum, reduce-scatter of the bf16
+      // gradients of every ring member, sharded SGD on the fp32 master, all-gather of the
+      // bf16 weights into every replica [barrier]
+      CollArgs a;
+      for (const auto& id : ring_) {
+        a.grads[a.n_src++] = workers_[id]->grad;
+        a.losses[a.n_loss++] = workers_[id]->loss;
+      }
+      for (const auto& p : peers_) {
+        a.flags[a.n_dst] = p.flags;
+        a.w_dst[a.n_dst++] = p.W;
+      }
+      a.me = me;
+      a.n_rep = n_rep;
+      a.epoch = epoch;
+      shard_range(P_ / 8, n_rep, me, &a.lo8, &a.hi8);
+      a.master = r->master;
+      a.mom = r->mom;
+      a.scale = count ? static_cast<float>(eta_t / static_cast<double>(count)) : 0.f;
+      a.inv_count = count ? static_cast<float>(1.0 / static_cast<double>(count)) : 0.f;
+      a.eta = static_cast<float>(eta_t);
+      a.mu = static_cast<float>(cfg_.momentum);
+      a.update = (count > 0 && !fused_update_) ? 1 : 0;
+      a.loss_out = r->loss_sum;
+      EDL_TRY(allreduce_sgd(a, r->stream));
+    } else {
+      LinearCollArgs a;
+      for (const auto& id : ring_) {
+        a.g[a.n_src] = workers_[id]->g;
+        a.losses[a.n_src] = workers_[id]->loss;
+        ++a.n_src;
+      }
+      for (size_t i = 0; i < peers_.size(); ++i) a.flags[i] = peers_[i].flags;
+      a.me = me;
+      a.n_rep = n_rep;
+      a.epoch = epoch;
+      a.dim = cfg_.data.dim;
+      a.total = r->total;
+      a.w = r->w;
+      a.eta = eta_t;
+      a.loss_out = r->loss_sum;
+      EDL_TRY(linear_allreduce_sgd(a, r->stream));
     }
-    for (const auto& p : peers_) {
-      a.w_dst[a.n_dst++] = p.W;
-      a.flags[&p - peers_.data()] = p.flags;
-    }
-    a.me = me;
-    a.n_rep = n_rep;
-    a.epoch = ++coll_epoch_;
-    shard_range(P_ / 8, n_rep, me, &a.lo8, &a.hi8);
-    a.master = r->master;
-    a.mom = r->mom;
-    a.scale = count ? static_cast<float>(eta_t / static_cast<double>(count)) : 0.f;
-    a.inv_count = count ? static_cast<float>(1.0 / static_cast<double>(count)) : 0.f;
-    a.eta = static_cast<float>(eta_t);
-    a.mu = static_cast<float>(cfg_.momentum);
-    a.update = (count > 0 && !fused_update_) ? 1 : 0;
-    a.loss_out = r->loss_sum;
-    EDL_TRY(allreduce_sgd(a, r->stream));
-    launches_ += 1;
-  } else {
-    LinearCollArgs a;
-    for (const auto& id : ring_) {
-      a.g[a.n_src] = workers_[id]->g;
-      a.losses[a.n_src] = workers_[id]->loss;
-      ++a.n_src;
-    }
-    for (const auto& p : peers_) a.flags[&p - peers_.data()] = p.flags;
-    a.me = me;
-    a.n_rep = n_rep;
-    a.epoch = ++coll_epoch_;
-    a.dim = cfg_.data.dim;
-    a.total = r->total;
-    a.w = r->w;
-    a.eta = eta_t;
-    a.loss_out = r->loss_sum;
-    EDL_TRY(linear_allreduce_sgd(a, r->stream));
     launches_ += 1;
   }
-  m = mark(slot, 4, m, r->stream);
+  m = mark(slot, 4, m, prim->stream);
   (void)m;
+  return EDL_OK;
+}
+
+// All-gather of the sharded fp32 master among the local replicas, enqueued on their streams
+// (no host sync): before a topology switch changes the sharding, and for checkpoints.
+int Job::consolidate_master() {
+  if (!mlp_ || peers_.size() < 2 || dry_) return EDL_OK;
+  const uint32_t epoch = ++coll_epoch_;
+  const int n_rep = static_cast<int>(peers_.size());
+  for (int me = 0; me < n_rep; ++me) {
+    if (!peers_[me].local) continue;
+    Replica* r = peers_[me].rep;
+    DeviceGuard dg(r->device);
+    CollArgs a;
+    for (const auto& p : peers_) {
+      a.m_dst[a.n_dst] = p.master;
+      a.flags[a.n_dst] = p.flags;
+      ++a.n_dst;
+    }
+    a.me = me;
+    a.n_rep = n_rep;
+    a.epoch = epoch;
+    shard_range(P_ / 8, n_rep, me, &a.lo8, &a.hi8);
+    a.master = r->master;
+    EDL_TRY(master_allgather(a, r->stream));
+  }
+  return EDL_OK;
+}
+
+// Model broadcast to a joining GPU: peer copies over NVLink from the
+// lowest existing replica, ordered after the source's work so far; the source's next write
+// to its model is its next collective, whose barrier waits for the newcomer.
+int Job::broadcast_model(Replica* src, Replica* dst) {
+  if (dry_ || src == dst) return EDL_OK;
+  {
+    DeviceGuard dg(src->device);
+    EDL_CUDA_TRY(cudaEventRecord(src->ev_sync, src->stream));
+  }
+  DeviceGuard dg(dst->device);
+  EDL_CUDA_TRY(cudaStreamWaitEvent(dst->stream, src->ev_sync, 0));
+  if (mlp_) {
+    EDL_CUDA_TRY(cudaMemcpyPeerAsync(dst->master, dst->device, src->master, src->device,
+                                     sizeof(float) * P_, dst->stream));
+    EDL_CUDA_TRY(cudaMemcpyPeerAsync(dst->W, dst->device, src->W, src->device,
+                                     sizeof(__nv_bfloat16) * P_, dst->stream));
+    if (src->mom && dst->mom)
+      EDL_CUDA_TRY(cudaMemcpyPeerAsync(dst->mom, dst->device, src->mom, src->device,
+                                       sizeof(float) * P_, dst->stream));
+  } else {
+    EDL_CUDA_TRY(cudaMemcpyPeerAsync(dst->w, dst->device, src->w, src->device,
+                                     sizeof(double) * P_, dst->stream));
+  }
+  // the newcomer must not start computing before it holds the model (same stream: ordered)
+  EDL_CUDA_TRY(cudaEventRecord(dst->ev_sync, dst->stream));
   return EDL_OK;
 }
 
 void Job::collect_completed() {
   while (!inflight_.empty()) {
     Pending& p = inflight_.front();
-    Replica* r = reps_.begin()->second.get();
+    Replica* r = p.rep;
     if (cudaEventQuery(r->ev_end[p.slot]) != cudaSuccess) break;
     EdlStepReport rep{};
     rep.t = p.t;
@@ -609,6 +760,7 @@ void Job::collect_completed() {
       float st = 0.f;
       if (cudaEventElapsedTime(&st, p.prev_end, r->ev_begin[p.slot]) == cudaSuccess)
         rep.stall_ms = st;
+      cudaGetLastError();  // events of a previous primary on another GPU are not comparable
     }
     std::vector<cudaEvent_t> used;
     for (const Mark& mk : marks_[p.slot]) {
@@ -682,15 +834,15 @@ int Job::step_dry(EdlStepReport* out) {
 
 int Job::step(EdlStepReport* out) {
   if (dry_) return step_dry(out);
-  Replica* r = reps_.begin()->second.get();
-  DeviceGuard g(r->device);
   const int slot = static_cast<int>(launched_ % kSlots);
-  // pinned staging for this slot is free once the step that used it kSlots ago is done
-  if (launched_ >= kSlots) EDL_CUDA_TRY(cudaEventSynchronize(r->ev_end[slot]));
+  // pinned staging for this slot is free once the mini-batch that used it kSlots ago is done
+  if (slot_end_[slot]) EDL_CUDA_TRY(cudaEventSynchronize(slot_end_[slot]));
   collect_completed();
 
   bool switched = false;
   EDL_TRY(install_due(&switched));
+  Replica* prim = primary();
+  DeviceGuard g(prim->device);
 
   // protocol step 2: lease draws in ring order, runs for the gather kernel
   uint64_t count = 0;
@@ -712,27 +864,35 @@ int Job::step(EdlStepReport* out) {
   }
 
   // one ring member, plain SGD: no collective, the update runs inside the wgrad GEMMs
-  fused_update_ = mlp_ && ring_.size() == 1 && cfg_.momentum == 0.0 && reps_.size() == 1;
+  fused_update_ = mlp_ && ring_.size() == 1 && cfg_.momentum == 0.0 && peers_.size() == 1;
   if (count > 0)
     step_scale_ = static_cast<float>(
         cfg_.eta / (1.0 + cfg_.decay * static_cast<double>(t_)) / static_cast<double>(count));
 
-  // device work
-  EDL_CUDA_TRY(cudaEventRecord(r->ev_begin[slot], r->stream));
+  // device work: each worker on its replica's stream (GPUs run concurrently)
+  EDL_CUDA_TRY(cudaEventRecord(prim->ev_begin[slot], prim->stream));
   for (const auto& id : ring_) {
     Worker* w = workers_[id].get();
     if (w->remote) continue;  // computed by its own process
     EDL_TRY(mlp_ ? run_worker_mlp(w, slot) : run_worker_linear(w, slot));
   }
   EDL_TRY(reduce_and_update(count, t_, slot));
-  EDL_CUDA_TRY(cudaMemcpyAsync(&r->host_loss[slot], r->loss_sum, sizeof(double),
-                               cudaMemcpyDeviceToHost, r->stream));
-  EDL_CUDA_TRY(cudaEventRecord(r->ev_end[slot], r->stream));
+  EDL_CUDA_TRY(cudaMemcpyAsync(&prim->host_loss[slot], prim->loss_sum, sizeof(double),
+                               cudaMemcpyDeviceToHost, prim->stream));
+  // the primary's end event covers every local replica's share of the mini-batch
+  for (const auto& p : peers_) {
+    if (!p.local || p.rep == prim) continue;
+    DeviceGuard dg(p.rep->device);
+    EDL_CUDA_TRY(cudaEventRecord(p.rep->ev_done[slot], p.rep->stream));
+    EDL_CUDA_TRY(cudaStreamWaitEvent(prim->stream, p.rep->ev_done[slot], 0));
+  }
+  EDL_CUDA_TRY(cudaEventRecord(prim->ev_end[slot], prim->stream));
+  slot_end_[slot] = prim->ev_end[slot];
 
-  Pending p{t_, slot, count, version_, static_cast<int>(ring_.size()), switched ? 1 : 0,
+  Pending p{prim, t_, slot, count, version_, static_cast<int>(ring_.size()), switched ? 1 : 0,
             last_end_ != nullptr, last_end_};
   inflight_.push_back(p);
-  last_end_ = r->ev_end[slot];
+  last_end_ = prim->ev_end[slot];
 
   if (cfg_.keep_log) {
     for (const auto& id : ring_) {
@@ -778,6 +938,10 @@ int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<
   if (ids.empty()) return fail(EDL_EINVAL, "scale: empty worker set");
   if (explicit_switch < 0 && !events_.empty())
     return fail(EDL_RETRY, "a scaling operation is in progress");
+  if (!dry_)
+    for (const auto& p : peers_)
+      if (!p.local)
+        return fail(EDL_EINVAL, "scale events need a single-process job in this build");
   auto ev = std::make_unique<Event>();
   ev->out = out;
   ev->ids = ids;
@@ -795,19 +959,39 @@ int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<
       if (workers_.count(id) && explicit_switch < 0)
         return fail(EDL_EINVAL, "scale_out: worker already in the job");
     if (devices.size() != ids.size()) return fail(EDL_EINVAL, "scale_out: one device per worker");
-    for (int d : devices) {
-      int rc = EDL_OK;
-      if (!replica_for(d, &rc)) return rc;
-    }
-    // execution-context preparation off the training thread (§4.2): buffers,
-    // pinned staging; the training loop keeps stepping meanwhile.
+    for (int d : devices)
+      if (d < 0) return fail(EDL_EINVAL, "scale_out: newcomers need a local GPU");
+    // Execution-context preparation off the training thread (§4.2): a
+    // new GPU gets its CUDA context, HBM dataset, model buffers, peer mappings and staging
+    // here while the job keeps stepping; the switch only copies the model.
     ev->prepared.resize(ids.size());
     Event* raw = ev.get();
     ev->prep = std::make_unique<std::thread>([this, raw]() {
+      std::map<int, Replica*> made;
       for (size_t i = 0; i < raw->ids.size(); ++i) {
+        const int d = raw->devices[i];
+        Replica* r = nullptr;
+        auto it = reps_.find(d);  // reps_ only changes on the stepping thread at install
+        if (it != reps_.end()) {
+          r = it->second.get();
+        } else if (made.count(d)) {
+          r = made[d];
+        } else {
+          auto nr = std::make_unique<Replica>();
+          nr->device = d;
+          int rc = build_replica(nr.get());
+          if (rc == EDL_OK) rc = enable_peers(nr.get());
+          if (rc != EDL_OK) {
+            raw->prep_rc = rc;
+            return;
+          }
+          r = nr.get();
+          made[d] = r;
+          raw->new_reps.push_back(std::move(nr));
+        }
         auto w = std::make_unique<Worker>();
         w->id = raw->ids[i];
-        int rc = build_worker(w.get(), reps_[raw->devices[i]].get());
+        int rc = build_worker(w.get(), r);
         if (rc != EDL_OK) {
           raw->prep_rc = rc;
           return;
@@ -836,13 +1020,39 @@ int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<
 int Job::params(const std::string& worker, void* host, size_t bytes) {
   auto it = workers_.find(worker);
   if (it == workers_.end()) return fail(EDL_UNKNOWN_WORKER, "params: unknown worker " + worker);
+  if (it->second->remote) return fail(EDL_EINVAL, "params: worker hosted by another process");
   Replica* r = it->second->rep;
+  bool all_local = true;
+  for (const auto& p : peers_) all_local = all_local && p.local;
+  if (all_local) EDL_TRY(consolidate_master());  // multi-process: call edl_job_gather_master
+  for (auto& [dev, rr] : reps_) {
+    DeviceGuard g(dev);
+    EDL_CUDA_TRY(cudaStreamSynchronize(rr->stream));
+  }
   DeviceGuard g(r->device);
-  EDL_CUDA_TRY(cudaStreamSynchronize(r->stream));
   const size_t need = mlp_ ? sizeof(float) * P_ : sizeof(double) * P_;
   if (bytes < need) return fail(EDL_EINVAL, "params: buffer too small");
   EDL_CUDA_TRY(cudaMemcpy(host, mlp_ ? static_cast<void*>(r->master) : static_cast<void*>(r->w),
                           need, cudaMemcpyDeviceToHost));
+  return EDL_OK;
+}
+
+// Checkpoint restore (stop-resume baseline, recovery): every replica takes the parameters;
+// MLP replicas re-derive their bf16 working weights from the fp32 master.
+int Job::set_params(const void* host, size_t bytes) {
+  const size_t need = mlp_ ? sizeof(float) * P_ : sizeof(double) * P_;
+  if (bytes < need) return fail(EDL_EINVAL, "set_params: buffer too small");
+  for (auto& [dev, r] : reps_) {
+    DeviceGuard g(dev);
+    EDL_CUDA_TRY(cudaStreamSynchronize(r->stream));
+    if (mlp_) {
+      EDL_CUDA_TRY(cudaMemcpy(r->master, host, need, cudaMemcpyHostToDevice));
+      EDL_TRY(master_to_bf16(r->master, r->W, P_, r->stream));
+      EDL_CUDA_TRY(cudaStreamSynchronize(r->stream));
+    } else {
+      EDL_CUDA_TRY(cudaMemcpy(r->w, host, need, cudaMemcpyHostToDevice));
+    }
+  }
   return EDL_OK;
 }
 
@@ -880,6 +1090,12 @@ int Job::rep_index() const {
   for (size_t i = 0; i < peers_.size(); ++i)
     if (peers_[i].local) return static_cast<int>(i);
   return 0;
+}
+
+int Job::rep_index(const Replica* r) const {
+  for (size_t i = 0; i < peers_.size(); ++i)
+    if (peers_[i].rep == r) return static_cast<int>(i);
+  return -1;
 }
 
 bool Job::peers_ready() const {
@@ -1015,22 +1231,31 @@ int Job::import_handles(const uint8_t* blob, size_t len) {
 }
 
 int Job::gather_master() {
-  Replica* r = reps_.begin()->second.get();
-  DeviceGuard g(r->device);
-  if (!mlp_ || peers_.size() < 2) return EDL_OK;
-  CollArgs a;
-  for (const auto& p : peers_) {
-    a.m_dst[a.n_dst] = p.master;
-    a.flags[a.n_dst] = p.flags;
-    ++a.n_dst;
+  if (!mlp_ || peers_.size() < 2 || dry_) return EDL_OK;
+  Replica* r = primary();
+  bool all_local = true;
+  for (const auto& p : peers_) all_local = all_local && p.local;
+  if (all_local) {
+    EDL_TRY(consolidate_master());
+  } else {
+    DeviceGuard g(r->device);
+    CollArgs a;
+    for (const auto& p : peers_) {
+      a.m_dst[a.n_dst] = p.master;
+      a.flags[a.n_dst] = p.flags;
+      ++a.n_dst;
+    }
+    a.me = rep_index(r);
+    a.n_rep = static_cast<int>(peers_.size());
+    a.epoch = ++coll_epoch_;
+    shard_range(P_ / 8, a.n_rep, a.me, &a.lo8, &a.hi8);
+    a.master = r->master;
+    EDL_TRY(master_allgather(a, r->stream));
   }
-  a.me = rep_index();
-  a.n_rep = static_cast<int>(peers_.size());
-  a.epoch = ++coll_epoch_;
-  shard_range(P_ / 8, a.n_rep, a.me, &a.lo8, &a.hi8);
-  a.master = r->master;
-  EDL_TRY(master_allgather(a, r->stream));
-  EDL_CUDA_TRY(cudaStreamSynchronize(r->stream));
+  for (auto& [dev, rr] : reps_) {
+    DeviceGuard g(dev);
+    EDL_CUDA_TRY(cudaStreamSynchronize(rr->stream));
+  }
   return EDL_OK;
 }
 

@@ -66,6 +66,8 @@ struct Replica {
   // per-step events
   cudaEvent_t ev_begin[kSlots] = {};
   cudaEvent_t ev_end[kSlots] = {};
+  cudaEvent_t ev_done[kSlots] = {};  // end of this replica's share of a mini-batch
+  cudaEvent_t ev_sync = nullptr;     // cross-stream ordering (model broadcast)
   double* host_loss = nullptr;  // pinned [kSlots]
 };
 
@@ -99,6 +101,7 @@ struct Event {
   std::unique_ptr<std::thread> prep;
   int prep_rc = EDL_OK;
   double requested_ms = 0;
+  std::vector<std::unique_ptr<Replica>> new_reps;  // GPUs joining the job (built off-thread)
 };
 
 // A replica as seen by every process: pointers valid in this process (local allocations
@@ -110,6 +113,7 @@ struct PeerRep {
   __nv_bfloat16* W = nullptr;
   float* master = nullptr;
   uint32_t* flags = nullptr;
+  Replica* rep = nullptr;  // local replicas
 };
 
 class Job {
@@ -123,6 +127,7 @@ class Job {
   int scale(bool out, const std::vector<std::string>& ids, const std::vector<int>& devices,
             int64_t explicit_switch, int64_t* switch_t);
   int params(const std::string& worker, void* host, size_t bytes);
+  int set_params(const void* host, size_t bytes);
   std::string log_text() const;
   std::string ring_csv() const;
   uint64_t t() const { return t_; }
@@ -132,7 +137,10 @@ class Job {
     *out = lm_->snapshot();
     return EDL_OK;
   }
-  void* stream() const { return reps_.begin()->second->stream; }
+  void* stream() const {
+    Replica* r = primary();
+    return r ? r->stream : nullptr;
+  }
   // multi-process data parallelism (one process per GPU): CUDA IPC handle exchange
   int export_handles(std::vector<uint8_t>* out) const;
   int import_handles(const uint8_t* blob, size_t len);
@@ -162,6 +170,7 @@ class Job {
   int build_replica(Replica* r);
   int build_worker(Worker* w, Replica* r);
   void free_worker(Worker* w);
+  void free_replica(Replica* r);
   int ensure_plans(Worker* w, int64_t rows);
   int install_due(bool* switched);
   void resplit();
@@ -188,6 +197,13 @@ class Job {
   int my_rank_ = 0;
   std::vector<void*> ipc_mapped_;
   int rep_index() const;
+  int rep_index(const Replica* r) const;
+  Replica* primary() const;  // replica of the lowest-ranked local ring member
+  int enable_peers(Replica* a);
+  void rebuild_peers();
+  int consolidate_master();  // async all-gather of the sharded fp32 master (local replicas)
+  int broadcast_model(Replica* src, Replica* dst);
+  cudaEvent_t slot_end_[kSlots] = {};
   std::map<int, std::unique_ptr<Replica>> reps_;
   std::map<std::string, std::unique_ptr<Worker>> workers_;
   std::vector<std::string> ring_;
@@ -199,6 +215,7 @@ class Job {
   uint32_t coll_epoch_ = 0;
   // completed-step bookkeeping
   struct Pending {
+    Replica* rep;  // primary replica whose events time this mini-batch
     uint64_t t;
     int slot;
     uint64_t count;

@@ -150,6 +150,12 @@ class Job:
         _lib.check(self._L.edl_job_params(self._h, worker.encode(), out.ctypes.data, out.nbytes))
         return out
 
+    def set_params(self, params: np.ndarray) -> None:
+        """Checkpoint restore into every replica (MLP: fp32 master; linear: f64 w)."""
+        dt = np.float32 if self.cfg.model == MLP else np.float64
+        a = np.ascontiguousarray(params, dtype=dt)
+        _lib.check(self._L.edl_job_set_params(self._h, a.ctypes.data, a.nbytes))
+
     @property
     def t(self) -> int:
         return self._L.edl_job_t(self._h)
