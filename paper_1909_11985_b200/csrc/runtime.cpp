@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <limits>
 #include <set>
 #include <sstream>
 
@@ -167,10 +168,13 @@ Replica* Job::replica_for(int device, int* rc) {
 }
 
 // NVLink peer access between a new replica's GPU and every other replica's, both ways.
-int Job::enable_peers(Replica* a) {
+int Job::enable_peers(Replica* a, const std::vector<Replica*>& also) {
   if (dry_) return EDL_OK;
-  for (auto& [dev, r] : reps_) {
-    if (r.get() == a || dev == a->device) continue;
+  std::vector<int> devs;
+  for (auto& [dev, r] : reps_) devs.push_back(dev);
+  for (Replica* o : also) devs.push_back(o->device);
+  for (int dev : devs) {
+    if (dev == a->device) continue;
     for (int pass = 0; pass < 2; ++pass) {
       const int from = pass ? dev : a->device, to = pass ? a->device : dev;
       int can = 0;
@@ -397,7 +401,29 @@ std::vector<std::pair<uint64_t, uint64_t>> Job::draw(Worker* w, int64_t need) {
 }
 
 // Protocol step 1: topology switches due at this mini-batch.
+int64_t Job::switch_delay_steps() const {
+  const double tb = median_step_ms();
+  if (!(tb > 0)) return 1;
+  return std::max<int64_t>(1, static_cast<int64_t>(std::ceil(cfg_.t_a_ms / tb)));
+}
+
+void Job::arm_ready_events() {
+  bool armed = false;
+  for (auto& e : events_) {
+    if (!e->await_ready || !e->ready.load(std::memory_order_acquire)) continue;
+    e->await_ready = false;
+    e->switch_t = static_cast<int64_t>(t_) + switch_delay_steps();
+    armed = true;
+  }
+  if (armed)
+    std::stable_sort(events_.begin(), events_.end(),
+                     [](const std::unique_ptr<Event>& a, const std::unique_ptr<Event>& b) {
+                       return a->switch_t < b->switch_t;
+                     });
+}
+
 int Job::install_due(bool* switched) {
+  arm_ready_events();
   *switched = false;
   bool changed = false;
   while (!events_.empty() && events_.front()->switch_t <= static_cast<int64_t>(t_)) {
@@ -948,11 +974,11 @@ int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<
   ev->devices = devices;
   if (explicit_switch >= 0) {
     ev->switch_t = explicit_switch;
+  } else if (out) {
+    ev->await_ready = true;  // switch_t chosen when the newcomers are Ready
+    ev->switch_t = std::numeric_limits<int64_t>::max();
   } else {
-    const double tb = median_step_ms();
-    int64_t k = 1;
-    if (tb > 0) k = std::max<int64_t>(1, static_cast<int64_t>(std::ceil(cfg_.t_a_ms / tb)));
-    ev->switch_t = static_cast<int64_t>(t_) + k;
+    ev->switch_t = static_cast<int64_t>(t_) + switch_delay_steps();
   }
   if (out) {
     for (const auto& id : ids)
@@ -967,31 +993,45 @@ int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<
     ev->prepared.resize(ids.size());
     Event* raw = ev.get();
     ev->prep = std::make_unique<std::thread>([this, raw]() {
+      struct ReadyOnExit {
+        std::atomic<bool>& f;
+        ~ReadyOnExit() { f.store(true, std::memory_order_release); }
+      } ready_on_exit{raw->ready};
+      // new GPUs are prepared in parallel, one thread each (context, dataset, buffers)
       std::map<int, Replica*> made;
+      std::vector<std::unique_ptr<Replica>> fresh;
+      for (int d : raw->devices) {
+        if (reps_.count(d) || made.count(d)) continue;  // reps_ changes only at install
+        fresh.push_back(std::make_unique<Replica>());
+        fresh.back()->device = d;
+        made[d] = fresh.back().get();
+      }
+      std::vector<int> rcs(fresh.size(), EDL_OK);
+      std::vector<std::thread> builders;
+      for (size_t k = 0; k < fresh.size(); ++k)
+        builders.emplace_back([this, &fresh, &rcs, k]() { rcs[k] = build_replica(fresh[k].get()); });
+      for (auto& b : builders) b.join();
+      for (size_t k = 0; k < fresh.size(); ++k) {
+        if (rcs[k] != EDL_OK) {
+          raw->prep_rc = rcs[k];
+          for (auto& f : fresh) raw->new_reps.push_back(std::move(f));
+          return;
+        }
+        // peer mappings with the job's GPUs and with this event's other newcomers
+        std::vector<Replica*> others;
+        for (size_t o = 0; o < k; ++o) others.push_back(fresh[o].get());
+        const int rc = enable_peers(fresh[k].get(), others);
+        if (rc != EDL_OK) raw->prep_rc = rc;
+      }
+      for (auto& f : fresh) raw->new_reps.push_back(std::move(f));
+      if (raw->prep_rc != EDL_OK) return;
       for (size_t i = 0; i < raw->ids.size(); ++i) {
         const int d = raw->devices[i];
-        Replica* r = nullptr;
-        auto it = reps_.find(d);  // reps_ only changes on the stepping thread at install
-        if (it != reps_.end()) {
-          r = it->second.get();
-        } else if (made.count(d)) {
-          r = made[d];
-        } else {
-          auto nr = std::make_unique<Replica>();
-          nr->device = d;
-          int rc = build_replica(nr.get());
-          if (rc == EDL_OK) rc = enable_peers(nr.get());
-          if (rc != EDL_OK) {
-            raw->prep_rc = rc;
-            return;
-          }
-          r = nr.get();
-          made[d] = r;
-          raw->new_reps.push_back(std::move(nr));
-        }
+        auto it = reps_.find(d);
+        Replica* r = it != reps_.end() ? it->second.get() : made[d];
         auto w = std::make_unique<Worker>();
         w->id = raw->ids[i];
-        int rc = build_worker(w.get(), r);
+        const int rc = build_worker(w.get(), r);
         if (rc != EDL_OK) {
           raw->prep_rc = rc;
           return;
@@ -1010,7 +1050,7 @@ int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<
       if (leaving >= ring_.size()) return fail(EDL_EINVAL, "scale_in: no worker would remain");
     }
   }
-  if (switch_t) *switch_t = ev->switch_t;
+  if (switch_t) *switch_t = ev->await_ready ? -1 : ev->switch_t;
   auto pos = std::upper_bound(events_.begin(), events_.end(), ev->switch_t,
                               [](int64_t s, const std::unique_ptr<Event>& e) { return s < e->switch_t; });
   events_.insert(pos, std::move(ev));

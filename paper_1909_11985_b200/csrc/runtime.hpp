@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <deque>
 #include <map>
@@ -93,6 +94,10 @@ struct Worker {
 };
 
 struct Event {
+  // scheduler-facing scale_out: switch_t is fixed only once the newcomers report Ready
+  // (preparation done), as t_cur + max(1, ceil(T_a / T_b))
+  bool await_ready = false;
+  std::atomic<bool> ready{false};
   int64_t switch_t;
   bool out;
   std::vector<std::string> ids;
@@ -173,6 +178,8 @@ class Job {
   void free_replica(Replica* r);
   int ensure_plans(Worker* w, int64_t rows);
   int install_due(bool* switched);
+  void arm_ready_events();  // Ready -> switch_t for scale-outs whose preparation finished
+  int64_t switch_delay_steps() const;
   void resplit();
   std::vector<std::pair<uint64_t, uint64_t>> draw(Worker* w, int64_t need);
   int run_worker_mlp(Worker* w, int slot);
@@ -199,7 +206,7 @@ class Job {
   int rep_index() const;
   int rep_index(const Replica* r) const;
   Replica* primary() const;  // replica of the lowest-ranked local ring member
-  int enable_peers(Replica* a);
+  int enable_peers(Replica* a, const std::vector<Replica*>& also = {});
   void rebuild_peers();
   int consolidate_master();  // async all-gather of the sharded fp32 master (local replicas)
   int broadcast_model(Replica* src, Replica* dst);

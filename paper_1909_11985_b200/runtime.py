@@ -119,6 +119,10 @@ class Job:
         return StepReport.of(r)
 
     def scale_out(self, ids, devices=None) -> int:
+        """Stop-free scale-out.  Newcomers are prepared on a side thread
+        while the job keeps stepping; once they are Ready the switch is set to
+        t + max(1, ceil(T_a / T_b)).  Returns -1 (switch pending); the StepReport of the switch
+        mini-batch has switched=True.  Raises EdlError(Retry) while another op is pending."""
         ids = list(ids)
         devices = list(devices) if devices is not None else [0] * len(ids)
         st = C.c_int64()

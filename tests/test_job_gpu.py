@@ -172,18 +172,20 @@ def test_scale_api_retry_and_k():
     for _ in range(5):
         job.step()
     job.sync()
-    tb = job.median_step_ms()
-    st = job.scale_out(["w01"])
-    assert st == job.t + rt.switch_delay(500.0, tb)
+    # scale_out: the switch is fixed only when the newcomer is Ready
+    assert job.scale_out(["w01"]) == -1
     with pytest.raises(_lib.EdlError) as e:
         job.scale_in(["w00"])
     assert e.value.code == _lib.EDL_RETRY
-    while job.t < st:
+    for _ in range(100000):
         rep = job.step()
-    rep = job.step()
+        if rep.switched:
+            break
     assert rep.switched and rep.ring_size == 2 and rep.version == 2
     job.sync()
+    tb = job.median_step_ms()
     st2 = job.scale_in(["w00"])
+    assert st2 == job.t + rt.switch_delay(500.0, tb)
     while job.t <= st2:
         job.step()
     job.sync()
