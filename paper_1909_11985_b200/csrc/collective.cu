@@ -87,7 +87,10 @@ __global__ void __launch_bounds__(256) allreduce_sgd_kernel(CollArgs a) {
     for (int k = 0; k < a.n_loss; ++k) acc = __dadd_rn(acc, *a.losses[k]);
     *a.loss_out = acc;
   }
-  const size_t lo = a.lo8, hi = a.update ? a.hi8 : a.lo8;
+  const int n_seg = a.update ? (a.n_seg > 0 ? a.n_seg : 1) : 0;
+  for (int sg = 0; sg < n_seg; ++sg) {
+  const size_t lo = a.n_seg > 0 ? a.seg_lo8[sg] : a.lo8;
+  const size_t hi = a.n_seg > 0 ? a.seg_hi8[sg] : a.hi8;
   for (size_t i = lo + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < hi;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     float gs[8];
@@ -123,6 +126,7 @@ __global__ void __launch_bounds__(256) allreduce_sgd_kernel(CollArgs a) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) oh[k] = __floats2bfloat162_rn(m[2 * k], m[2 * k + 1]);
     for (int d = 0; d < a.n_dst; ++d) reinterpret_cast<uint4*>(a.w_dst[d])[i] = o;
+  }
   }
   if (a.n_rep > 1) cross_replica_barrier(a, 1);
 }
@@ -160,11 +164,16 @@ __global__ void linear_allreduce_sgd_kernel(LinearCollArgs a) {
 __global__ void __launch_bounds__(256) master_allgather_kernel(CollArgs a) {
   cross_replica_barrier(a, 0);
   const float4* src = reinterpret_cast<const float4*>(a.master);
-  for (size_t i = a.lo8 * 2 + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-       i < a.hi8 * 2; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const float4 v = src[i];
-    for (int d = 0; d < a.n_dst; ++d)
-      if (d != a.me) reinterpret_cast<float4*>(a.m_dst[d])[i] = v;
+  const int n_seg = a.n_seg > 0 ? a.n_seg : 1;
+  for (int sg = 0; sg < n_seg; ++sg) {
+    const size_t lo = a.n_seg > 0 ? a.seg_lo8[sg] : a.lo8;
+    const size_t hi = a.n_seg > 0 ? a.seg_hi8[sg] : a.hi8;
+    for (size_t i = lo * 2 + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+         i < hi * 2; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+      const float4 v = src[i];
+      for (int d = 0; d < a.n_dst; ++d)
+        if (d != a.me) reinterpret_cast<float4*>(a.m_dst[d])[i] = v;
+    }
   }
   cross_replica_barrier(a, 1);
 }
@@ -183,7 +192,8 @@ int allreduce_sgd(const CollArgs& a, cudaStream_t s) {
   if (a.n_src < 1 || a.n_src > kCollMaxSources) return fail(EDL_EINVAL, "allreduce_sgd: sources");
   if (a.n_dst < 0 || a.n_dst > kCollMaxReplicas || a.n_rep > kCollMaxReplicas)
     return fail(EDL_EINVAL, "allreduce_sgd: replicas");
-  const int blocks = coll_blocks();
+  const int blocks = a.blocks > 0 ? a.blocks : coll_blocks();
+  if (blocks > kCollMaxBlocks) return fail(EDL_EINVAL, "allreduce_sgd: grid");
   if (a.mu != 0.0f)
     allreduce_sgd_kernel<true><<<blocks, 256, 0, s>>>(a);
   else

@@ -11,6 +11,7 @@ namespace edl {
 constexpr int kCollMaxReplicas = 8;   // GPUs in one NVLink domain
 constexpr int kCollMaxSources = 16;   // ring members contributing gradients
 constexpr int kCollMaxBlocks = 1024;  // >= coll_blocks()
+constexpr int kCollMaxSegs = 64;      // owned parameter segments (one per MLP layer)
 // Flag buffer per replica: [2 phases][kCollMaxBlocks][kCollMaxReplicas] uint32.
 constexpr size_t kCollFlagBytes = 2ull * kCollMaxBlocks * kCollMaxReplicas * sizeof(uint32_t);
 
@@ -23,11 +24,16 @@ struct CollArgs {
   uint32_t* flags[kCollMaxReplicas];  // flag buffers of every replica (peer-mapped)
   int me = 0, n_rep = 1;
   uint32_t epoch = 0;  // strictly increasing per launch
-  size_t lo8 = 0, hi8 = 0;  // owned shard, in units of 8 params
+  size_t lo8 = 0, hi8 = 0;  // owned shard, in units of 8 params (when n_seg == 0)
+  // owned shard as a list of [lo, hi) segments in units of 8 params: every replica owns a
+  // slice of every layer, so a collective restricted to one layer stays balanced
+  int n_seg = 0;
+  size_t seg_lo8[kCollMaxSegs], seg_hi8[kCollMaxSegs];
   float* master = nullptr;  // this replica's fp32 master (full size; shard updated)
   float* mom = nullptr;
   float scale = 0.f, inv_count = 0.f, eta = 0.f, mu = 0.f;
   int update = 1;  // 0: barriers + loss only (count == 0 / fused single-replica update)
+  int blocks = 0;  // grid size; 0 = coll_blocks() (fewer to co-reside with running GEMMs)
   // ordered sum of the ring members' batch losses (between the barriers, so every peer's
   // loss is final and no peer has started the next mini-batch)
   const double* losses[kCollMaxSources];

@@ -34,11 +34,17 @@ struct EpiParams {
   // C (bf16) <- master.  Set per launch by gemm_plan_run(plan, stream, scale).
   int sgd;
   float scale;
+  // L2 prefetch distances (0 = off): operand k-blocks ahead in the producer; master tiles
+  // ahead in the fused-SGD epilogue.  Defaults from gemm_prefetch_defaults().
+  int pf_kb;
+  int pf_tiles;
+  int dbg;  // trace builds only: 1 = skip the K loop, 2 = skip the epilogue work
 };
 // Pre-encoded launch (TMA descriptors built once; launching costs one kernel launch).
 struct GemmPlan {
   CUtensorMap ta, tb, tc, tm;  // tm: fp32 master (fused-SGD plans)
   int M = 0, N = 0, K = 0, a_mn = 0, b_mn = 0, bn = 0, cg = 1;
+  int mc = 1;  // CTA-pair kernel: pairs per cluster sharing A by TMA multicast (1 or 2)
   EpiParams ep{};
 };
 int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B, int ldb,

@@ -23,6 +23,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "edl_internal.hpp"
 #include "sm100.cuh"
@@ -224,8 +225,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (!(__bfloat162float(mb[t]) > 0.0f)) v[j8 * 8 + t] = 0.0f;
             }
           } else {
-            for (int j = 0; j < lim; ++j)
-              if (!(__bfloat162float(mrow[j]) > 0.0f)) v[j] = 0.0f;
+            // constant indices only: a runtime-indexed v[] would live in local memory
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < lim && !(__bfloat162float(mrow[j]) > 0.0f)) v[j] = 0.0f;
           }
         }
         if (ep.out_f32) {
@@ -236,7 +239,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               *reinterpret_cast<float4*>(crow + j4 * 4) =
                   make_float4(v[j4 * 4], v[j4 * 4 + 1], v[j4 * 4 + 2], v[j4 * 4 + 3]);
           } else {
-            for (int j = 0; j < lim; ++j) crow[j] = v[j];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < lim) crow[j] = v[j];
           }
         } else {
           __nv_bfloat16* crow =
@@ -252,7 +257,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               *reinterpret_cast<uint4*>(crow + j8 * 8) = o;
             }
           } else {
-            for (int j = 0; j < lim; ++j) crow[j] = __float2bfloat16_rn(v[j]);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < lim) crow[j] = __float2bfloat16_rn(v[j]);
           }
         }
       }
@@ -275,17 +282,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 // 1-SM kernel needs (the 1-SM kernel is shared-memory-bound at BN=128).  The epilogue
 // goes TMEM -> registers -> 128B-swizzled smem -> TMA bulk-tensor store (coalesced,
 // asynchronous); the two accumulator buffers let tile i's epilogue overlap tile i+1's MMAs.
+//
+// kMc = 2: a cluster of 4 CTAs = 2 pairs working on horizontally adjacent N tiles of the
+// same 256-row M tile.  Both pairs need the same A rows, so each CTA loads half of its
+// 128-row A slice and multicasts it to the matching CTA of the other pair: the L2 -> SM
+// operand stream (which bounds the M=512 GEMMs of the step) drops from 3 to 2 units per k
+// block.  A stage is refilled only when both pairs' MMAs have consumed it (empty barriers
+// count one commit from each pair leader).
 constexpr int kEpiChunkBytes = 32 * 128;  // one warp's 32 rows x 128 B staging box
 
 #ifdef EDL_GEMM_TRACE
 // [cta][0] mma wait-full cycles, [1] mma wait-tempty, [2] mma loop total, [3] producer
 // wait-empty, [4] producer total, [5] epilogue wait-tfull (warp 2), [6] epilogue total
-__device__ unsigned long long g_gemm_trace[296][8];
+__device__ unsigned long long g_gemm_trace[296][16];
+// timeline (globaltimer ns, last write wins): [0] entry, [1] after the setup cluster_sync,
+// [2] first full stage seen by MMA, [3] MMA loop end, [4] first tfull seen by epilogue warp 2,
+// [5] warp 2 stores drained, [6] producer end, [7] after the final cluster_sync
+__device__ unsigned long long g_gemm_tl[296][16];
 #define TRACE_T0(v) const unsigned long long v = clock64()
-#define TRACE_ADD(slot, t0) atomicAdd(&g_gemm_trace[blockIdx.x][slot], clock64() - (t0))
+#define TRACE_ADD(slot, t0) \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&g_gemm_trace[blockIdx.x][slot], clock64() - (t0))
+#define TL(slot) \
+  if ((threadIdx.x & 31) == 0) g_gemm_tl[blockIdx.x][slot] = globaltimer_ns()
 #else
 #define TRACE_T0(v)
 #define TRACE_ADD(slot, t0)
+#define TL(slot)
 #endif
 
 template <int BN, bool kSgd = false>
@@ -298,26 +320,31 @@ struct Cfg2 {
   static constexpr uint32_t kBBytesMN = kBBoxesMN * kMnBlockBytes;
   static constexpr uint32_t kBSlot = kBBytesK > kBBytesMN ? kBBytesK : kBBytesMN;
   static constexpr uint32_t kStageBytes = kABytes + ((kBSlot + 1023) / 1024) * 1024;
-  // epilogue staging per warp x 2 buffers: plain 4 KB; fused SGD 8 KB master + 4 KB bf16 W
+  // epilogue warps: 4 (one per TMEM lane quarter); the fused-SGD epilogue is latency-bound
+  // (TMEM loads, master loads, smem shared with the mainloop) and runs two warps per quarter,
+  // each owning half of the tile's columns
+#ifndef EDL_SGD_EPI_WARPS
+#define EDL_SGD_EPI_WARPS 8
+#endif
+  static constexpr int kEpiWarps = kSgd ? EDL_SGD_EPI_WARPS : 4;
+  static constexpr int kThreads2 = 64 + 32 * kEpiWarps;
+  // epilogue staging per warp: plain 2 x 4 KB; fused SGD kSgdBufs x (8 KB master + 4 KB W)
   static constexpr uint32_t kSgdBufBytes = 3 * kEpiChunkBytes;
-  static constexpr int kSgdBufs = 2;  // master prefetch distance: 1 chunk per warp
+  static constexpr int kSgdBufs = kEpiWarps == 8 ? 1 : 2;
   static constexpr uint32_t kEpiBytes =
-      kSgd ? 4 * kSgdBufs * kSgdBufBytes : 4 * 2 * kEpiChunkBytes;
+      kSgd ? kEpiWarps * kSgdBufs * kSgdBufBytes : 4 * 2 * kEpiChunkBytes;
 #ifndef EDL_GEMM2_MAX_STAGES
 #define EDL_GEMM2_MAX_STAGES 6
 #endif
   static constexpr int kFit = (224 * 1024 - kEpiBytes) / kStageBytes;
   static constexpr int kStages = kFit > EDL_GEMM2_MAX_STAGES ? EDL_GEMM2_MAX_STAGES : kFit;
-  // N <= 128: two interleaved accumulators per tile (even / odd K-steps) so consecutive
-  // MMAs are independent; a dependent M=256 MMA chain is latency-bound below N = 256.
-  static constexpr int kSplit = 1;
-  static constexpr uint32_t kAccCols = BN * kSplit;
+  static constexpr uint32_t kAccCols = BN;
   static constexpr uint32_t kTmemCols = (2 * kAccCols <= 256) ? 256 : 512;
   static constexpr uint32_t kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 512;
 };
 
-template <int BN, bool A_MN, bool B_MN, bool kSgd>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+template <int BN, bool A_MN, bool B_MN, bool kSgd, int kMc>
+__global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                          const __grid_constant__ CUtensorMap tmap_b,
                          const __grid_constant__ CUtensorMap tmap_c,
@@ -338,24 +365,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
-  const int pair = blockIdx.x / 2, n_pairs = gridDim.x / 2;
+  const uint32_t pr = rank & 1;     // rank inside the CTA pair
+  const uint32_t pidx = rank >> 1;  // pair inside the cluster (kMc = 2)
+  const bool leader = pr == 0;
+  const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2 * pidx));
+  const int unit = blockIdx.x / (2 * kMc), n_units = gridDim.x / (2 * kMc);
   const int m_tiles = (M + 255) / 256;
-  const int n_tiles = (N + BN - 1) / BN;
-  const int num_tiles = m_tiles * n_tiles;
+  const int n_tiles = (N + BN - 1) / BN;  // the host guarantees n_tiles % kMc == 0
+  const int num_work = m_tiles * (n_tiles / kMc);
   const int num_kb = (K + BK - 1) / BK;
+  auto tile_m = [&](int w) { return w % m_tiles; };
+  auto tile_n = [&](int w) { return (w / m_tiles) * kMc + static_cast<int>(pidx); };
+#ifdef EDL_GEMM_TRACE
+  const int kb_end = (ep.dbg & 1) ? 0 : num_kb;
+  const bool skip_epi = (ep.dbg & 2) != 0;
+#else
+  const int kb_end = num_kb;
+  constexpr bool skip_epi = false;
+#endif
 
+  if (warp == 0) TL(0);
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmap_a);
     prefetch_tmap(&tmap_b);
     prefetch_tmap(&tmap_c);
+    if (kSgd) prefetch_tmap(&tmap_m);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], kMc);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 8);  // lane 0 of the 4 epilogue warps of both CTAs
+      mbar_init(&tempty_bar[a], 2 * C::kEpiWarps);  // lane 0 of every epilogue warp, both CTAs
     }
     for (int a = 0; a < 16; ++a) mbar_init(&sgd_bar[a], 1);
     fence_barrier_init();
@@ -365,6 +406,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();  // barriers of both CTAs initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (warp == 1) TL(1);
 
   // Producer and MMA loops run warp-uniform (all 32 lanes wait on the barriers; elect.sync
   // picks the issuing lane) so descriptors and coordinates stay in uniform registers and
@@ -376,10 +418,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // both CTAs' bytes (full boxes, OOB included) are counted on the leader's barrier
     const uint32_t tx = 2 * (C::kABytes + (B_MN ? C::kBBytesMN : C::kBBytesK));
     TRACE_T0(t_prod);
-    for (int tile = pair; tile < num_tiles; tile += n_pairs) {
-      const int m0 = (tile % m_tiles) * 256 + static_cast<int>(rank) * 128;
-      const int n0 = (tile / m_tiles) * BN + static_cast<int>(rank) * C::kHalfN;
-      for (int kb = 0; kb < num_kb; ++kb) {
+    const uint16_t a_mask = static_cast<uint16_t>((1u << pr) | (1u << (pr + 2)));
+    for (int w = unit; w < num_work; w += n_units) {
+      const int m0 = tile_m(w) * 256 + static_cast<int>(pr) * 128;
+      const int n0 = tile_n(w) * BN + static_cast<int>(pr) * C::kHalfN;
+      for (int kb = 0; kb < kb_end; ++kb) {
         TRACE_T0(t_w);
         mbar_wait(&empty_bar[stage], phase ^ 1);
         TRACE_ADD(3, t_w);
@@ -387,7 +430,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           uint8_t* sa = smem + stage * C::kStageBytes;
           uint8_t* sb = sa + C::kABytes;
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], tx);
-          if (A_MN) {
+          if (kMc == 2) {  // my half of the A slice, to me and my twin in the other pair
+            if (A_MN)
+              tma_load_2d_2sm_mc(sa + pidx * kMnBlockBytes, &tmap_a, &full_bar[stage],
+                                 m0 + 64 * static_cast<int>(pidx), kb * BK, a_mask);
+            else
+              tma_load_2d_2sm_mc(sa + pidx * (64 * 128), &tmap_a, &full_bar[stage], kb * BK,
+                                 m0 + 64 * static_cast<int>(pidx), a_mask);
+          } else if (A_MN) {
             tma_load_2d_2sm(sa, &tmap_a, &full_bar[stage], m0, kb * BK);
             tma_load_2d_2sm(sa + kMnBlockBytes, &tmap_a, &full_bar[stage], m0 + 64, kb * BK);
           } else {
@@ -401,6 +451,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           } else {
             tma_load_2d_2sm(sb, &tmap_b, &full_bar[stage], kb * BK, n0);
           }
+          // pull k-block kb + pf_kb into L2 now so its TMA load above (kStages later) does
+          // not pay the HBM latency the stage ring is too shallow to cover
+          const int kp = kb + ep.pf_kb;
+          if (ep.pf_kb > 0 && kp < num_kb) {
+            if (A_MN) {
+              tma_prefetch_2d(&tmap_a, m0, kp * BK);
+              tma_prefetch_2d(&tmap_a, m0 + 64, kp * BK);
+            } else {
+              tma_prefetch_2d(&tmap_a, kp * BK, m0);
+            }
+            if (B_MN) {
+#pragma unroll
+              for (int j = 0; j < C::kBBoxesMN; ++j) tma_prefetch_2d(&tmap_b, n0 + 64 * j, kp * BK);
+            } else {
+              tma_prefetch_2d(&tmap_b, kp * BK, n0);
+            }
+          }
         }
         __syncwarp();
         if (++stage == C::kStages) {
@@ -410,6 +477,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
     TRACE_ADD(4, t_prod);
+    TL(6);
   } else if (warp == 1) {
     if (leader) {
       // ------------------------------------------------------------ MMA issuer (pair leader)
@@ -427,7 +495,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // one fixed issuing lane: tcgen05.commit only tracks the MMAs of the executing thread
       const bool issuer = elect_one();
       TRACE_T0(t_mma);
-      for (int tile = pair; tile < num_tiles; tile += n_pairs, ++local) {
+      for (int w = unit; w < num_work; w += n_units, ++local) {
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         TRACE_T0(t_te);
@@ -435,10 +503,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         TRACE_ADD(1, t_te);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * C::kAccCols;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = 0; kb < kb_end; ++kb) {
           TRACE_T0(t_f);
           mbar_wait(&full_bar[stage], phase);
           TRACE_ADD(0, t_f);
+          if (local == 0 && kb == 0) TL(2);
           tc_fence_after();
           const uint64_t so = static_cast<uint64_t>(stage * C::kStageBytes) >> 4;
           if (issuer) {
@@ -446,7 +515,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int k = 0; k < BK / 16; ++k)
               umma_bf16_2sm(d_tmem, a0 + so + ((k * kStepA) >> 4), b0 + so + ((k * kStepB) >> 4),
                             idesc, (kb | k) != 0 ? 1u : 0u);
-            umma_commit_2sm(&empty_bar[stage], 0x3);
+            // kMc = 2: the stage also holds A multicast by the other pair -> free it there too
+            umma_commit_2sm(&empty_bar[stage], kMc == 2 ? 0xF : pair_mask);
           }
           __syncwarp();
           if (++stage == C::kStages) {
@@ -454,10 +524,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             phase ^= 1;
           }
         }
-        if (issuer) umma_commit_2sm(&tfull_bar[acc], 0x3);
+        if (issuer) umma_commit_2sm(&tfull_bar[acc], pair_mask);
         __syncwarp();
       }
       TRACE_ADD(2, t_mma);
+      TL(3);
     }
   } else if (kSgd) {
     // ------------------------------------------------------------ fused SGD epilogue
@@ -465,16 +536,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // chunk (prefetched one chunk ahead, across tiles), fold master -= scale * bf16(acc) in
     // place in swizzled smem, then TMA-store master and the bf16 working weights.
     // HBM per parameter: 4 B master read + 4 B master write + 2 B weight write.
-    const int q = warp & 3;
+    const int q = warp & 3;          // TMEM lane quarter
+    const int ew = warp - 2;         // epilogue warp index
+    constexpr int kHalves = C::kEpiWarps / 4;
+    const int half = ew / 4;         // which column half of the tile (8 warps)
     constexpr int kChunks = BN / 64;
+    static_assert(kChunks % kHalves == 0, "fused SGD: column chunks split across warps");
+    constexpr int kCPW = kChunks / kHalves;  // 64-column chunks per warp per tile
     constexpr int NB = C::kSgdBufs;
-    uint8_t* wbase = epi + q * NB * C::kSgdBufBytes;
-    uint64_t* mb = sgd_bar + q * NB;
+    uint8_t* wbase = epi + ew * NB * C::kSgdBufBytes;
+    uint64_t* mb = sgd_bar + ew * NB;
     auto coords = [&](int j, int* r0, int* c0) -> bool {
-      const int t = pair + (j / kChunks) * n_pairs;
-      if (t >= num_tiles) return false;
-      *r0 = (t % m_tiles) * 256 + static_cast<int>(rank) * 128 + q * 32;
-      *c0 = (t / m_tiles) * BN + (j % kChunks) * 64;
+      const int t = unit + (j / kCPW) * n_units;
+      if (t >= num_work) return false;
+      *r0 = tile_m(t) * 256 + static_cast<int>(pr) * 128 + q * 32;
+      *c0 = tile_n(t) * BN + (half * kCPW + j % kCPW) * 64;
       return true;
     };
     auto prefetch = [&](int j) {
@@ -485,47 +561,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tma_load_2d(dst, &tmap_m, &mb[j % NB], c0, r0);
       tma_load_2d(dst + kEpiChunkBytes, &tmap_m, &mb[j % NB], c0 + 32, r0);
     };
-    if (lane == 0)
-      for (int p0 = 0; p0 < NB - 1; ++p0) prefetch(p0);
+    // L2 prefetch of this warp's 32 master rows of tile t (BN columns, 32-column boxes): the
+    // master stream is the kernel's HBM traffic, and pf_tiles tiles of lead time keep enough
+    // of it in flight without spending shared memory on it
+    auto l2_prefetch_tile = [&](int t) {
+      if (t >= num_work) return;
+      const int r0 = tile_m(t) * 256 + static_cast<int>(pr) * 128 + q * 32;
+      const int c0 = tile_n(t) * BN + half * (BN / kHalves);
+#pragma unroll
+      for (int c = 0; c < BN / kHalves; c += 32) tma_prefetch_2d(&tmap_m, c0 + c, r0);
+    };
+    if (lane == 0) {
+      for (int i = 0; i < ep.pf_tiles; ++i) l2_prefetch_tile(unit + i * n_units);
+      for (int p0 = 0; p0 < (NB > 1 ? NB - 1 : 1) && !skip_epi; ++p0) prefetch(p0);
+    }
     int j = 0;
     int local = 0;
     TRACE_T0(t_epi);
-    for (int tile = pair; tile < num_tiles; tile += n_pairs, ++local) {
+    for (int w = unit; w < num_work; w += n_units, ++local) {
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
+      if (lane == 0 && ep.pf_tiles > 0) l2_prefetch_tile(w + ep.pf_tiles * n_units);
       TRACE_T0(t_tf);
       mbar_wait(&tfull_bar[acc], acc_phase);
-      if (lane == 0) TRACE_ADD(5, t_tf);
+      if (warp == 2) TRACE_ADD(5, t_tf);
+      if (warp == 2 && local == 0) TL(4);
       tc_fence_after();
       const uint32_t t_row =
           tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::kAccCols;
 #pragma unroll 1
-      for (int cc = 0; cc < kChunks; ++cc, ++j) {
+      for (int cc = 0; cc < (skip_epi ? 0 : kCPW); ++cc, ++j) {
         const int b = j % NB;
-        if (lane == 0) {
+        if (NB > 1 && lane == 0) {
           TRACE_T0(t_wr);
           tma_store_wait_read<0>();  // chunk j-1's stores have read the buffer refilled next
-          TRACE_ADD(6, t_wr);
+          if (warp == 2) TRACE_ADD(6, t_wr);
           prefetch(j + NB - 1);
         }
+        TRACE_T0(t_ld);
         float g[64];
         {
-          uint32_t r[32];
-          tmem_ld32(t_row + cc * 64, r);
+          const uint32_t col = static_cast<uint32_t>((half * kCPW + cc) * 64);
+          uint32_t r[32], r2[32];
+          tmem_ld32(t_row + col, r);
+          tmem_ld32(t_row + col + 32, r2);
           tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) g[e] = __uint_as_float(r[e]);
-          tmem_ld32(t_row + cc * 64 + 32, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) g[32 + e] = __uint_as_float(r[e]);
+          for (int e = 0; e < 32; ++e) {
+            g[e] = __uint_as_float(r[e]);
+            g[32 + e] = __uint_as_float(r2[e]);
+          }
         }
         // same numerics as the unfused path: the gradient is rounded to bf16 first
 #pragma unroll
         for (int e = 0; e < 64; ++e) g[e] = __bfloat162float(__float2bfloat16_rn(g[e]));
+        if (warp == 2) TRACE_ADD(9, t_ld);
         TRACE_T0(t_ml);
         mbar_wait(&mb[b], (j / NB) & 1);
-        if (lane == 0) TRACE_ADD(7, t_ml);
+        if (warp == 2) TRACE_ADD(7, t_ml);
+        TRACE_T0(t_cs);
         uint8_t* buf = wbase + b * C::kSgdBufBytes;
         uint8_t* wrow = buf + 2 * kEpiChunkBytes + lane * 128;
 #pragma unroll
@@ -547,6 +641,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             g[h * 32 + k4 * 4 + 3] = m.w;
           }
         }
+        if (warp == 2) TRACE_ADD(11, t_cs);
+        TRACE_T0(t_w8);
 #pragma unroll
         for (int j8 = 0; j8 < 8; ++j8) {
           uint4 o;
@@ -556,8 +652,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           o.w = pack_bf16(g[8 * j8 + 6], g[8 * j8 + 7]);
           *reinterpret_cast<uint4*>(wrow + ((j8 ^ (lane & 7)) << 4)) = o;
         }
+        if (warp == 2) TRACE_ADD(12, t_w8);
+        TRACE_T0(t_fe);
         fence_proxy_async_smem();
         __syncwarp();
+        if (warp == 2) TRACE_ADD(13, t_fe);
         if (lane == 0) {
           int r0, c0;
           coords(j, &r0, &c0);
@@ -565,27 +664,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tma_store_2d(&tmap_m, buf + kEpiChunkBytes, c0 + 32, r0);
           tma_store_2d(&tmap_c, buf + 2 * kEpiChunkBytes, c0, r0);
           tma_store_commit();
+          if (NB == 1) {  // single buffer: refill it for this warp's next chunk (next tile)
+            TRACE_T0(t_wr);
+            tma_store_wait_read<0>();
+            if (warp == 2) TRACE_ADD(6, t_wr);
+            prefetch(j + 1);
+          }
         }
+        if (warp == 2) TRACE_ADD(10, t_cs);
         __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_remote(&tempty_bar[acc], 0);
+      if (lane == 0) mbar_arrive_remote(&tempty_bar[acc], 2 * pidx);
     }
     if (lane == 0) tma_store_wait<0>();
-    if (lane == 0) TRACE_ADD(4, t_epi);  // note: slot 4 shared with producer total
+    if (warp == 2) TRACE_ADD(8, t_epi);
+    if (warp == 2) TL(5);
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int q = warp & 3;  // TMEM lane quarter
     uint8_t* stage_buf = epi + q * 2 * kEpiChunkBytes;
     int buf = 0;
     int local = 0;
-    for (int tile = pair; tile < num_tiles; tile += n_pairs, ++local) {
+    for (int w = unit; w < num_work; w += n_units, ++local) {
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      const int row0 = (tile % m_tiles) * 256 + static_cast<int>(rank) * 128 + q * 32;
-      const int n0 = (tile / m_tiles) * BN;
+      const int row0 = tile_m(w) * 256 + static_cast<int>(pr) * 128 + q * 32;
+      const int n0 = tile_n(w) * BN;
       mbar_wait(&tfull_bar[acc], acc_phase);
+      if (warp == 2 && local == 0) TL(4);
       tc_fence_after();
       const int row = row0 + lane;
       const uint32_t t_row =
@@ -595,28 +703,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int c = 0; c < BN; c += cw) {
         float v[64];
         {
-          uint32_t r[32];
+          uint32_t r[32], r2[32];
           tmem_ld32(t_row + c, r);
+          if (!ep.out_f32) tmem_ld32(t_row + c + 32, r2);
           tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
           if (!ep.out_f32) {
-            tmem_ld32(t_row + c + 32, r);
-            tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[32 + j] = __uint_as_float(r[j]);
-          }
-          if (C::kSplit == 2) {  // fold the odd-K accumulator
-            tmem_ld32(t_row + BN + c, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += __uint_as_float(r[j]);
-            if (!ep.out_f32) {
-              tmem_ld32(t_row + BN + c + 32, r);
-              tmem_ld_wait();
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[32 + j] += __uint_as_float(r[j]);
-            }
+            for (int j = 0; j < 32; ++j) v[32 + j] = __uint_as_float(r2[j]);
           }
         }
         if (ep.relu) {
@@ -635,8 +730,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (!(__bfloat162float(mb[t]) > 0.0f)) v[j8 * 8 + t] = 0.0f;
             }
           } else {
-            for (int j = 0; j < 64 && n0 + c + j < N; ++j)
-              if (!(__bfloat162float(mrow[j]) > 0.0f)) v[j] = 0.0f;
+            // constant indices only: a runtime-indexed v[] would live in local memory
+#pragma unroll
+            for (int j = 0; j < 64; ++j)
+              if (n0 + c + j < N && !(__bfloat162float(mrow[j]) > 0.0f)) v[j] = 0.0f;
           }
         }
         // staging buffer reuse: the TMA store issued two chunks ago must have read it
@@ -668,17 +765,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tma_store_2d(&tmap_c, stage_buf + buf * kEpiChunkBytes, n0 + c, row0);
           tma_store_commit();
         }
+        if (warp == 2 && local == 0) {
+          if (c == 0) TL(9);
+          else TL(10);
+        }
         buf ^= 1;
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_remote(&tempty_bar[acc], 0);
+      if (lane == 0) mbar_arrive_remote(&tempty_bar[acc], 2 * pidx);
     }
+    if (warp == 2) TL(11);
     if (lane == 0) tma_store_wait<0>();
+    if (warp == 2) TL(5);
+    if (warp == 5) TL(12);
   }
+  if (warp == 0) TL(13);
+  if (warp == 1) TL(14);
 
   tc_fence_before();
   cluster_sync();
+  if (warp == 0) TL(7);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_2sm<C::kTmemCols>(tmem_base);
@@ -759,25 +866,43 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
   return EDL_OK;
 }
 
-template <int BN, bool A_MN, bool B_MN, bool kSgd = false>
+template <int BN, bool A_MN, bool B_MN, bool kSgd = false, int kMc = 1>
 int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream, float scale = 0.f) {
   using Cf = Cfg2<BN, kSgd>;
-  auto kern = gemm_bf16_2sm_kernel<BN, A_MN, B_MN, kSgd>;
+  auto kern = gemm_bf16_2sm_kernel<BN, A_MN, B_MN, kSgd, kMc>;
   static uint64_t attr_set = 0;  // per device: the attribute lives in each context
+  static int max_units[64];      // co-resident clusters per device (persistent grid size)
   int dev = 0;
   cudaGetDevice(&dev);
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(Cf::kThreads2);
+  cfg.dynamicSmemBytes = Cf::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2 * kMc;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (!(attr_set >> dev & 1)) {
     EDL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       Cf::kSmemBytes));
+    // a persistent grid must not exceed what the GPCs can hold at once (4-CTA clusters
+    // need two TPCs of one GPC)
+    cfg.gridDim = dim3(num_sms());
+    int n = 0;
+    EDL_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
+    max_units[dev] = n > 0 ? n : 1;
     attr_set |= 1ull << dev;
   }
-  const int tiles = ((p.M + 255) / 256) * ((p.N + BN - 1) / BN);
-  const int pairs = num_sms() / 2;
-  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  const int work = ((p.M + 255) / 256) * ((p.N + BN - 1) / BN / kMc);
+  int units = num_sms() / (2 * kMc);
+  if (units > max_units[dev]) units = max_units[dev];
   EpiParams ep = p.ep;
   ep.scale = scale;
-  kern<<<grid, kThreads, Cf::kSmemBytes, stream>>>(p.ta, p.tb, p.tc, p.tm, p.M, p.N, p.K, ep);
-  EDL_CUDA_TRY(cudaGetLastError());
+  cfg.gridDim = dim3(2 * kMc * (work < units ? work : units));
+  EDL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p.ta, p.tb, p.tc, p.tm, p.M, p.N, p.K, ep));
   return EDL_OK;
 }
 
@@ -823,6 +948,31 @@ int gemm_pick_bn(int M, int N, bool b_mn) {
   return best;
 }
 
+// A-operand multicast across two CTA pairs (EDL_GEMM_MC=0 disables, for comparisons).
+static bool gemm_multicast_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("EDL_GEMM_MC");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on != 0;
+}
+
+// L2 prefetch distances; EDL_GEMM_PF_KB / EDL_GEMM_PF_TILES override (tuning runs).
+static void gemm_prefetch_defaults(EpiParams* ep) {
+  static int kb = -1, tiles = -1;
+  if (kb < 0) {
+    const char* e = getenv("EDL_GEMM_PF_KB");
+    kb = e ? atoi(e) : 8;
+    e = getenv("EDL_GEMM_PF_TILES");
+    tiles = e ? atoi(e) : 1;
+  }
+  ep->pf_kb = kb;
+  ep->pf_tiles = tiles;
+  const char* d = getenv("EDL_GEMM_DBG");
+  ep->dbg = d ? atoi(d) : 0;
+}
+
 int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B, int ldb,
                    int b_mn, void* Cout, int ldc, int M, int N, int K, int relu, int out_f32,
                    const void* mask, int ldm, int bn) {
@@ -844,8 +994,17 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B,
   p->cg = cg;
   if (cg == 2) {
     if (bn != 128 && bn != 192 && bn != 256) return fail(EDL_EINVAL, "gemm: 2-SM N tile");
-    int rc = a_mn ? make_tmap(&p->ta, A, K, M, lda, 64) : make_tmap(&p->ta, A, M, K, lda, 128);
+    // pairs of N tiles share A through multicast when the N tiles pair up and the grid is a
+    // single wave (persistent multi-wave grids lose more to 4-CTA cluster placement)
+    const int n_tiles = (N + bn - 1) / bn, m_tiles = (M + 255) / 256;
+    const int mc = (n_tiles % 2 == 0 && m_tiles * n_tiles <= num_sms() / 2 &&
+                    gemm_multicast_enabled())
+                       ? 2
+                       : 1;
+    int rc = a_mn ? make_tmap(&p->ta, A, K, M, lda, 64)
+                  : make_tmap(&p->ta, A, M, K, lda, mc == 2 ? 64 : 128);
     if (rc) return fail(rc, "gemm: tensor map A");
+    p->mc = mc;
     rc = b_mn ? make_tmap(&p->tb, B, K, N, ldb, 64) : make_tmap(&p->tb, B, N, K, ldb, bn / 2);
     if (rc) return fail(rc, "gemm: tensor map B");
     rc = make_tmap_t(&p->tc, Cout, M, N, ldc, out_f32 ? 32 : 64, 32, out_f32 != 0);
@@ -858,6 +1017,7 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B,
     p->b_mn = b_mn;
     p->bn = bn;
     p->ep = EpiParams{Cout, static_cast<const __nv_bfloat16*>(mask), ldc, ldm, relu, out_f32, 0, 0.f};
+    gemm_prefetch_defaults(&p->ep);
     p->tm = p->tc;
     return EDL_OK;
   }
@@ -879,9 +1039,18 @@ int gemm_plan_init_sgd(GemmPlan* p, const void* A, int lda, int a_mn, const void
                        int b_mn, float* master, __nv_bfloat16* W, int ldw, int M, int N, int K) {
   if (!a_mn || !b_mn) return fail(EDL_EINVAL, "fused SGD: weight-gradient layout (MN-major A/B)");
   if (M <= 0 || N <= 0 || K <= 0 || (ldw * 2) % 16) return fail(EDL_EINVAL, "fused SGD: shape");
+  // N tile 128 (measured: 256 halves the operand re-reads but is slower in the step);
+  // EDL_SGD_BN=256 selects the wide tile
+  static int sgd_bn = -1;
+  if (sgd_bn < 0) {
+    const char* e = getenv("EDL_SGD_BN");
+    sgd_bn = e ? atoi(e) : 128;
+  }
+  const int bn = (sgd_bn == 256 && N >= 256) ? 256 : 128;
   int rc = gemm_plan_init(p, A, lda, a_mn, B, ldb, b_mn, W, ldw, M, N, K, 0, 0, nullptr, 0,
-                          1000 + 128);
+                          1000 + bn);
   if (rc) return rc;
+  p->mc = 1;
   rc = make_tmap_t(&p->tm, master, M, N, ldw, 32, 32, true);
   if (rc) return fail(rc, "fused SGD: tensor map master");
   p->ep.sgd = 1;
@@ -891,17 +1060,26 @@ int gemm_plan_init_sgd(GemmPlan* p, const void* A, int lda, int a_mn, const void
 int gemm_plan_run(const GemmPlan& p, cudaStream_t stream, float sgd_scale) {
   const int a_mn = p.a_mn, b_mn = p.b_mn;
   if (p.ep.sgd) {
-    if (p.cg != 2 || p.bn != 128 || !a_mn || !b_mn)
-      return fail(EDL_EINVAL, "gemm: fused SGD plans are CTA-pair, N tile 128, MN-major A/B");
-    return launch_gemm_2sm<128, true, true, true>(p, stream, sgd_scale);
+    if (p.cg != 2 || (p.bn != 128 && p.bn != 256) || !a_mn || !b_mn || p.mc != 1)
+      return fail(EDL_EINVAL, "gemm: fused SGD plans are CTA-pair, N tile 128/256, MN-major A/B");
+    if (p.bn == 256) return launch_gemm_2sm<256, true, true, true, 1>(p, stream, sgd_scale);
+    return launch_gemm_2sm<128, true, true, true, 1>(p, stream, sgd_scale);
   }
   if (p.cg == 2) {
+#define EDL_GEMM2_MC(BNV, AM, BM_, MC) \
+  return launch_gemm_2sm<BNV, AM, BM_, false, MC>(p, stream);
 #define EDL_GEMM2_CASE(BNV)                                                          \
   case BNV:                                                                          \
-    if (!a_mn && !b_mn) return launch_gemm_2sm<BNV, false, false>(p, stream);        \
-    if (!a_mn && b_mn) return launch_gemm_2sm<BNV, false, true>(p, stream);          \
-    if (a_mn && !b_mn) return launch_gemm_2sm<BNV, true, false>(p, stream);          \
-    return launch_gemm_2sm<BNV, true, true>(p, stream);
+    if (p.mc == 2) {                                                                 \
+      if (!a_mn && !b_mn) EDL_GEMM2_MC(BNV, false, false, 2)                         \
+      if (!a_mn && b_mn) EDL_GEMM2_MC(BNV, false, true, 2)                           \
+      if (a_mn && !b_mn) EDL_GEMM2_MC(BNV, true, false, 2)                           \
+      EDL_GEMM2_MC(BNV, true, true, 2)                                               \
+    }                                                                                \
+    if (!a_mn && !b_mn) EDL_GEMM2_MC(BNV, false, false, 1)                           \
+    if (!a_mn && b_mn) EDL_GEMM2_MC(BNV, false, true, 1)                             \
+    if (a_mn && !b_mn) EDL_GEMM2_MC(BNV, true, false, 1)                             \
+    EDL_GEMM2_MC(BNV, true, true, 1)
     switch (p.bn) {
       EDL_GEMM2_CASE(128)
       EDL_GEMM2_CASE(192)
@@ -910,6 +1088,7 @@ int gemm_plan_run(const GemmPlan& p, cudaStream_t stream, float sgd_scale) {
         return fail(EDL_EINVAL, "gemm: unsupported 2-SM N tile");
     }
 #undef EDL_GEMM2_CASE
+#undef EDL_GEMM2_MC
   }
 #define EDL_GEMM_CASE(BNV)                                                                  \
   case BNV:                                                                                 \
@@ -945,11 +1124,16 @@ int gemm_bf16(const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn
 }  // namespace edl
 
 #ifdef EDL_GEMM_TRACE
+extern "C" int edl_debug_gemm_timeline(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, edl::g_gemm_tl, sizeof(edl::g_gemm_tl));
+  return 0;
+}
 extern "C" int edl_debug_gemm_trace(unsigned long long* out, int reset) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out, edl::g_gemm_trace, sizeof(edl::g_gemm_trace));
   if (reset) {
-    static unsigned long long zero[296][8];
+    static unsigned long long zero[296][16];
     cudaMemcpyToSymbol(edl::g_gemm_trace, zero, sizeof(zero));
   }
   return 0;

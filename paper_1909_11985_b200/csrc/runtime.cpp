@@ -90,6 +90,7 @@ int Job::init(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
   if (mlp_) {
     L_ = cfg.layers;
     if (L_ < 1 || cfg.hidden <= 0 || cfg.num_classes <= 0) return fail(EDL_EINVAL, "job: MLP shape");
+    if (L_ > kCollMaxSegs) return fail(EDL_EINVAL, "job: too many MLP layers");
     if (cfg.data.dim % 8 || cfg.hidden % 8 || cfg.num_classes % 8)
       return fail(EDL_EINVAL, "job: MLP widths must be multiples of 8 (16-byte TMA rows)");
     if (cfg.num_classes > 4096) return fail(EDL_EINVAL, "job: num_classes > 4096");
@@ -238,6 +239,12 @@ int Job::build_replica(Replica* r) {
     EDL_CUDA_TRY(cudaEventCreateWithFlags(&r->ev_done[s], cudaEventDisableTiming));
   }
   EDL_CUDA_TRY(cudaEventCreateWithFlags(&r->ev_sync, cudaEventDisableTiming));
+  if (mlp_) {
+    EDL_CUDA_TRY(cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking));
+    EDL_CUDA_TRY(cudaEventCreateWithFlags(&r->ev_side, cudaEventDisableTiming));
+    r->ev_grad.assign(static_cast<size_t>(L_), nullptr);
+    for (auto& e : r->ev_grad) EDL_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   EDL_CUDA_TRY(cudaMallocHost(&r->host_loss, sizeof(double) * kSlots));
   EDL_TRY(dataset_create(cfg_.data, mlp_ ? EDL_DTYPE_BF16 : EDL_DTYPE_F64,
                          mlp_ ? cfg_.num_classes : 0, &r->ds));
@@ -336,6 +343,15 @@ void Job::free_replica(Replica* r) {
     cudaEventDestroy(r->ev_done[s]);
   }
   cudaEventDestroy(r->ev_sync);
+  for (auto e : r->ev_grad) cudaEventDestroy(e);
+  r->ev_grad.clear();
+  if (r->ev_side) cudaEventDestroy(r->ev_side);
+  if (r->side) {
+    cudaStreamSynchronize(r->side);
+    cudaStreamDestroy(r->side);
+  }
+  r->side = nullptr;
+  r->ev_side = nullptr;
   cudaStreamDestroy(r->stream);
   r->ds = nullptr;
   r->stream = nullptr;
@@ -586,7 +602,7 @@ cudaEvent_t Job::mark(int slot, int phase, cudaEvent_t start, cudaStream_t s) {
   return e;
 }
 
-int Job::run_worker_mlp(Worker* w, int slot) {
+int Job::run_worker_mlp(Worker* w, int slot, bool last) {
   Replica* r = w->rep;
   DeviceGuard dg(r->device);
   const bool prof = profile_ && r == primary();
@@ -594,6 +610,7 @@ int Job::run_worker_mlp(Worker* w, int slot) {
   EDL_CUDA_TRY(cudaMemsetAsync(w->loss, 0, sizeof(double), r->stream));
   if (rows == 0) {  // ShardPending for the whole step: contributes a zero gradient
     EDL_CUDA_TRY(cudaMemsetAsync(w->grad, 0, sizeof(__nv_bfloat16) * P_, r->stream));
+    if (overlap_ && last) EDL_TRY(finish_layer_colls(r));
     return EDL_OK;
   }
   EDL_TRY(ensure_plans(w, rows));
@@ -611,14 +628,85 @@ int Job::run_worker_mlp(Worker* w, int slot) {
   m = mark(slot, 2, m, r->stream);
   for (int l = L_ - 1; l >= 0; --l) {
     if (l > 0) EDL_TRY(gemm_plan_run(r->dgrad[l], r->stream));
-    if (fused_update_)
-      EDL_TRY(gemm_plan_run(w->wgrad_sgd[l], r->stream, step_scale_));  // dW + sgd_step
-    else
+    if (fused_update_ && (!overlap_ || l == 0)) {
+      // dW + sgd_step in one kernel (layer 0 ends the backward: nothing left to overlap)
+      EDL_TRY(gemm_plan_run(w->wgrad_sgd[l], r->stream, step_scale_));
+    } else {
       EDL_TRY(gemm_plan_run(w->wgrad[l], r->stream));
+      if (overlap_ && last) EDL_TRY(launch_layer_coll(r, l));
+    }
   }
+  if (overlap_ && last) EDL_TRY(finish_layer_colls(r));
   m = mark(slot, 3, m, r->stream);
   (void)m;
   launches_ += 1 + static_cast<uint64_t>(L_) + 2 + static_cast<uint64_t>(2 * L_ - 1);
+  return EDL_OK;
+}
+
+// Layer l's update on the replica's side stream, after the main stream's layer-l weight
+// gradients (of every local worker: they run in stream order before this point).  With
+// several replicas it is the fused NVLink collective restricted to layer l's parameters;
+// the shard boundaries, epochs and launch order are the same on every replica.
+int Job::launch_layer_coll(Replica* r, int l) {
+  EDL_CUDA_TRY(cudaEventRecord(r->ev_grad[l], r->stream));
+  EDL_CUDA_TRY(cudaStreamWaitEvent(r->side, r->ev_grad[l], 0));
+  const int n_rep = static_cast<int>(peers_.size());
+  const int me = rep_index(r);
+  CollArgs a;
+  for (const auto& id : ring_) a.grads[a.n_src++] = workers_[id]->grad;
+  for (const auto& p : peers_) {
+    a.flags[a.n_dst] = p.flags;
+    a.w_dst[a.n_dst++] = p.W;
+  }
+  a.me = me;
+  a.n_rep = n_rep;
+  a.epoch = layer_epoch0_ + static_cast<uint32_t>(r->layer_colls);
+  const size_t len8 = static_cast<size_t>(in_[l]) * out_[l] / 8, base8 = off_[l] / 8;
+  shard_range(len8, n_rep, me, &a.lo8, &a.hi8);  // = own_segments()'s segment of layer l
+  a.lo8 += base8;
+  a.hi8 += base8;
+  a.master = r->master;
+  a.mom = r->mom;
+  const double eta_t = cfg_.eta / (1.0 + cfg_.decay * static_cast<double>(t_));
+  a.scale = static_cast<float>(eta_t / static_cast<double>(step_count_));
+  a.inv_count = static_cast<float>(1.0 / static_cast<double>(step_count_));
+  a.eta = static_cast<float>(eta_t);
+  a.mu = static_cast<float>(cfg_.momentum);
+  a.update = 1;
+  static int blocks = -1;  // one CTA per SM: co-resides with the backward GEMMs
+  if (blocks < 0) {
+    const char* e = getenv("EDL_OVERLAP_BLOCKS");
+    blocks = e ? atoi(e) : 148;
+  }
+  a.blocks = blocks;
+  EDL_TRY(allreduce_sgd(a, r->side));
+  ++r->layer_colls;
+  launches_ += 1;
+  return EDL_OK;
+}
+
+void Job::own_segments(int me, int n_rep, CollArgs* a) const {
+  a->n_seg = 0;
+  for (int l = 0; l < L_; ++l) {
+    size_t lo, hi;
+    shard_range(static_cast<size_t>(in_[l]) * out_[l] / 8, n_rep, me, &lo, &hi);
+    if (hi <= lo) continue;
+    a->seg_lo8[a->n_seg] = off_[l] / 8 + lo;
+    a->seg_hi8[a->n_seg] = off_[l] / 8 + hi;
+    ++a->n_seg;
+  }
+}
+
+// Launches the layer updates not issued yet (a worker with an empty batch ends the step
+// early) and makes the replica's main stream wait for the side stream.
+int Job::finish_layer_colls(Replica* r) {
+  const int want = fused_update_ ? L_ - 1 : L_;
+  while (r->layer_colls < want) {
+    const int l = L_ - 1 - r->layer_colls;  // layers go L-1 .. 0 (fused: .. 1)
+    EDL_TRY(launch_layer_coll(r, l));
+  }
+  EDL_CUDA_TRY(cudaEventRecord(r->ev_side, r->side));
+  EDL_CUDA_TRY(cudaStreamWaitEvent(r->stream, r->ev_side, 0));
   return EDL_OK;
 }
 
@@ -677,14 +765,14 @@ int Job::reduce_and_update(uint64_t count, uint64_t t, int slot) {
       a.me = me;
       a.n_rep = n_rep;
       a.epoch = epoch;
-      shard_range(P_ / 8, n_rep, me, &a.lo8, &a.hi8);
+      own_segments(me, n_rep, &a);
       a.master = r->master;
       a.mom = r->mom;
       a.scale = count ? static_cast<float>(eta_t / static_cast<double>(count)) : 0.f;
       a.inv_count = count ? static_cast<float>(1.0 / static_cast<double>(count)) : 0.f;
       a.eta = static_cast<float>(eta_t);
       a.mu = static_cast<float>(cfg_.momentum);
-      a.update = (count > 0 && !fused_update_) ? 1 : 0;
+      a.update = (count > 0 && !fused_update_ && !overlap_) ? 1 : 0;
       a.loss_out = r->loss_sum;
       EDL_TRY(allreduce_sgd(a, r->stream));
     } else {
@@ -731,7 +819,7 @@ int Job::consolidate_master() {
     a.me = me;
     a.n_rep = n_rep;
     a.epoch = epoch;
-    shard_range(P_ / 8, n_rep, me, &a.lo8, &a.hi8);
+    own_segments(me, n_rep, &a);
     a.master = r->master;
     EDL_TRY(master_allgather(a, r->stream));
   }
@@ -895,12 +983,30 @@ int Job::step(EdlStepReport* out) {
     step_scale_ = static_cast<float>(
         cfg_.eta / (1.0 + cfg_.decay * static_cast<double>(t_)) / static_cast<double>(count));
 
+  static int overlap_env = -1;
+  if (overlap_env < 0) {
+    const char* e = getenv("EDL_OVERLAP");
+    overlap_env = e ? atoi(e) : 0;
+  }
+  overlap_ = mlp_ && count > 0 && overlap_env != 0;
+  step_count_ = count;
+  if (overlap_) {  // every process reserves the same epochs for the layer collectives
+    layer_epoch0_ = coll_epoch_ + 1;
+    coll_epoch_ += static_cast<uint32_t>(fused_update_ ? L_ - 1 : L_);
+  }
+  std::map<Replica*, Worker*> last_on;  // last local worker of each replica, in ring order
+  for (const auto& id : ring_) {
+    Worker* w = workers_[id].get();
+    if (!w->remote) last_on[w->rep] = w;
+  }
+  for (auto& [rr, lw] : last_on) rr->layer_colls = 0;
+
   // device work: each worker on its replica's stream (GPUs run concurrently)
   EDL_CUDA_TRY(cudaEventRecord(prim->ev_begin[slot], prim->stream));
   for (const auto& id : ring_) {
     Worker* w = workers_[id].get();
     if (w->remote) continue;  // computed by its own process
-    EDL_TRY(mlp_ ? run_worker_mlp(w, slot) : run_worker_linear(w, slot));
+    EDL_TRY(mlp_ ? run_worker_mlp(w, slot, last_on[w->rep] == w) : run_worker_linear(w, slot));
   }
   EDL_TRY(reduce_and_update(count, t_, slot));
   EDL_CUDA_TRY(cudaMemcpyAsync(&prim->host_loss[slot], prim->loss_sum, sizeof(double),
@@ -1288,7 +1394,7 @@ int Job::gather_master() {
     a.me = rep_index(r);
     a.n_rep = static_cast<int>(peers_.size());
     a.epoch = ++coll_epoch_;
-    shard_range(P_ / 8, a.n_rep, a.me, &a.lo8, &a.hi8);
+    own_segments(a.me, a.n_rep, &a);
     a.master = r->master;
     EDL_TRY(master_allgather(a, r->stream));
   }

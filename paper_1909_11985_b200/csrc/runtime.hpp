@@ -69,6 +69,12 @@ struct Replica {
   cudaEvent_t ev_end[kSlots] = {};
   cudaEvent_t ev_done[kSlots] = {};  // end of this replica's share of a mini-batch
   cudaEvent_t ev_sync = nullptr;     // cross-stream ordering (model broadcast)
+  // overlapped update: per-layer update / collective on `side` while the backward continues
+  // on `stream`; ev_grad[l] = layer l's gradients final, ev_side = side work of the step done
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev_grad;
+  cudaEvent_t ev_side = nullptr;
+  int layer_colls = 0;  // layer collectives launched this step
   double* host_loss = nullptr;  // pinned [kSlots]
 };
 
@@ -182,7 +188,7 @@ class Job {
   int64_t switch_delay_steps() const;
   void resplit();
   std::vector<std::pair<uint64_t, uint64_t>> draw(Worker* w, int64_t need);
-  int run_worker_mlp(Worker* w, int slot);
+  int run_worker_mlp(Worker* w, int slot, bool last);
   int run_worker_linear(Worker* w, int slot);
   int reduce_and_update(uint64_t count, uint64_t t, int slot);
   int step_dry(EdlStepReport* out);
@@ -195,6 +201,16 @@ class Job {
   // (there is nothing to all-reduce); set per step.
   bool fused_update_ = false;
   float step_scale_ = 0.f;
+  // Overlapped update (EDL_OVERLAP, default on): layer l's update (and, with several
+  // replicas, its NVLink reduce-scatter / all-gather) runs on the replica's side stream as
+  // soon as layer l's weight gradients exist, under the rest of the backward pass.
+  bool overlap_ = false;
+  uint64_t step_count_ = 0;
+  uint32_t layer_epoch0_ = 0;  // epoch of the first layer collective of the step
+  int launch_layer_coll(Replica* r, int l);
+  // replica `me` owns slice me/n_rep of every layer (all MLP collectives, checkpoints)
+  void own_segments(int me, int n_rep, CollArgs* a) const;
+  int finish_layer_colls(Replica* r);
   int L_ = 0;
   std::vector<int> in_, out_;
   std::vector<size_t> off_;

@@ -78,6 +78,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, uint64_
       : "memory");
 }
 
+// L2 prefetch of one tensor-map box: no shared memory, no barrier; used to hide HBM latency
+// of operands that are read again a few microseconds later by tma_load_2d.
+__device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
@@ -154,6 +163,17 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const void* tmap, uin
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
+// 2-SM multicast TMA load: the box lands at the same smem offset in every CTA of `mask`;
+// each destination's bytes are counted on its own pair leader's mbarrier.
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* dst, const void* tmap, uint64_t* bar,
+                                                   int c0, int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
+      "h"(mask)
       : "memory");
 }
 __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* src, int c0, int c1) {

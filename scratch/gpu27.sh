@@ -1,0 +1,6 @@
+export PYTHONUNBUFFERED=1
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/ov_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/ov_pytest.log; tail -3 gpurun_out/ov_pytest.log
+for ov in 1 0; do EDL_OVERLAP=$ov timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu > gpurun_out/ov$ov.log 2>&1; python -c "
+import json; d=json.loads(open('gpurun_out/ov$ov.log').read().strip().splitlines()[-1]); print('overlap', $ov, round(d['value']), d['ms_per_step'], {k: round(v*1e3,1) for k,v in d['phase_ms_per_step'].items()})"; done
+for ov in 1 0; do EDL_OVERLAP=$ov timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 30 --warmup 5 --no-cpu > gpurun_out/ov2_$ov.log 2>&1; python -c "
+import json; d=json.loads(open('gpurun_out/ov2_$ov.log').read().strip().splitlines()[-1]); print('N=2 overlap', $ov, round(d['value']), d['ms_per_step'], {k: round(v*1e3,1) for k,v in d['phase_ms_per_step'].items()})"; done

@@ -58,3 +58,29 @@ def test_gemm_relu_mask_bf16(bn):
     out = _gemm(A, 0, B, 0, M, N, K, relu=1, mask=mask, bn=bn)
     ref = torch.relu(_ref(A, 0, B, 0)) * (mask.float() > 0)
     assert torch.allclose(out.float(), ref.bfloat16().float(), rtol=2e-2, atol=2e-1)
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 128, 64), (1024, 1024, 512), (4096, 4096, 512),
+                                   (384, 640, 192)])
+def test_wgrad_sgd_fused(M, N, K):
+    """dW = dY^T X fused with master -= scale * bf16(dW), W = bf16(master) (mlp.cu update)."""
+    from paper_1909_11985_b200 import _lib
+    L = _lib.lib()
+    torch.manual_seed(2)
+    dy = torch.randn(K, M).to(torch.bfloat16).cuda()
+    x = torch.randn(K, N).to(torch.bfloat16).cuda()
+    master = torch.randn(M, N, device="cuda")
+    m0 = master.clone()
+    W = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    scale = 1e-3
+    rc = L.edl_gemm_wgrad_sgd(dy.data_ptr(), M, x.data_ptr(), N, master.data_ptr(), W.data_ptr(),
+                              N, M, N, K, C.c_float(scale),
+                              C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    _lib.check(rc)
+    torch.cuda.synchronize()
+    g = (dy.float().t() @ x.float()).bfloat16().float()
+    ref = m0 - scale * g
+    # bf16 rounding of the fp32 accumulator can differ by 1 ulp where the sums differ in order
+    tol = scale * g.abs().max().item() * 2 ** -7 + 1e-6
+    assert (master - ref).abs().max().item() <= tol
+    assert torch.equal(W, master.bfloat16())
