@@ -178,7 +178,111 @@ __global__ void __launch_bounds__(256) master_allgather_kernel(CollArgs a) {
   cross_replica_barrier(a, 1);
 }
 
+__device__ __forceinline__ uint32_t* ce_flag(uint32_t* base, int kind, int layer, int src) {
+  return base + kCollBarrierWords +
+         (static_cast<size_t>(kind) * kCollMaxSegs + layer) * kCollMaxReplicas + src;
+}
+
+__global__ void ce_signal_kernel(CeSignal a) {
+  __threadfence_system();  // the copies before this kernel (stream order) are performed
+  for (int r = 0; r < a.n_rep; ++r)
+    if (r != a.me) st_release_sys(ce_flag(a.flags[r], a.kind, a.layer, a.me), a.epoch);
+}
+
+__global__ void ce_wait_kernel(CeWait a) {
+  uint32_t* base = const_cast<uint32_t*>(a.flags);
+  for (int l = a.l_lo; l < a.l_hi; ++l)
+    for (int r = 0; r < a.n_rep; ++r) {
+      if (r == a.me) continue;
+      const uint32_t* f = ce_flag(base, a.kind, l, r);
+      const uint64_t t0 = clock64();
+      while (static_cast<int32_t>(ld_acquire_sys(f) - a.epoch) < 0) {
+        __nanosleep(64);
+        if (clock64() - t0 > (1ull << 36)) __trap();  // a peer died: fail, don't hang
+      }
+    }
+  __threadfence_system();
+}
+
+template <bool kMomentum>
+__global__ void __launch_bounds__(256) shard_update_kernel(ShardUpdateArgs a) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < a.n8;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float gs[8];
+    bf16x8_to_f32(__ldcs(reinterpret_cast<const uint4*>(a.src[0]) + i), gs);
+    for (int k = 1; k < a.n_src; ++k) {
+      float t[8];
+      bf16x8_to_f32(__ldcs(reinterpret_cast<const uint4*>(a.src[k]) + i), t);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) gs[e] = __fadd_rn(gs[e], t[e]);
+    }
+    float4* mp = reinterpret_cast<float4*>(a.master) + 2 * i;
+    const float4 m0 = __ldcs(mp), m1 = __ldcs(mp + 1);
+    float m[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+    if (kMomentum) {
+      float4* vp = reinterpret_cast<float4*>(a.mom) + 2 * i;
+      const float4 v0 = __ldcs(vp), v1 = __ldcs(vp + 1);
+      float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        v[e] = __fadd_rn(__fmul_rn(a.mu, v[e]), __fmul_rn(gs[e], a.inv_count));
+        m[e] = __fsub_rn(m[e], __fmul_rn(a.eta, v[e]));
+      }
+      __stcs(vp, make_float4(v[0], v[1], v[2], v[3]));
+      __stcs(vp + 1, make_float4(v[4], v[5], v[6], v[7]));
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) m[e] = __fsub_rn(m[e], __fmul_rn(a.scale, gs[e]));
+    }
+    __stcs(mp, make_float4(m[0], m[1], m[2], m[3]));
+    __stcs(mp + 1, make_float4(m[4], m[5], m[6], m[7]));
+    uint4 o;
+    __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) oh[k] = __floats2bfloat162_rn(m[2 * k], m[2 * k + 1]);
+    reinterpret_cast<uint4*>(a.W)[i] = o;
+  }
+}
+
+__global__ void stamp_kernel(unsigned long long* dst) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *dst = t;
+}
+
 }  // namespace
+
+int stamp(unsigned long long* dst, cudaStream_t s) {
+  stamp_kernel<<<1, 1, 0, s>>>(dst);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
+
+int ce_signal(const CeSignal& a, cudaStream_t s) {
+  if (a.n_rep <= 1) return EDL_OK;
+  ce_signal_kernel<<<1, 1, 0, s>>>(a);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
+
+int ce_wait(const CeWait& a, cudaStream_t s) {
+  if (a.n_rep <= 1 || a.l_hi <= a.l_lo) return EDL_OK;
+  ce_wait_kernel<<<1, 1, 0, s>>>(a);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
+
+int shard_update(const ShardUpdateArgs& a, cudaStream_t s) {
+  if (a.n8 == 0) return EDL_OK;
+  if (a.n_src < 1 || a.n_src > kCollMaxSources) return fail(EDL_EINVAL, "shard_update: sources");
+  const int blocks = a.blocks > 0 ? a.blocks : coll_blocks();
+  if (a.mu != 0.0f)
+    shard_update_kernel<true><<<blocks, 256, 0, s>>>(a);
+  else
+    shard_update_kernel<false><<<blocks, 256, 0, s>>>(a);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
 
 int master_allgather(const CollArgs& a, cudaStream_t s) {
   master_allgather_kernel<<<coll_blocks(), 256, 0, s>>>(a);

@@ -12,8 +12,11 @@ constexpr int kCollMaxReplicas = 8;   // GPUs in one NVLink domain
 constexpr int kCollMaxSources = 16;   // ring members contributing gradients
 constexpr int kCollMaxBlocks = 1024;  // >= coll_blocks()
 constexpr int kCollMaxSegs = 64;      // owned parameter segments (one per MLP layer)
-// Flag buffer per replica: [2 phases][kCollMaxBlocks][kCollMaxReplicas] uint32.
-constexpr size_t kCollFlagBytes = 2ull * kCollMaxBlocks * kCollMaxReplicas * sizeof(uint32_t);
+// Flag buffer per replica: barrier flags [2 phases][kCollMaxBlocks][kCollMaxReplicas], then
+// copy-engine overlap flags [2 kinds][kCollMaxSegs layers][kCollMaxReplicas] (uint32 each).
+constexpr size_t kCollBarrierWords = 2ull * kCollMaxBlocks * kCollMaxReplicas;
+constexpr size_t kCeFlagWords = 2ull * kCollMaxSegs * kCollMaxReplicas;
+constexpr size_t kCollFlagBytes = (kCollBarrierWords + kCeFlagWords) * sizeof(uint32_t);
 
 struct CollArgs {
   const __nv_bfloat16* grads[kCollMaxSources];  // ring order; local or peer pointers
@@ -57,7 +60,40 @@ struct LinearCollArgs {
   uint32_t epoch = 0;
 };
 
+// Copy-engine overlapped collective (runtime.cpp launch_layer_ce): NVLink transfers are
+// cudaMemcpyAsync peer copies (no SM time, so they run under the backward GEMMs); these
+// kernels only signal / wait on flags and apply the sharded update.
+//   kind 0: "my gradient slices of layer l are in your recv buffer"
+//   kind 1: "my updated bf16 weights of layer l are in your W"
+struct CeSignal {
+  uint32_t* flags[kCollMaxReplicas];  // every replica's flag buffer (peer-mapped)
+  int n_rep = 1, me = 0, kind = 0, layer = 0;
+  uint32_t epoch = 0;
+};
+struct CeWait {
+  const uint32_t* flags = nullptr;  // this replica's flag buffer
+  int n_rep = 1, me = 0, kind = 0, l_lo = 0, l_hi = 0;  // layers [l_lo, l_hi)
+  uint32_t epoch = 0;
+};
+// master[i] -= scale * sum_k src[k][i] (ring order, fp32 adds of bf16 terms; momentum with
+// mu != 0), W[i] = bf16(master[i]), for one owned segment of n8 * 8 parameters.
+struct ShardUpdateArgs {
+  const __nv_bfloat16* src[kCollMaxSources];
+  int n_src = 0;
+  float* master = nullptr;
+  float* mom = nullptr;
+  __nv_bfloat16* W = nullptr;
+  size_t n8 = 0;
+  float scale = 0.f, inv_count = 0.f, eta = 0.f, mu = 0.f;
+  int blocks = 0;
+};
+int ce_signal(const CeSignal& a, cudaStream_t s);
+int ce_wait(const CeWait& a, cudaStream_t s);
+int shard_update(const ShardUpdateArgs& a, cudaStream_t s);
+
 int coll_blocks();
+// Debug timeline: one thread writes %globaltimer (ns) to dst (mapped pinned host memory).
+int stamp(unsigned long long* dst, cudaStream_t s);
 int allreduce_sgd(const CollArgs& a, cudaStream_t s);
 int replica_barrier(const CollArgs& a, cudaStream_t s);
 int linear_allreduce_sgd(const LinearCollArgs& a, cudaStream_t s);

@@ -22,6 +22,7 @@
 #include "runtime.hpp"
 
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -137,6 +138,7 @@ int Job::init(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
     me.W = r->W;
     me.master = r->master;
     me.flags = r->flags;
+    me.recv = r->recv;
     me.rep = r;
     peers_.push_back(me);
   }
@@ -221,6 +223,7 @@ void Job::rebuild_peers() {
     p.W = r->W;
     p.master = r->master;
     p.flags = r->flags;
+    p.recv = r->recv;
     p.rep = r.get();
     v.push_back(p);
   }
@@ -241,6 +244,12 @@ int Job::build_replica(Replica* r) {
   EDL_CUDA_TRY(cudaEventCreateWithFlags(&r->ev_sync, cudaEventDisableTiming));
   if (mlp_) {
     EDL_CUDA_TRY(cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking));
+    EDL_CUDA_TRY(cudaStreamCreateWithFlags(&r->side2, cudaStreamNonBlocking));
+    EDL_CUDA_TRY(cudaStreamCreateWithFlags(&r->side3, cudaStreamNonBlocking));
+    r->ev_rs.assign(static_cast<size_t>(L_), nullptr);
+    for (auto& e : r->ev_rs) EDL_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    r->ev_upd.assign(static_cast<size_t>(L_), nullptr);
+    for (auto& e : r->ev_upd) EDL_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     EDL_CUDA_TRY(cudaEventCreateWithFlags(&r->ev_side, cudaEventDisableTiming));
     r->ev_grad.assign(static_cast<size_t>(L_), nullptr);
     for (auto& e : r->ev_grad) EDL_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -255,6 +264,7 @@ int Job::build_replica(Replica* r) {
   if (mlp_) {
     EDL_TRY(dalloc(&r->master, P_));
     EDL_TRY(dalloc(&r->W, P_));
+    EDL_TRY(dalloc(&r->recv, P_));
     if (cfg_.momentum != 0.0) {
       EDL_TRY(dalloc(&r->mom, P_));
       EDL_CUDA_TRY(cudaMemset(r->mom, 0, sizeof(float) * P_));
@@ -321,6 +331,7 @@ void Job::free_replica(Replica* r) {
   dataset_destroy(r->ds);
   cudaFree(r->master);
   cudaFree(r->W);
+  cudaFree(r->recv);
   cudaFree(r->mom);
   cudaFree(r->flags);
   for (auto* a : r->act) cudaFree(a);
@@ -345,6 +356,17 @@ void Job::free_replica(Replica* r) {
   cudaEventDestroy(r->ev_sync);
   for (auto e : r->ev_grad) cudaEventDestroy(e);
   r->ev_grad.clear();
+  for (auto e : r->ev_rs) cudaEventDestroy(e);
+  r->ev_rs.clear();
+  for (auto e : r->ev_upd) cudaEventDestroy(e);
+  r->ev_upd.clear();
+  for (cudaStream_t* st : {&r->side2, &r->side3}) {
+    if (*st) {
+      cudaStreamSynchronize(*st);
+      cudaStreamDestroy(*st);
+    }
+    *st = nullptr;
+  }
   if (r->ev_side) cudaEventDestroy(r->ev_side);
   if (r->side) {
     cudaStreamSynchronize(r->side);
@@ -648,6 +670,7 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
 // several replicas it is the fused NVLink collective restricted to layer l's parameters;
 // the shard boundaries, epochs and launch order are the same on every replica.
 int Job::launch_layer_coll(Replica* r, int l) {
+  if (overlap_mode_ == 2) return launch_layer_ce(r, l);
   EDL_CUDA_TRY(cudaEventRecord(r->ev_grad[l], r->stream));
   EDL_CUDA_TRY(cudaStreamWaitEvent(r->side, r->ev_grad[l], 0));
   const int n_rep = static_cast<int>(peers_.size());
@@ -685,6 +708,160 @@ int Job::launch_layer_coll(Replica* r, int l) {
   return EDL_OK;
 }
 
+int Job::host_index(const std::string& id) const {
+  const Worker* w = workers_.at(id).get();
+  for (size_t i = 0; i < peers_.size(); ++i) {
+    if (!w->remote && peers_[i].local && peers_[i].rep == w->rep) return static_cast<int>(i);
+    if (w->remote && peers_[i].rank == w->host_rank) return static_cast<int>(i);
+  }
+  return -1;
+}
+
+size_t Job::shard8(int l, int p, size_t* lo) const {
+  size_t a, b;
+  shard_range(static_cast<size_t>(in_[l]) * out_[l] / 8, static_cast<int>(peers_.size()), p, &a,
+              &b);
+  if (lo) *lo = a;
+  return b - a;
+}
+
+size_t Job::shard_total8(int p) const {
+  size_t t = 0;
+  for (int l = 0; l < L_; ++l) t += shard8(l, p, nullptr);
+  return t;
+}
+
+size_t Job::seg_off8(int p, int l) const {
+  size_t t = 0;
+  for (int k = 0; k < l; ++k) t += shard8(k, p, nullptr);
+  return t;
+}
+
+// Replica p's recv buffer holds one slot (its whole shard) per ring member hosted elsewhere,
+// in ring order.
+int Job::recv_slot(int p, size_t k) const {
+  int j = 0;
+  for (size_t i = 0; i < k; ++i)
+    if (host_index(ring_[i]) != p) ++j;
+  return j;
+}
+
+bool Job::ce_fits() const {
+  for (size_t p = 0; p < peers_.size(); ++p) {
+    if (!peers_[p].recv || !peers_[p].W) return false;
+    size_t remote = 0;
+    for (const auto& id : ring_) {
+      const int h = host_index(id);
+      if (h < 0) return false;
+      if (h != static_cast<int>(p)) ++remote;
+    }
+    if (remote * shard_total8(static_cast<int>(p)) * 8 > P_) return false;
+  }
+  return ring_.size() <= static_cast<size_t>(kCollMaxSources);
+}
+
+// Layer l with copy-engine transfers, on the replica's side stream:
+//   push my members' gradient slices of layer l owned by each peer into that peer's recv
+//   (cudaMemcpyAsync over NVLink), signal; wait for every peer's slices of my shard; apply
+//   the ring-order sum + SGD to my shard (shard_update); push my updated bf16 weights of the
+//   shard into every peer's W, signal.  The NVLink bytes are the reduce-scatter +
+//   all-gather lower bound, moved by the copy engines while the SMs run the backward.
+void Job::ce_mark(const std::string& what, cudaStream_t s) {
+  if (!ce_trace_ || ce_marks_.size() >= 256) return;
+  if (!ce_stamps_ && cudaHostAlloc(&ce_stamps_, 256 * sizeof(unsigned long long),
+                                   cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+    return;
+  stamp(ce_stamps_ + ce_marks_.size(), s);
+  ce_marks_.push_back(what);
+}
+
+int Job::launch_layer_ce(Replica* r, int l) {
+  // side2: reduce-scatter pushes of layer l (as soon as its gradients exist); side: the
+  // update + all-gather of layer l, pipelined against layer l-1's pushes
+  EDL_CUDA_TRY(cudaEventRecord(r->ev_grad[l], r->stream));
+  ce_mark("L" + std::to_string(l) + " wgrad done (main)", r->stream);
+  EDL_CUDA_TRY(cudaStreamWaitEvent(r->side2, r->ev_grad[l], 0));
+  const int n_rep = static_cast<int>(peers_.size());
+  const int me = rep_index(r);
+  const size_t base = off_[l];
+  for (int p = 0; p < n_rep; ++p) {
+    if (p == me) continue;
+    size_t lo;
+    const size_t n8 = shard8(l, p, &lo);
+    if (n8 == 0) continue;
+    const size_t slot8 = shard_total8(p);
+    for (size_t k = 0; k < ring_.size(); ++k) {
+      if (host_index(ring_[k]) != me) continue;
+      __nv_bfloat16* dst =
+          peers_[p].recv + (static_cast<size_t>(recv_slot(p, k)) * slot8 + seg_off8(p, l)) * 8;
+      const __nv_bfloat16* src = workers_[ring_[k]]->grad + base + lo * 8;
+      EDL_CUDA_TRY(cudaMemcpyAsync(dst, src, n8 * 16, cudaMemcpyDeviceToDevice, r->side2));
+    }
+  }
+  CeSignal sg;
+  for (int p = 0; p < n_rep; ++p) sg.flags[p] = peers_[p].flags;
+  sg.n_rep = n_rep;
+  sg.me = me;
+  sg.kind = 0;
+  sg.layer = l;
+  sg.epoch = ce_epoch_;
+  EDL_TRY(ce_signal(sg, r->side2));
+  ce_mark("L" + std::to_string(l) + " RS pushed (side2)", r->side2);
+  EDL_CUDA_TRY(cudaEventRecord(r->ev_rs[l], r->side2));
+  EDL_CUDA_TRY(cudaStreamWaitEvent(r->side, r->ev_rs[l], 0));
+  CeWait cw;
+  cw.flags = r->flags;
+  cw.n_rep = n_rep;
+  cw.me = me;
+  cw.kind = 0;
+  cw.l_lo = l;
+  cw.l_hi = l + 1;
+  cw.epoch = ce_epoch_;
+  EDL_TRY(ce_wait(cw, r->side));
+  ce_mark("L" + std::to_string(l) + " peers' RS in (side)", r->side);
+
+  size_t lo;
+  const size_t n8 = shard8(l, me, &lo);
+  ShardUpdateArgs u;
+  const size_t slot8 = shard_total8(me), seg8 = seg_off8(me, l);
+  for (size_t k = 0; k < ring_.size(); ++k) {
+    if (host_index(ring_[k]) == me)
+      u.src[u.n_src++] = workers_[ring_[k]]->grad + base + lo * 8;
+    else
+      u.src[u.n_src++] = r->recv + (static_cast<size_t>(recv_slot(me, k)) * slot8 + seg8) * 8;
+  }
+  u.master = r->master + base + lo * 8;
+  u.mom = r->mom ? r->mom + base + lo * 8 : nullptr;
+  u.W = r->W + base + lo * 8;
+  u.n8 = n8;
+  const double eta_t = cfg_.eta / (1.0 + cfg_.decay * static_cast<double>(t_));
+  u.scale = static_cast<float>(eta_t / static_cast<double>(step_count_));
+  u.inv_count = static_cast<float>(1.0 / static_cast<double>(step_count_));
+  u.eta = static_cast<float>(eta_t);
+  u.mu = static_cast<float>(cfg_.momentum);
+  static int ublocks = -1;  // few CTAs: the update shares the SMs with the backward GEMMs
+  if (ublocks < 0) {
+    const char* e = getenv("EDL_CE_UPDATE_BLOCKS");
+    ublocks = e ? atoi(e) : 148;
+  }
+  u.blocks = ublocks;
+  EDL_TRY(shard_update(u, r->side));
+  ce_mark("L" + std::to_string(l) + " update done (side)", r->side);
+  EDL_CUDA_TRY(cudaEventRecord(r->ev_upd[l], r->side));
+  EDL_CUDA_TRY(cudaStreamWaitEvent(r->side3, r->ev_upd[l], 0));
+  for (int p = 0; p < n_rep; ++p) {
+    if (p == me || n8 == 0) continue;
+    EDL_CUDA_TRY(cudaMemcpyAsync(peers_[p].W + base + lo * 8, r->W + base + lo * 8, n8 * 16,
+                                 cudaMemcpyDeviceToDevice, r->side3));
+  }
+  sg.kind = 1;
+  EDL_TRY(ce_signal(sg, r->side3));
+  ce_mark("L" + std::to_string(l) + " AG pushed (side3)", r->side3);
+  ++r->layer_colls;
+  launches_ += 4;
+  return EDL_OK;
+}
+
 void Job::own_segments(int me, int n_rep, CollArgs* a) const {
   a->n_seg = 0;
   for (int l = 0; l < L_; ++l) {
@@ -704,6 +881,21 @@ int Job::finish_layer_colls(Replica* r) {
   while (r->layer_colls < want) {
     const int l = L_ - 1 - r->layer_colls;  // layers go L-1 .. 0 (fused: .. 1)
     EDL_TRY(launch_layer_coll(r, l));
+  }
+  if (overlap_mode_ == 2) {  // every peer's weights of every layer have landed here
+    EDL_CUDA_TRY(cudaEventRecord(r->ev_rs[0], r->side3));  // reuse: side3 drained
+    EDL_CUDA_TRY(cudaStreamWaitEvent(r->side, r->ev_rs[0], 0));
+    CeWait cw;
+    cw.flags = r->flags;
+    cw.n_rep = static_cast<int>(peers_.size());
+    cw.me = rep_index(r);
+    cw.kind = 1;
+    cw.l_lo = 0;
+    cw.l_hi = L_;
+    cw.epoch = ce_epoch_;
+    EDL_TRY(ce_wait(cw, r->side));
+    ce_mark("all AG in (side)", r->side);
+    launches_ += 1;
   }
   EDL_CUDA_TRY(cudaEventRecord(r->ev_side, r->side));
   EDL_CUDA_TRY(cudaStreamWaitEvent(r->stream, r->ev_side, 0));
@@ -988,11 +1180,40 @@ int Job::step(EdlStepReport* out) {
     const char* e = getenv("EDL_OVERLAP");
     overlap_env = e ? atoi(e) : 0;
   }
-  overlap_ = mlp_ && count > 0 && overlap_env != 0;
+  // overlapped update (EDL_OVERLAP=1: side-stream collective kernels per layer, 2: copy-engine
+  // transfers per layer).  Off by default: measured on B200 the
+  // single fused collective after the backward is as fast at N=2 and faster at N=4, because
+  // the overlapped transfers / update kernels slow the backward GEMMs they share the GPU with.
+  overlap_mode_ = 0;
+  if (mlp_ && count > 0 && overlap_env > 0) {
+    overlap_mode_ = (peers_.size() > 1 || overlap_env == 1) ? overlap_env : 0;
+    if (overlap_mode_ == 2 && !ce_fits()) overlap_mode_ = 1;
+  }
+  overlap_ = overlap_mode_ != 0;
   step_count_ = count;
-  if (overlap_) {  // every process reserves the same epochs for the layer collectives
+  if (overlap_mode_ == 1) {  // every process reserves the same epochs for the layer collectives
     layer_epoch0_ = coll_epoch_ + 1;
     coll_epoch_ += static_cast<uint32_t>(fused_update_ ? L_ - 1 : L_);
+  }
+  if (overlap_mode_ == 2) ++ce_epoch_;  // same on every process
+  static int trace_env = -1;
+  if (trace_env < 0) {
+    const char* e = getenv("EDL_CE_TRACE");
+    trace_env = e ? atoi(e) : 0;
+  }
+  ce_trace_ = trace_env != 0 && overlap_mode_ == 2;
+  if (ce_trace_) {  // print the previous step's timeline, start this one's
+    if (!ce_marks_.empty()) {
+      for (auto& [dev, rr] : reps_) {
+        DeviceGuard g(dev);
+        cudaStreamSynchronize(rr->stream);
+      }
+      for (size_t i = 0; i < ce_marks_.size(); ++i)
+        fprintf(stderr, "[ce-trace rank %d] %8.1f us  %s\n", my_rank_,
+                1e-3 * static_cast<double>(ce_stamps_[i] - ce_stamps_[0]), ce_marks_[i].c_str());
+      ce_marks_.clear();
+    }
+    ce_mark("step begin (main)", prim->stream);
   }
   std::map<Replica*, Worker*> last_on;  // last local worker of each replica, in ring order
   for (const auto& id : ring_) {
@@ -1313,6 +1534,7 @@ int Job::export_handles(std::vector<uint8_t>* out) const {
   EDL_TRY(w.handle(r->W));
   EDL_TRY(w.handle(r->master));
   EDL_TRY(w.handle(r->flags));
+  EDL_TRY(w.handle(r->recv));
   uint32_t n = 0;
   for (const auto& [id, wk] : workers_) n += wk->remote ? 0 : 1;
   w.pod(n);
@@ -1352,6 +1574,8 @@ int Job::import_handles(const uint8_t* blob, size_t len) {
   peer.master = static_cast<float*>(p);
   EDL_TRY(open(&p));
   peer.flags = static_cast<uint32_t*>(p);
+  EDL_TRY(open(&p));
+  peer.recv = static_cast<__nv_bfloat16*>(p);
   const uint32_t n = rd.pod<uint32_t>();
   for (uint32_t i = 0; i < n && rd.ok; ++i) {
     const std::string id = rd.text();
@@ -1360,6 +1584,7 @@ int Job::import_handles(const uint8_t* blob, size_t len) {
       return fail(EDL_UNKNOWN_WORKER, "import: " + id + " is not a remote member of this ring");
     Worker* w = it->second.get();
     w->imported = true;
+    w->host_rank = peer.rank;
     EDL_TRY(open(&p));
     w->grad = static_cast<__nv_bfloat16*>(p);
     EDL_TRY(open(&p));

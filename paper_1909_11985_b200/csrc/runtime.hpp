@@ -72,6 +72,11 @@ struct Replica {
   // overlapped update: per-layer update / collective on `side` while the backward continues
   // on `stream`; ev_grad[l] = layer l's gradients final, ev_side = side work of the step done
   cudaStream_t side = nullptr;
+  // copy-engine mode: side2 = reduce-scatter pushes, side = shard updates, side3 =
+  // all-gather pushes; ev_rs[l] / ev_upd[l] order them per layer
+  cudaStream_t side2 = nullptr, side3 = nullptr;
+  std::vector<cudaEvent_t> ev_rs, ev_upd;
+  __nv_bfloat16* recv = nullptr;  // [P]: peers' gradient slices of the shard this replica owns
   std::vector<cudaEvent_t> ev_grad;
   cudaEvent_t ev_side = nullptr;
   int layer_colls = 0;  // layer collectives launched this step
@@ -82,6 +87,7 @@ struct Worker {
   std::string id;
   bool remote = false;    // hosted by another process; buffers below are IPC-mapped
   bool imported = false;  // remote worker whose handles have been imported
+  int host_rank = -1;     // remote worker: PeerRep::rank of the process hosting it
   Replica* rep = nullptr;
   __nv_bfloat16* grad = nullptr;  // MLP gradient sum [P]
   double* g = nullptr;            // linear [grad_sum, count] (dim + 1)
@@ -124,6 +130,7 @@ struct PeerRep {
   __nv_bfloat16* W = nullptr;
   float* master = nullptr;
   uint32_t* flags = nullptr;
+  __nv_bfloat16* recv = nullptr;
   Replica* rep = nullptr;  // local replicas
 };
 
@@ -205,6 +212,20 @@ class Job {
   // replicas, its NVLink reduce-scatter / all-gather) runs on the replica's side stream as
   // soon as layer l's weight gradients exist, under the rest of the backward pass.
   bool overlap_ = false;
+  int overlap_mode_ = 0;  // 1: side-stream collective kernels, 2: copy-engine transfers
+  uint32_t ce_epoch_ = 0;
+  int host_index(const std::string& id) const;  // peers_ index of the replica hosting id
+  size_t shard8(int l, int p, size_t* lo) const;  // replica p's slice of layer l (units of 8)
+  size_t shard_total8(int p) const;
+  size_t seg_off8(int p, int l) const;
+  int recv_slot(int p, size_t k) const;  // k-th ring member's slot in replica p's recv
+  bool ce_fits() const;
+  int launch_layer_ce(Replica* r, int l);
+  // EDL_CE_TRACE=1: timing events of one step's overlapped transfers, printed by sync()
+  bool ce_trace_ = false;
+  std::vector<std::string> ce_marks_;
+  unsigned long long* ce_stamps_ = nullptr;  // mapped pinned [256]
+  void ce_mark(const std::string& what, cudaStream_t s);
   uint64_t step_count_ = 0;
   uint32_t layer_epoch0_ = 0;  // epoch of the first layer collective of the step
   int launch_layer_coll(Replica* r, int l);
