@@ -289,6 +289,22 @@ void edl_job_set_profile(EdlJob* job, int32_t on);
 void edl_job_counters(const EdlJob* job, double* phase_ms, uint64_t* steps, uint64_t* launches);
 void edl_job_reset_counters(EdlJob* job);
 
+/* Straggler detection ("longer than 1.2 times of the median
+ * for 10 mini-batches"): durations[n_batches][n_workers] (NaN = worker absent); *worker =
+ * the lowest index whose duration exceeds factor x the per-batch median (strict) in each
+ * of the last `window` batches, else -1.                                                */
+int edl_detect_straggler(const double* durations, int32_t n_batches, int32_t n_workers,
+                         int32_t window, double factor, int32_t* worker);
+/* The job's own statistics: device time of each worker's share of a mini-batch (gather to
+ * end of backward), the last 64 completed steps.  edl_job_straggler writes the straggler's
+ * id ("" if none) into buf.  edl_job_set_worker_delay injects a slowdown of `us`
+ * microseconds per mini-batch into one worker (PAPER.md:529's straggler experiment).     */
+int edl_job_worker_ms(const EdlJob* job, const char* worker, double* out, size_t cap,
+                      size_t* n);
+int edl_job_straggler(const EdlJob* job, int32_t window, double factor, char* buf, size_t cap,
+                      size_t* len);
+int edl_job_set_worker_delay(EdlJob* job, const char* worker, double us);
+
 /* Weight-gradient GEMM with sgd_step (trainer.cpp:56-61) fused into its epilogue, for a job
  * with a single replica: dW[M][N] = dy^T x (dy row-major [K][ld_dy], x row-major [K][ld_x]),
  * then master -= scale * bf16(dW) and W (bf16) <- master.  No gradient buffer is written. */

@@ -159,6 +159,10 @@ def _declare(L: C.CDLL) -> None:
         "edl_job_gather_master": ([vp], ci),
         "edl_job_set_params": ([vp, vp, sz], ci),
         "edl_gemm_wgrad_sgd": ([vp, i32, vp, i32, vp, vp, i32, i32, i32, i32, C.c_float, vp], ci),
+        "edl_detect_straggler": ([P(f64), i32, i32, i32, f64, P(i32)], ci),
+        "edl_job_worker_ms": ([vp, cp, P(f64), sz, P(sz)], ci),
+        "edl_job_straggler": ([vp, i32, f64, vp, sz, P(sz)], ci),
+        "edl_job_set_worker_delay": ([vp, cp, f64], ci),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)  # AttributeError = the library lacks a declared entry point

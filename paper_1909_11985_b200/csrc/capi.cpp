@@ -377,3 +377,32 @@ int edl_job_gather_master(EdlJob* job) {
   return guarded([&]() -> int { return job->job->gather_master(); });
 }
 }  // extern "C"
+
+extern "C" {
+int edl_detect_straggler(const double* durations, int32_t n_batches, int32_t n_workers,
+                         int32_t window, double factor, int32_t* worker) {
+  return guarded([&]() -> int {
+    if (!worker || (n_batches > 0 && n_workers > 0 && !durations))
+      return edl::fail(EDL_EINVAL, "detect_straggler: null argument");
+    *worker = edl::detect_straggler(durations, n_batches, n_workers, window, factor);
+    return EDL_OK;
+  });
+}
+int edl_job_worker_ms(const EdlJob* job, const char* worker, double* out, size_t cap,
+                      size_t* n) {
+  return guarded([&]() -> int {
+    std::vector<double> v;
+    job->job->worker_ms(worker, &v);
+    if (n) *n = v.size();
+    if (out) std::memcpy(out, v.data(), sizeof(double) * (v.size() < cap ? v.size() : cap));
+    return EDL_OK;
+  });
+}
+int edl_job_straggler(const EdlJob* job, int32_t window, double factor, char* buf, size_t cap,
+                      size_t* len) {
+  return guarded([&]() -> int { return copy_text(job->job->straggler(window, factor), buf, cap, len); });
+}
+int edl_job_set_worker_delay(EdlJob* job, const char* worker, double us) {
+  return guarded([&]() -> int { return job->job->set_worker_delay(worker, us); });
+}
+}  // extern "C"

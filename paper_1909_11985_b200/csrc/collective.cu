@@ -250,7 +250,22 @@ __global__ void stamp_kernel(unsigned long long* dst) {
   *dst = t;
 }
 
+__global__ void spin_kernel(uint64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(256);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 }  // namespace
+
+int spin(uint64_t ns, cudaStream_t s) {
+  spin_kernel<<<1, 1, 0, s>>>(ns);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
 
 int stamp(unsigned long long* dst, cudaStream_t s) {
   stamp_kernel<<<1, 1, 0, s>>>(dst);

@@ -94,6 +94,8 @@ int shard_update(const ShardUpdateArgs& a, cudaStream_t s);
 int coll_blocks();
 // Debug timeline: one thread writes %globaltimer (ns) to dst (mapped pinned host memory).
 int stamp(unsigned long long* dst, cudaStream_t s);
+// One thread busy-waits `ns` nanoseconds of %globaltimer (injected straggler delay).
+int spin(uint64_t ns, cudaStream_t s);
 int allreduce_sgd(const CollArgs& a, cudaStream_t s);
 int replica_barrier(const CollArgs& a, cudaStream_t s);
 int linear_allreduce_sgd(const LinearCollArgs& a, cudaStream_t s);

@@ -310,6 +310,10 @@ int Job::build_worker(Worker* w, Replica* r) {
     EDL_TRY(dalloc(&w->grad, P_));
   else
     EDL_TRY(dalloc(&w->g, static_cast<size_t>(cfg_.data.dim) + 1));
+  for (int s = 0; s < kSlots; ++s) {
+    EDL_CUDA_TRY(cudaEventCreate(&w->ev_w0[s]));
+    EDL_CUDA_TRY(cudaEventCreate(&w->ev_w1[s]));
+  }
   return EDL_OK;
 }
 
@@ -321,6 +325,11 @@ void Job::free_worker(Worker* w) {
   cudaFree(w->loss);
   cudaFree(w->grad);
   cudaFree(w->g);
+  for (int s = 0; s < kSlots; ++s) {
+    if (w->ev_w0[s]) cudaEventDestroy(w->ev_w0[s]);
+    if (w->ev_w1[s]) cudaEventDestroy(w->ev_w1[s]);
+    w->ev_w0[s] = w->ev_w1[s] = nullptr;
+  }
   w->rep = nullptr;
 }
 
@@ -629,10 +638,12 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
   DeviceGuard dg(r->device);
   const bool prof = profile_ && r == primary();
   const int64_t rows = static_cast<int64_t>(w->plan.size());
+  EDL_CUDA_TRY(cudaEventRecord(w->ev_w0[slot], r->stream));
   EDL_CUDA_TRY(cudaMemsetAsync(w->loss, 0, sizeof(double), r->stream));
   if (rows == 0) {  // ShardPending for the whole step: contributes a zero gradient
     EDL_CUDA_TRY(cudaMemsetAsync(w->grad, 0, sizeof(__nv_bfloat16) * P_, r->stream));
     if (overlap_ && last) EDL_TRY(finish_layer_colls(r));
+    EDL_CUDA_TRY(cudaEventRecord(w->ev_w1[slot], r->stream));
     return EDL_OK;
   }
   EDL_TRY(ensure_plans(w, rows));
@@ -658,6 +669,11 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
       if (overlap_ && last) EDL_TRY(launch_layer_coll(r, l));
     }
   }
+  if (w->delay_us > 0) {
+    EDL_TRY(spin(static_cast<uint64_t>(w->delay_us * 1e3), r->stream));
+    launches_ += 1;
+  }
+  EDL_CUDA_TRY(cudaEventRecord(w->ev_w1[slot], r->stream));
   if (overlap_ && last) EDL_TRY(finish_layer_colls(r));
   m = mark(slot, 3, m, r->stream);
   (void)m;
@@ -766,6 +782,67 @@ bool Job::ce_fits() const {
 //   the ring-order sum + SGD to my shard (shard_update); push my updated bf16 weights of the
 //   shard into every peer's W, signal.  The NVLink bytes are the reduce-scatter +
 //   all-gather lower bound, moved by the copy engines while the SMs run the backward.
+int Job::set_worker_delay(const std::string& id, double us) {
+  auto it = workers_.find(id);
+  if (it == workers_.end()) return fail(EDL_UNKNOWN_WORKER, "set_worker_delay: unknown worker " + id);
+  if (!(us >= 0.0)) return fail(EDL_EINVAL, "set_worker_delay: negative delay");
+  it->second->delay_us = us;
+  return EDL_OK;
+}
+
+int Job::worker_ms(const std::string& id, std::vector<double>* out) const {
+  out->clear();
+  for (const auto& step : wtimes_)
+    for (const auto& [wid, ms] : step)
+      if (wid == id) out->push_back(ms);
+  return EDL_OK;
+}
+
+std::string Job::straggler(int window, double factor) const {
+  if (window < 1 || wtimes_.size() < static_cast<size_t>(window)) return "";
+  std::vector<std::string> ids;
+  std::vector<double> dur;  // [window][ids.size()], NaN = absent
+  const size_t first = wtimes_.size() - static_cast<size_t>(window);
+  for (size_t b = first; b < wtimes_.size(); ++b)
+    for (const auto& [id, ms] : wtimes_[b])
+      if (std::find(ids.begin(), ids.end(), id) == ids.end()) ids.push_back(id);
+  dur.assign(static_cast<size_t>(window) * ids.size(), std::nan(""));
+  for (size_t b = first; b < wtimes_.size(); ++b)
+    for (const auto& [id, ms] : wtimes_[b]) {
+      const size_t k = static_cast<size_t>(std::find(ids.begin(), ids.end(), id) - ids.begin());
+      dur[(b - first) * ids.size() + k] = ms;
+    }
+  const int k = detect_straggler(dur.data(), window, static_cast<int>(ids.size()), window, factor);
+  return k >= 0 ? ids[static_cast<size_t>(k)] : "";
+}
+
+// worker k is a straggler if in each of the last `window`
+// mini-batches its duration exceeds factor x that mini-batch's median over the workers
+// present (strict inequality; median of an even count = mean of the middle two).  Returns
+// the lowest such index, or -1.  durations: [n_batches][n_workers], NaN = absent.
+int detect_straggler(const double* dur, int n_batches, int n_workers, int window, double factor) {
+  if (window < 1 || n_batches < window || n_workers < 1) return -1;
+  std::vector<int> hits(static_cast<size_t>(n_workers), 0);
+  for (int b = n_batches - window; b < n_batches; ++b) {
+    std::vector<double> v;
+    for (int k = 0; k < n_workers; ++k) {
+      const double d = dur[static_cast<size_t>(b) * n_workers + k];
+      if (!std::isnan(d)) v.push_back(d);
+    }
+    if (v.empty()) return -1;
+    std::sort(v.begin(), v.end());
+    const size_t m = v.size();
+    const double med = (m % 2) ? v[m / 2] : 0.5 * (v[m / 2 - 1] + v[m / 2]);
+    for (int k = 0; k < n_workers; ++k) {
+      const double d = dur[static_cast<size_t>(b) * n_workers + k];
+      if (!std::isnan(d) && d > factor * med) ++hits[static_cast<size_t>(k)];
+    }
+  }
+  for (int k = 0; k < n_workers; ++k)
+    if (hits[static_cast<size_t>(k)] == window) return k;
+  return -1;
+}
+
 void Job::ce_mark(const std::string& what, cudaStream_t s) {
   if (!ce_trace_ || ce_marks_.size() >= 256) return;
   if (!ce_stamps_ && cudaHostAlloc(&ce_stamps_, 256 * sizeof(unsigned long long),
@@ -906,6 +983,7 @@ int Job::run_worker_linear(Worker* w, int slot) {
   Replica* r = w->rep;
   DeviceGuard dg(r->device);
   const int64_t rows = static_cast<int64_t>(w->plan.size());
+  EDL_CUDA_TRY(cudaEventRecord(w->ev_w0[slot], r->stream));
   cudaEvent_t m = (profile_ && r == primary()) ? mark_begin(r->stream) : nullptr;
   if (rows > 0) {
     EdlRun* host = w->runs_host + static_cast<size_t>(slot) * w->runs_cap;
@@ -922,6 +1000,11 @@ int Job::run_worker_linear(Worker* w, int slot) {
                             r->stream));
   m = mark(slot, 2, m, r->stream);
   (void)m;
+  if (w->delay_us > 0) {
+    EDL_TRY(spin(static_cast<uint64_t>(w->delay_us * 1e3), r->stream));
+    launches_ += 1;
+  }
+  EDL_CUDA_TRY(cudaEventRecord(w->ev_w1[slot], r->stream));
   launches_ += (rows > 0 ? 2 : 1) + (rows > 0 ? 2 : 1);
   return EDL_OK;
 }
@@ -1082,6 +1165,17 @@ void Job::collect_completed() {
     marks_[p.slot].clear();
     step_ms_.push_back(rep.step_ms);
     if (step_ms_.size() > 64) step_ms_.erase(step_ms_.begin());
+    std::vector<std::pair<std::string, double>> wt;
+    for (const auto& [id, w] : p.timed) {
+      float wms = 0.f;
+      DeviceGuard g(w->rep ? w->rep->device : r->device);
+      if (w->ev_w0[p.slot] &&
+          cudaEventElapsedTime(&wms, w->ev_w0[p.slot], w->ev_w1[p.slot]) == cudaSuccess)
+        wt.emplace_back(id, static_cast<double>(wms));
+      cudaGetLastError();
+    }
+    wtimes_.push_back(std::move(wt));
+    if (wtimes_.size() > kTimeWindow) wtimes_.pop_front();
     last_ = rep;
     inflight_.pop_front();
   }
@@ -1243,7 +1337,11 @@ int Job::step(EdlStepReport* out) {
   slot_end_[slot] = prim->ev_end[slot];
 
   Pending p{prim, t_, slot, count, version_, static_cast<int>(ring_.size()), switched ? 1 : 0,
-            last_end_ != nullptr, last_end_};
+            last_end_ != nullptr, last_end_, {}};
+  for (const auto& id : ring_) {
+    Worker* w = workers_[id].get();
+    if (!w->remote) p.timed.emplace_back(id, w);
+  }
   inflight_.push_back(p);
   last_end_ = prim->ev_end[slot];
 

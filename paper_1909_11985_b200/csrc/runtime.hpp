@@ -88,6 +88,9 @@ struct Worker {
   bool remote = false;    // hosted by another process; buffers below are IPC-mapped
   bool imported = false;  // remote worker whose handles have been imported
   int host_rank = -1;     // remote worker: PeerRep::rank of the process hosting it
+  // device time of this worker's share of each in-flight mini-batch (gather .. backward)
+  cudaEvent_t ev_w0[kSlots] = {}, ev_w1[kSlots] = {};
+  double delay_us = 0.0;  // injected slowdown (straggler experiments)
   Replica* rep = nullptr;
   __nv_bfloat16* grad = nullptr;  // MLP gradient sum [P]
   double* g = nullptr;            // linear [grad_sum, count] (dim + 1)
@@ -104,6 +107,10 @@ struct Worker {
   std::vector<std::pair<uint64_t, uint64_t>> plan;
   int n_runs = 0;
 };
+
+// Straggler rule of SPEC.md:348-356 over a [n_batches][n_workers] duration matrix (NaN =
+// worker absent); returns the worker index or -1 (runtime.cpp).
+int detect_straggler(const double* dur, int n_batches, int n_workers, int window, double factor);
 
 struct Event {
   // scheduler-facing scale_out: switch_t is fixed only once the newcomers report Ready
@@ -221,6 +228,18 @@ class Job {
   int recv_slot(int p, size_t k) const;  // k-th ring member's slot in replica p's recv
   bool ce_fits() const;
   int launch_layer_ce(Replica* r, int l);
+  // per-worker mini-batch durations of the last kTimeWindow completed steps (straggler
+  // detection)
+  static constexpr size_t kTimeWindow = 64;
+  std::deque<std::vector<std::pair<std::string, double>>> wtimes_;
+
+ public:
+  int set_worker_delay(const std::string& id, double us);
+  int worker_ms(const std::string& id, std::vector<double>* out) const;
+  // worker over factor x the per-step median in each of the last `window` steps ("" if none)
+  std::string straggler(int window, double factor) const;
+
+ private:
   // EDL_CE_TRACE=1: timing events of one step's overlapped transfers, printed by sync()
   bool ce_trace_ = false;
   std::vector<std::string> ce_marks_;
@@ -268,6 +287,7 @@ class Job {
     int switched;
     bool have_prev;
     cudaEvent_t prev_end;
+    std::vector<std::pair<std::string, Worker*>> timed;  // local workers of this step
   };
   std::deque<Pending> inflight_;
   std::vector<double> step_ms_;

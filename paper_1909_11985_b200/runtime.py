@@ -32,6 +32,19 @@ def eta_at(eta: float, decay: float, t: int) -> float:  # trainer.hpp:27-29
     return _lib.lib().edl_eta_at(eta, decay, t)
 
 
+def detect_straggler(durations, window: int = 10, factor: float = 1.2):
+    """durations[batch][worker] (NaN = absent) -> index of the worker slower
+    than factor x the per-batch median in each of the last `window` batches, or None."""
+    d = np.ascontiguousarray(durations, dtype=np.float64)
+    if d.ndim != 2:
+        raise ValueError("durations must be [n_batches][n_workers]")
+    out = C.c_int32(-1)
+    _lib.check(_lib.lib().edl_detect_straggler(
+        d.ctypes.data_as(C.POINTER(C.c_double)), d.shape[0], d.shape[1], window, factor,
+        C.byref(out)))
+    return None if out.value < 0 else out.value
+
+
 @dataclass
 class JobConfig:
     model: int = LEAST_SQUARES
@@ -221,3 +234,69 @@ class Job:
         buf = (C.c_uint8 * n.value)()
         self._L.edl_job_lease_snapshot(self._h, buf, n.value, C.byref(n))
         return bytes(buf)
+
+    # ---- straggler mitigation and profiling
+    def worker_ms(self, worker: str) -> list:
+        """Device time of `worker`'s share of each of the last completed mini-batches."""
+        n = C.c_size_t()
+        _lib.check(self._L.edl_job_worker_ms(self._h, worker.encode(), None, 0, C.byref(n)))
+        buf = (C.c_double * max(1, n.value))()
+        _lib.check(self._L.edl_job_worker_ms(self._h, worker.encode(), buf, n.value,
+                                             C.byref(n)))
+        return list(buf[:n.value])
+
+    def straggler(self, window: int = 10, factor: float = 1.2):
+        """Worker over factor x the per-mini-batch median for `window` consecutive mini-batches
+        (the leader's detection rule), or None."""
+        n = C.c_size_t()
+        buf = C.create_string_buffer(256)
+        _lib.check(self._L.edl_job_straggler(self._h, window, factor, buf, 256, C.byref(n)))
+        return buf.value.decode() or None
+
+    def set_worker_delay(self, worker: str, us: float) -> None:
+        """Inject `us` microseconds of extra device time into every mini-batch of `worker`."""
+        _lib.check(self._L.edl_job_set_worker_delay(self._h, worker.encode(), float(us)))
+
+    def mitigate_straggler(self, window: int = 10, factor: float = 1.2,
+                           allowance_ms: float = 30000.0):
+        """Leader action of PAPER.md:418: scale_in the detected straggler (advise-only callers
+        use straggler()).  Returns (worker, switch_t) or None."""
+        w = self.straggler(window, factor)
+        if w is None or len(self.ring()) < 2:
+            return None
+        return w, self.scale_in([w], allowance_ms)
+
+    def profile(self, min_p: int, max_p: int = None, steps: int = 20) -> list:
+        """from the current parallelism (max_p) scale in one worker at a time
+        down to min_p, timing `steps` mini-batches per level.  Returns one dict per level:
+        parallelism p, samples/s S(p) = t(p) * p, per-GPU throughput t(p) and GPU efficiency
+        t(p) / t(p*) with p* = argmax t(p) (PAPER.md:89 footnote)."""
+        ring = self.ring()
+        max_p = len(ring) if max_p is None else max_p
+        if min_p < 1 or min_p > max_p:
+            raise _lib.EdlError(_lib.EDL_EINVAL, "profile: min_p > max_p")
+        if max_p != len(ring):
+            raise _lib.EdlError(_lib.EDL_EINVAL, "profile: the job must run at max_p")
+        levels = []
+        p = max_p
+        while True:
+            self.sync()
+            reps = []
+            for _ in range(steps):
+                self.step()
+                reps.append(self.sync())
+            ms = sorted(r.step_ms for r in reps)[len(reps) // 2]
+            count = sorted(r.count for r in reps)[len(reps) // 2]
+            thr = 1e3 * count / ms if ms > 0 else 0.0
+            levels.append({"p": p, "samples_per_s": thr, "per_gpu": thr / p,
+                           "step_ms": ms, "ring": list(self.ring())})
+            if p <= min_p:
+                break
+            st = self.scale_in([self.ring()[-1]])
+            while self.t <= st:
+                self.step()
+            p -= 1
+        best = max(lv["per_gpu"] for lv in levels) or 1.0
+        for lv in levels:
+            lv["efficiency"] = lv["per_gpu"] / best
+        return levels
