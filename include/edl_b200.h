@@ -40,7 +40,8 @@ enum {
   EDL_ENOMEM = 11,             /* allocation failure                                      */
   EDL_ALLOWANCE_EXCEEDED = 12, /* scale_in leaver missed its allowance      */
   EDL_EIO = 13,                /* std::runtime_error on file I/O (trainer.cpp:104)        */
-  EDL_ETRUNCATED = 14          /* std::runtime_error "truncated payload" (bytes.hpp:112)  */
+  EDL_ETRUNCATED = 14,         /* std::runtime_error "truncated payload" (bytes.hpp:112)  */
+  EDL_NO_CHECKPOINT = 15       /* consistent recovery without a checkpoint  */
 };
 
 const char* edl_last_error(void);
@@ -222,6 +223,8 @@ typedef struct {
   double t_a_ms;             /* switch allowance T_a, default 500             */
   int32_t keep_log;          /* record the assignment log                                  */
   int32_t dry_run;           /* host protocol only (leases, ring, log): no device work      */
+  int32_t appx_recovery;     /* keep the mini-batch boundary state for approximate recovery
+                                (USE_APPX_RECOVERY; default from that env var) */
 } EdlJobConfig;
 
 typedef struct {
@@ -288,6 +291,28 @@ int edl_job_gather_master(EdlJob* job);
 void edl_job_set_profile(EdlJob* job, int32_t on);
 void edl_job_counters(const EdlJob* job, double* phase_ms, uint64_t* steps, uint64_t* launches);
 void edl_job_reset_counters(EdlJob* job);
+
+/* Failure recovery (§4.2).  A checkpoint file holds the
+ * JobCheckpoint fields: fp32 master (or f64 w), momentum, t_cur, topology
+ * version, B and the lease state in the reference snapshot layout (datapipeline.cpp:115);
+ * saving waits for the device.  Loading resumes at its t_cur with the job's current
+ * workers: the checkpointed members' in-flight shards are reclaimed at their offsets,
+ * leavers unregistered, newcomers registered, `restore <t-1>` + `topo` are logged.
+ * edl_job_fail(ids) reports that `ids` failed during the last launched mini-batch:
+ * approximate != 0 (needs cfg.appx_recovery) rolls the model, leases and log back to that
+ * mini-batch's start and redoes it without them; approximate == 0 restores the latest
+ * checkpoint saved by this job with the survivors, or (EDL_NO_CHECKPOINT) restarts them
+ * from the initial state.                                                                 */
+typedef struct {
+  int32_t mode;      /* 1 approximate (redo the mini-batch), 0 consistent (checkpoint)  */
+  int32_t status;    /* EDL_OK, or EDL_NO_CHECKPOINT (restarted from the initial state)  */
+  uint64_t t_resume; /* next mini-batch index                                           */
+  uint64_t version;  /* topology version after recovery                                 */
+} EdlRecovery;
+int edl_job_save_checkpoint(EdlJob* job, const char* path);
+int edl_job_load_checkpoint(EdlJob* job, const char* path);
+int edl_job_fail(EdlJob* job, const char* const* ids, int32_t n, int32_t approximate,
+                 EdlRecovery* out);
 
 /* Straggler detection ("longer than 1.2 times of the median
  * for 10 mini-batches"): durations[n_batches][n_workers] (NaN = worker absent); *worker =

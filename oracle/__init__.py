@@ -75,6 +75,10 @@ class Native:
             "job_ring_size": ([vp], C.c_int),
             "job_plan": ([vp, C.c_int, C.c_char_p, sz, P(u64), P(u64), sz, P(sz)], C.c_int),
             "job_log_text": ([vp, C.c_char_p, sz, P(sz)], C.c_int),
+            "job_snapshot": ([vp], vp),
+            "job_snap_free": ([vp, vp], None),
+            "job_restore": ([vp, vp, cp], None),
+            "job_fail_approximate": ([vp, cp], None),
             "split_batch": ([i64, C.c_int, P(i64)], C.c_int),
             "switch_delay": ([f64, f64], i64),
             "eta_at": ([f64, f64, u64], f64),

@@ -153,12 +153,35 @@ class Job:
             out.append((name.value.decode(), list(zip(ep[:n.value], ids[:n.value]))))
         return out
 
+    # ---- recovery (job_driver.hpp restore / fail_approximate)
+    def snapshot(self) -> "Snapshot":
+        """JobCheckpoint at the current mini-batch boundary (params, t, pipeline state)."""
+        return Snapshot(self, self.n.job_snapshot(self.h))
+
+    def restore(self, snap: "Snapshot", ring) -> None:
+        """Consistent recovery: resume from `snap` with the workers in `ring`."""
+        self.n.job_restore(self.h, snap.h, ",".join(ring).encode())
+
+    def fail_approximate(self, failed) -> None:
+        """Approximate recovery: redo the last mini-batch without the `failed` workers."""
+        self.n.job_fail_approximate(self.h, ",".join(failed).encode())
+
     def log_text(self) -> str:
         ln = C.c_size_t()
         self.n.job_log_text(self.h, None, 0, C.byref(ln))
         buf = C.create_string_buffer(ln.value + 1)
         self.n.job_log_text(self.h, buf, ln.value + 1, C.byref(ln))
         return buf.value.decode()
+
+
+class Snapshot:
+    def __init__(self, job: Job, h):
+        self.job, self.h = job, h
+
+    def __del__(self):
+        if getattr(self, "h", None) and getattr(self.job, "h", None):
+            self.job.n.job_snap_free(self.job.h, self.h)
+            self.h = None
 
 
 def check_coverage(nat: Native, log_text: str, n: int):

@@ -19,7 +19,15 @@
 //     batch for the static-scaling sweeps (BASELINE.json configs[1]);
 //   * per-worker [grad_sum, count] vectors are combined in ring order
 //     (ring_order_reduce == ring_allreduce, allreduce.cpp:60-148) and applied with
-//     sgd_step(eta_at(t)) (trainer.cpp:244-271).
+//     sgd_step(eta_at(t)) (trainer.cpp:244-271);
+//   * failure recovery: consistent = restore a JobCheckpoint (params,
+//     t_cur, pipeline state) with the remaining workers: the lease state is restored, every
+//     checkpointed member's in-flight shards are reclaimed at their reported offsets
+//     (datapipeline.cpp:73-84) so the survivors resume them, leavers are unregistered,
+//     the ring becomes the survivors (version + 1, `restore <t-1>` + `topo` records);
+//     approximate = roll params, leases, cursors and log back to the start of the failed
+//     mini-batch (after its topology install), remove the failed workers as a scale-in
+//     would, and redo that mini-batch.
 #pragma once
 
 #include <algorithm>
@@ -74,6 +82,7 @@ class JobDriver {
   // One mini-batch; returns mean loss over the global batch (0 if empty).
   double step(uint64_t* count_out) {
     install_due();
+    pre_ = snapshot();  // boundary state for approximate recovery
     const size_t p = ring_.size();
     plan_.assign(p, {});
     for (size_t r = 0; r < p; ++r) plan_[r] = draw(ring_[r], splits_[r]);
@@ -111,6 +120,87 @@ class JobDriver {
     ++t_;
     if (count_out) *count_out = count;
     return mean;
+  }
+
+  // State at a mini-batch boundary (JobCheckpoint).
+  struct Snap {
+    uint64_t t = 0, version = 0;
+    std::vector<std::string> ring;
+    std::vector<uint8_t> lease;
+    std::map<std::string, Cursor> cur;
+    std::vector<double> w;
+    size_t log_len = 0;
+  };
+  Snap snapshot() const {
+    Snap s;
+    s.t = t_;
+    s.version = version_;
+    s.ring = ring_;
+    s.lease = lm_.snapshot();
+    s.cur = cur_;
+    s.w = w_;
+    s.log_len = log_.size();
+    return s;
+  }
+
+  // Consistent recovery: resume from checkpoint `s` with workers `ring`.
+  void restore(const Snap& s, std::vector<std::string> ring) {
+    lm_.restore(s.lease.data(), s.lease.size());
+    for (const auto& w : s.ring) {
+      lm_.reclaim(w);
+      if (std::find(ring.begin(), ring.end(), w) == ring.end()) lm_.remove_worker(w);
+    }
+    for (const auto& w : ring)
+      if (std::find(s.ring.begin(), s.ring.end(), w) == s.ring.end()) lm_.add_worker(w);
+    cur_.clear();
+    events_.clear();
+    w_ = s.w;
+    t_ = s.t;
+    ring_ = std::move(ring);
+    version_ = std::max(version_, s.version) + 1;
+    if (t_ > 0) {
+      Rec r;
+      r.kind = Rec::Restore;
+      r.t = t_ - 1;
+      log_.push_back(r);
+    }
+    Rec r;
+    r.kind = Rec::Topo;
+    r.t = t_ == 0 ? 0 : t_ - 1;
+    r.version = version_;
+    r.ring = ring_;
+    log_.push_back(r);
+    resplit();
+  }
+
+  // Approximate recovery: the last mini-batch failed; `failed` leave and it is redone.
+  void fail_approximate(const std::vector<std::string>& failed) {
+    lm_.restore(pre_.lease.data(), pre_.lease.size());
+    cur_ = pre_.cur;
+    w_ = pre_.w;
+    t_ = pre_.t;
+    ring_ = pre_.ring;
+    version_ = pre_.version;
+    log_.resize(pre_.log_len);
+    std::vector<std::string> keep;
+    for (const auto& w : ring_) {
+      if (std::find(failed.begin(), failed.end(), w) != failed.end()) {
+        lm_.reclaim(w);
+        lm_.remove_worker(w);
+        cur_.erase(w);
+      } else {
+        keep.push_back(w);
+      }
+    }
+    ring_ = keep;
+    ++version_;
+    Rec r;
+    r.kind = Rec::Topo;
+    r.t = t_ == 0 ? 0 : t_ - 1;
+    r.version = version_;
+    r.ring = ring_;
+    log_.push_back(r);
+    resplit();
   }
 
   const std::vector<std::string>& ring() const { return ring_; }
@@ -214,6 +304,7 @@ class JobDriver {
   std::vector<Rec> log_;
   uint64_t t_ = 0;
   uint64_t version_ = 1;
+  Snap pre_;
 };
 
 }  // namespace orc

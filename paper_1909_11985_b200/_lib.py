@@ -27,11 +27,13 @@ EDL_ENOMEM = 11
 EDL_ALLOWANCE_EXCEEDED = 12
 EDL_EIO = 13
 EDL_ETRUNCATED = 14
+EDL_NO_CHECKPOINT = 15
 
 STATUS_NAMES = {
     0: "Ok", 1: "Retry", 2: "Invalid", 3: "PeerGone", 4: "Timeout", 5: "VersionMismatch",
     6: "UnknownWorker", 7: "StaleShard", 8: "ShapeMismatch", 9: "OutOfRange", 10: "CudaError",
     11: "OutOfMemory", 12: "AllowanceExceeded", 13: "IOError", 14: "Truncated",
+    15: "NoCheckpoint",
 }
 
 
@@ -85,7 +87,13 @@ class EdlJobConfig(C.Structure):
                 ("decay", C.c_double), ("momentum", C.c_double), ("batch", C.c_int64),
                 ("per_worker_batch", C.c_int64), ("lease_seed", C.c_uint64),
                 ("partitions", C.c_int32), ("max_workers", C.c_int32), ("init_seed", C.c_uint64),
-                ("t_a_ms", C.c_double), ("keep_log", C.c_int32), ("dry_run", C.c_int32)]
+                ("t_a_ms", C.c_double), ("keep_log", C.c_int32), ("dry_run", C.c_int32),
+                ("appx_recovery", C.c_int32)]
+
+
+class EdlRecovery(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("status", C.c_int32), ("t_resume", C.c_uint64),
+                ("version", C.c_uint64)]
 
 
 class EdlStepReport(C.Structure):
@@ -160,6 +168,9 @@ def _declare(L: C.CDLL) -> None:
         "edl_job_set_params": ([vp, vp, sz], ci),
         "edl_gemm_wgrad_sgd": ([vp, i32, vp, i32, vp, vp, i32, i32, i32, i32, C.c_float, vp], ci),
         "edl_detect_straggler": ([P(f64), i32, i32, i32, f64, P(i32)], ci),
+        "edl_job_save_checkpoint": ([vp, cp], ci),
+        "edl_job_load_checkpoint": ([vp, cp], ci),
+        "edl_job_fail": ([vp, cpp, i32, i32, P(EdlRecovery)], ci),
         "edl_job_worker_ms": ([vp, cp, P(f64), sz, P(sz)], ci),
         "edl_job_straggler": ([vp, i32, f64, vp, sz, P(sz)], ci),
         "edl_job_set_worker_delay": ([vp, cp, f64], ci),

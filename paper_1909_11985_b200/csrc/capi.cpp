@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <set>
@@ -270,6 +271,8 @@ void edl_job_config_default(EdlJobConfig* c) {
   c->t_a_ms = 500.0;
   c->keep_log = 1;
   c->dry_run = 0;
+  const char* appx = std::getenv("USE_APPX_RECOVERY");  // SPEC.md:384, default consistent
+  c->appx_recovery = (appx && std::atoi(appx) != 0) ? 1 : 0;
 }
 
 int edl_job_create(const EdlJobConfig* cfg, const char* const* ring, const int32_t* devices,
@@ -404,5 +407,25 @@ int edl_job_straggler(const EdlJob* job, int32_t window, double factor, char* bu
 }
 int edl_job_set_worker_delay(EdlJob* job, const char* worker, double us) {
   return guarded([&]() -> int { return job->job->set_worker_delay(worker, us); });
+}
+}  // extern "C"
+
+extern "C" {
+int edl_job_save_checkpoint(EdlJob* job, const char* path) {
+  return guarded([&]() -> int { return job->job->save_checkpoint(path ? path : ""); });
+}
+int edl_job_load_checkpoint(EdlJob* job, const char* path) {
+  return guarded([&]() -> int { return job->job->load_checkpoint(path ? path : ""); });
+}
+int edl_job_fail(EdlJob* job, const char* const* ids, int32_t n, int32_t approximate,
+                 EdlRecovery* out) {
+  return guarded([&]() -> int {
+    std::vector<std::string> v;
+    for (int32_t i = 0; i < n; ++i) v.emplace_back(ids[i]);
+    EdlRecovery r{};
+    const int rc = job->job->recover(v, approximate != 0, &r);
+    if (out) *out = r;
+    return rc;
+  });
 }
 }  // extern "C"

@@ -110,6 +110,8 @@ int Job::init(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
   std::ostringstream loc;
   loc << "synthetic:" << cfg.data.seed << ":" << cfg.data.size;  // dataset.cpp:56-58
   lm_ = std::make_unique<LeaseManager>(cfg.data.size, parts, cfg.lease_seed, loc.str());
+  lm_parts_ = parts;
+  lm_loc_ = loc.str();
   int first_local = -1;
   for (size_t i = 0; i < ring.size(); ++i) {
     if (workers_.count(ring[i])) return fail(EDL_EINVAL, "job: duplicate worker id");
@@ -356,6 +358,11 @@ void Job::free_replica(Replica* r) {
   cudaFree(r->ws);
   cudaFree(r->total);
   cudaFree(r->loss_sum);
+  cudaFree(r->shadow_master);
+  cudaFree(r->shadow_mom);
+  cudaFree(r->shadow_w);
+  r->shadow_master = r->shadow_mom = nullptr;
+  r->shadow_w = nullptr;
   cudaFreeHost(r->host_loss);
   for (int s = 0; s < kSlots; ++s) {
     cudaEventDestroy(r->ev_begin[s]);
@@ -782,6 +789,307 @@ bool Job::ce_fits() const {
 //   the ring-order sum + SGD to my shard (shard_update); push my updated bf16 weights of the
 //   shard into every peer's W, signal.  The NVLink bytes are the reduce-scatter +
 //   all-gather lower bound, moved by the copy engines while the SMs run the backward.
+// ------------------------------------------------------------------ failure recovery
+// SPEC.md:321-329 / PAPER.md §4.2; the oracle (oracle/job_driver.hpp restore /
+// fail_approximate) applies the same lease / ring / log transitions.
+
+int Job::take_pre_snapshot() {
+  pre_.valid = true;
+  pre_.t = t_;
+  pre_.version = version_;
+  pre_.ring = ring_;
+  pre_.lease = lm_->snapshot();
+  pre_.cur.clear();
+  for (const auto& id : ring_) pre_.cur[id] = workers_[id]->cur;
+  pre_.log_len = log_.size();
+  if (dry_) return EDL_OK;
+  for (auto& [dev, r] : reps_) {  // device copy in stream order: the state before this step
+    DeviceGuard g(dev);
+    if (mlp_) {
+      if (!r->shadow_master) EDL_TRY(dalloc(&r->shadow_master, P_));
+      EDL_CUDA_TRY(cudaMemcpyAsync(r->shadow_master, r->master, sizeof(float) * P_,
+                                   cudaMemcpyDeviceToDevice, r->stream));
+      if (r->mom) {
+        if (!r->shadow_mom) EDL_TRY(dalloc(&r->shadow_mom, P_));
+        EDL_CUDA_TRY(cudaMemcpyAsync(r->shadow_mom, r->mom, sizeof(float) * P_,
+                                     cudaMemcpyDeviceToDevice, r->stream));
+      }
+    } else {
+      if (!r->shadow_w) EDL_TRY(dalloc(&r->shadow_w, P_));
+      EDL_CUDA_TRY(cudaMemcpyAsync(r->shadow_w, r->w, sizeof(double) * P_,
+                                   cudaMemcpyDeviceToDevice, r->stream));
+    }
+  }
+  return EDL_OK;
+}
+
+// Immediate scale-in of `ids` (failed workers): shards back at their reported offsets.
+int Job::remove_members(const std::vector<std::string>& ids) {
+  std::vector<std::string> keep;
+  for (const auto& id : ring_) {
+    if (std::find(ids.begin(), ids.end(), id) == ids.end()) {
+      keep.push_back(id);
+      continue;
+    }
+    lm_->reclaim(id);
+    lm_->retire(id);
+    auto it = workers_.find(id);
+    if (!dry_ && !it->second->remote) free_worker(it->second.get());
+    workers_.erase(it);
+  }
+  ring_ = keep;
+  rebuild_peers();
+  return EDL_OK;
+}
+
+namespace {
+constexpr char kCkptMagic[8] = {'E', 'D', 'L', 'C', 'K', 'P', 'T', '1'};
+template <class T>
+void put(std::string* b, const T& v) {
+  b->append(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+template <class T>
+bool get(const std::string& b, size_t* o, T* v) {
+  if (*o + sizeof(T) > b.size()) return false;
+  std::memcpy(v, b.data() + *o, sizeof(T));
+  *o += sizeof(T);
+  return true;
+}
+}  // namespace
+
+int Job::save_checkpoint(const std::string& path) {
+  if (path.empty()) return fail(EDL_EINVAL, "checkpoint: empty path");
+  for (const auto& p : peers_)
+    if (!p.local) return fail(EDL_EINVAL, "checkpoint: multi-process jobs gather first (not supported)");
+  EDL_TRY(sync(nullptr));
+  std::string b(kCkptMagic, 8);
+  put<uint32_t>(&b, 1);  // format version
+  put<int32_t>(&b, cfg_.model);
+  put<uint64_t>(&b, t_);
+  put<uint64_t>(&b, version_);
+  put<int64_t>(&b, cfg_.batch);
+  put<uint64_t>(&b, static_cast<uint64_t>(P_));
+  put<uint32_t>(&b, static_cast<uint32_t>(ring_.size()));
+  for (const auto& id : ring_) {
+    put<uint32_t>(&b, static_cast<uint32_t>(id.size()));
+    b += id;
+  }
+  const std::vector<uint8_t> lease = lm_->snapshot();  // PipelineCheckpoint + RNG state
+  put<uint64_t>(&b, lease.size());
+  b.append(reinterpret_cast<const char*>(lease.data()), lease.size());
+  const size_t esz = mlp_ ? sizeof(float) : sizeof(double);
+  std::vector<char> params(dry_ ? 0 : esz * P_), mom;
+  if (!dry_) {
+    Replica* r = primary();
+    EDL_TRY(consolidate_master());
+    DeviceGuard g(r->device);
+    EDL_CUDA_TRY(cudaStreamSynchronize(r->stream));
+    EDL_CUDA_TRY(cudaMemcpy(params.data(), mlp_ ? static_cast<void*>(r->master)
+                                                : static_cast<void*>(r->w),
+                            params.size(), cudaMemcpyDeviceToHost));
+    if (mlp_ && r->mom) {
+      mom.resize(sizeof(float) * P_);
+      EDL_CUDA_TRY(cudaMemcpy(mom.data(), r->mom, mom.size(), cudaMemcpyDeviceToHost));
+    }
+  }
+  put<uint64_t>(&b, params.size());
+  b.append(params.data(), params.size());
+  put<uint64_t>(&b, mom.size());
+  b.append(mom.data(), mom.size());
+  FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) return fail(EDL_EIO, "checkpoint: cannot open " + path);
+  const bool ok = std::fwrite(b.data(), 1, b.size(), f) == b.size();
+  if (std::fclose(f) != 0 || !ok) return fail(EDL_EIO, "checkpoint: write failed " + path);
+  last_ckpt_ = path;
+  return EDL_OK;
+}
+
+int Job::load_checkpoint(const std::string& path) {
+  for (const auto& p : peers_)
+    if (!p.local) return fail(EDL_EINVAL, "checkpoint: multi-process restore not supported");
+  if (!events_.empty()) return fail(EDL_RETRY, "checkpoint: a scaling operation is pending");
+  std::string b;
+  {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) return fail(EDL_EIO, "checkpoint: cannot open " + path);
+    char buf[1 << 16];
+    size_t n;
+    while ((n = std::fread(buf, 1, sizeof(buf), f)) > 0) b.append(buf, n);
+    std::fclose(f);
+  }
+  size_t o = 8;
+  if (b.size() < 8 || std::memcmp(b.data(), kCkptMagic, 8) != 0)
+    return fail(EDL_EINVAL, "checkpoint: not an edl checkpoint");
+  uint32_t fmt = 0, nring = 0;
+  int32_t model = 0;
+  uint64_t t = 0, version = 0, P = 0, llen = 0, plen = 0, mlen = 0;
+  int64_t B = 0;
+  bool ok = get(b, &o, &fmt) && get(b, &o, &model) && get(b, &o, &t) && get(b, &o, &version) &&
+            get(b, &o, &B) && get(b, &o, &P) && get(b, &o, &nring);
+  std::vector<std::string> ring;
+  for (uint32_t i = 0; ok && i < nring; ++i) {
+    uint32_t len = 0;
+    ok = get(b, &o, &len) && o + len <= b.size();
+    if (ok) ring.emplace_back(b.data() + o, len);
+    o += len;
+  }
+  ok = ok && get(b, &o, &llen) && o + llen <= b.size();
+  const size_t lease_at = o;
+  o += ok ? llen : 0;
+  ok = ok && get(b, &o, &plen) && o + plen <= b.size();
+  const size_t params_at = o;
+  o += ok ? plen : 0;
+  ok = ok && get(b, &o, &mlen) && o + mlen <= b.size();
+  const size_t mom_at = o;
+  if (!ok || fmt != 1) return fail(EDL_ETRUNCATED, "checkpoint: truncated payload");
+  if (model != cfg_.model || P != P_ || B != cfg_.batch)
+    return fail(EDL_SHAPE_MISMATCH, "checkpoint: model / size / batch differ from the job");
+  const size_t esz = mlp_ ? sizeof(float) : sizeof(double);
+  if (!dry_ && plen != esz * P_) return fail(EDL_SHAPE_MISMATCH, "checkpoint: parameter bytes");
+  EDL_TRY(sync(nullptr));
+  // parameters (every replica; MLP bf16 weights re-derived from the master)
+  if (!dry_) {
+    EDL_TRY(set_params(b.data() + params_at, plen));
+    for (auto& [dev, r] : reps_) {
+      if (!r->mom) continue;
+      DeviceGuard g(dev);
+      if (mlen == sizeof(float) * P_)
+        EDL_CUDA_TRY(cudaMemcpy(r->mom, b.data() + mom_at, mlen, cudaMemcpyHostToDevice));
+      else
+        EDL_CUDA_TRY(cudaMemset(r->mom, 0, sizeof(float) * P_));
+    }
+  }
+  // pipeline: lease state as checkpointed; the checkpointed members' in-flight shards go
+  // back to the reclaimed queue at their offsets (their cursors are gone), leavers retire
+  const LeaseStatus ls = lm_->restore(reinterpret_cast<const uint8_t*>(b.data()) + lease_at, llen);
+  if (ls != LeaseStatus::Ok) return fail(EDL_SHAPE_MISMATCH, "checkpoint: lease state rejected");
+  for (const auto& id : ring) {
+    lm_->reclaim(id);
+    if (std::find(ring_.begin(), ring_.end(), id) == ring_.end()) lm_->retire(id);
+  }
+  for (const auto& id : ring_)
+    if (std::find(ring.begin(), ring.end(), id) == ring.end()) lm_->enroll(id);
+  for (auto& [id, w] : workers_) w->cur = Cursor{};
+  t_ = t;
+  version_ = std::max(version_, version) + 1;
+  pre_.valid = false;
+  if (cfg_.keep_log) {
+    if (t_ > 0) {
+      LogRec r;
+      r.kind = LogRec::Restore;
+      r.t = t_ - 1;
+      log_.push_back(r);
+    }
+    LogRec r;
+    r.kind = LogRec::Topo;
+    r.t = t_ == 0 ? 0 : t_ - 1;
+    r.version = version_;
+    r.ring = ring_;
+    log_.push_back(r);
+  }
+  resplit();
+  return EDL_OK;
+}
+
+int Job::recover(const std::vector<std::string>& failed, bool approximate, EdlRecovery* out) {
+  for (const auto& p : peers_)
+    if (!p.local) return fail(EDL_EINVAL, "recover: multi-process recovery not supported");
+  size_t hit = 0;
+  for (const auto& id : failed) hit += std::count(ring_.begin(), ring_.end(), id);
+  if (hit == 0 || hit != failed.size()) return fail(EDL_UNKNOWN_WORKER, "recover: not ring members");
+  if (hit >= ring_.size()) return fail(EDL_EINVAL, "recover: no surviving worker");
+  if (!events_.empty()) return fail(EDL_RETRY, "recover: a scaling operation is pending");
+  EDL_TRY(sync(nullptr));
+  *out = EdlRecovery{};
+  out->mode = approximate ? 1 : 0;
+  out->status = EDL_OK;
+  if (approximate) {
+    if (!cfg_.appx_recovery || !pre_.valid)
+      return fail(EDL_EINVAL, "recover: approximate recovery needs cfg.appx_recovery");
+    // model: back to the boundary state (every replica restores its own copy; the sharded
+    // master is made whole before the membership change re-shards it)
+    if (!dry_) {
+      for (auto& [dev, r] : reps_) {
+        DeviceGuard g(dev);
+        if (mlp_) {
+          EDL_CUDA_TRY(cudaMemcpyAsync(r->master, r->shadow_master, sizeof(float) * P_,
+                                       cudaMemcpyDeviceToDevice, r->stream));
+          if (r->mom)
+            EDL_CUDA_TRY(cudaMemcpyAsync(r->mom, r->shadow_mom, sizeof(float) * P_,
+                                         cudaMemcpyDeviceToDevice, r->stream));
+        } else {
+          EDL_CUDA_TRY(cudaMemcpyAsync(r->w, r->shadow_w, sizeof(double) * P_,
+                                       cudaMemcpyDeviceToDevice, r->stream));
+        }
+      }
+      EDL_TRY(consolidate_master());
+      if (mlp_)
+        for (auto& [dev, r] : reps_) {
+          DeviceGuard g(dev);
+          EDL_TRY(master_to_bf16(r->master, r->W, P_, r->stream));
+        }
+    }
+    // pipeline and protocol state: back to the start of the failed mini-batch
+    if (lm_->restore(pre_.lease.data(), pre_.lease.size()) != LeaseStatus::Ok)
+      return fail(EDL_EINVAL, "recover: lease rollback failed");
+    for (const auto& id : ring_) {
+      auto it = pre_.cur.find(id);
+      workers_[id]->cur = it == pre_.cur.end() ? Cursor{} : it->second;
+    }
+    if (log_.size() > pre_.log_len) log_.resize(pre_.log_len);
+    t_ = pre_.t;
+    version_ = pre_.version;
+    pre_.valid = false;
+    EDL_TRY(remove_members(failed));
+  } else {
+    EDL_TRY(remove_members(failed));
+    if (!last_ckpt_.empty()) {
+      EDL_TRY(load_checkpoint(last_ckpt_));
+      out->t_resume = t_;
+      out->version = version_;
+      return EDL_OK;
+    }
+    // no checkpoint: the survivors restart from the initial state
+    out->status = EDL_NO_CHECKPOINT;
+    lm_ = std::make_unique<LeaseManager>(cfg_.data.size, lm_parts_, cfg_.lease_seed, lm_loc_);
+    for (const auto& id : ring_) {
+      lm_->enroll(id);
+      workers_[id]->cur = Cursor{};
+    }
+    if (!dry_) {
+      for (auto& [dev, r] : reps_) {
+        DeviceGuard g(dev);
+        if (mlp_) {
+          for (int l = 0; l < L_; ++l) {
+            const double bound = std::sqrt(6.0 / static_cast<double>(in_[l]));
+            EDL_TRY(mlp_init_weights(r->master + off_[l], r->W + off_[l],
+                                     static_cast<size_t>(in_[l]) * out_[l], cfg_.init_seed,
+                                     off_[l], bound, r->stream));
+          }
+          if (r->mom) EDL_CUDA_TRY(cudaMemsetAsync(r->mom, 0, sizeof(float) * P_, r->stream));
+        } else {
+          EDL_CUDA_TRY(cudaMemsetAsync(r->w, 0, sizeof(double) * P_, r->stream));
+        }
+      }
+    }
+    t_ = 0;
+    if (cfg_.keep_log) log_.clear();
+  }
+  ++version_;
+  if (cfg_.keep_log) {
+    LogRec r;
+    r.kind = LogRec::Topo;
+    r.t = t_ == 0 ? 0 : t_ - 1;
+    r.version = version_;
+    r.ring = ring_;
+    log_.push_back(r);
+  }
+  resplit();
+  out->t_resume = t_;
+  out->version = version_;
+  return EDL_OK;
+}
+
 int Job::set_worker_delay(const std::string& id, double us) {
   auto it = workers_.find(id);
   if (it == workers_.end()) return fail(EDL_UNKNOWN_WORKER, "set_worker_delay: unknown worker " + id);
@@ -1203,6 +1511,7 @@ double Job::median_step_ms() const {
 int Job::step_dry(EdlStepReport* out) {
   bool switched = false;
   EDL_TRY(install_due(&switched));
+  if (cfg_.appx_recovery) EDL_TRY(take_pre_snapshot());
   uint64_t count = 0;
   for (size_t k = 0; k < ring_.size(); ++k) {
     Worker* w = workers_[ring_[k]].get();
@@ -1243,6 +1552,7 @@ int Job::step(EdlStepReport* out) {
   EDL_TRY(install_due(&switched));
   Replica* prim = primary();
   DeviceGuard g(prim->device);
+  if (cfg_.appx_recovery) EDL_TRY(take_pre_snapshot());
 
   // protocol step 2: lease draws in ring order, runs for the gather kernel
   uint64_t count = 0;

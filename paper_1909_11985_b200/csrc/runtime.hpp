@@ -64,6 +64,10 @@ struct Replica {
   double* ws = nullptr;
   double* total = nullptr;
   double* loss_sum = nullptr;
+  // approximate recovery: parameters at the start of the last launched mini-batch
+  float* shadow_master = nullptr;
+  float* shadow_mom = nullptr;
+  double* shadow_w = nullptr;
   // per-step events
   cudaEvent_t ev_begin[kSlots] = {};
   cudaEvent_t ev_end[kSlots] = {};
@@ -233,7 +237,26 @@ class Job {
   static constexpr size_t kTimeWindow = 64;
   std::deque<std::vector<std::pair<std::string, double>>> wtimes_;
 
+  // approximate recovery: host state at the start of the last launched mini-batch
+  struct HostSnap {
+    bool valid = false;
+    uint64_t t = 0, version = 0;
+    std::vector<std::string> ring;
+    std::vector<uint8_t> lease;
+    std::map<std::string, Cursor> cur;
+    size_t log_len = 0;
+  };
+  HostSnap pre_;
+  int lm_parts_ = 0;
+  std::string lm_loc_;
+  std::string last_ckpt_;  // latest checkpoint written by this job (consistent recovery)
+  int take_pre_snapshot();
+  int remove_members(const std::vector<std::string>& ids);  // immediate scale-in
+
  public:
+  int save_checkpoint(const std::string& path);
+  int load_checkpoint(const std::string& path);
+  int recover(const std::vector<std::string>& failed, bool approximate, EdlRecovery* out);
   int set_worker_delay(const std::string& id, double us);
   int worker_ms(const std::string& id, std::vector<double>* out) const;
   // worker over factor x the per-step median in each of the last `window` steps ("" if none)

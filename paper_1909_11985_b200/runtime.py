@@ -7,6 +7,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -68,6 +69,8 @@ class JobConfig:
     t_a_ms: float = 500.0
     keep_log: bool = True
     dry_run: bool = False
+    appx_recovery: bool = field(
+        default_factory=lambda: os.environ.get("USE_APPX_RECOVERY", "0") not in ("", "0"))
 
     def to_c(self) -> _lib.EdlJobConfig:
         c = _lib.EdlJobConfig()
@@ -80,6 +83,7 @@ class JobConfig:
         c.lease_seed, c.partitions, c.max_workers = self.lease_seed, self.partitions, self.max_workers
         c.init_seed, c.t_a_ms, c.keep_log = self.init_seed, self.t_a_ms, int(self.keep_log)
         c.dry_run = int(self.dry_run)
+        c.appx_recovery = int(bool(self.appx_recovery))
         return c
 
 
@@ -300,3 +304,28 @@ class Job:
         for lv in levels:
             lv["efficiency"] = lv["per_gpu"] / best
         return levels
+
+    # ---- failure recovery (§4.2)
+    def save_checkpoint(self, path: str) -> None:
+        """JobCheckpoint (params, momentum, t_cur, version, B, lease state) to `path`."""
+        _lib.check(self._L.edl_job_save_checkpoint(self._h, os.fsencode(path)))
+
+    def load_checkpoint(self, path: str) -> None:
+        """Resume from `path` with the job's current workers (consistent recovery)."""
+        _lib.check(self._L.edl_job_load_checkpoint(self._h, os.fsencode(path)))
+
+    def fail(self, ids, approximate: bool = None) -> dict:
+        """`ids` failed during the last launched mini-batch.  approximate (default:
+        JobConfig.appx_recovery): roll back to that mini-batch's start and redo it without
+        them; otherwise resume the survivors from the latest checkpoint (status
+        "NoCheckpoint": restarted from the initial state)."""
+        if approximate is None:
+            approximate = self.cfg.appx_recovery
+        arr = _lib.cstrs(ids)
+        out = _lib.EdlRecovery()
+        rc = self._L.edl_job_fail(self._h, arr, len(ids), 1 if approximate else 0,
+                                  C.byref(out))
+        _lib.check(rc)
+        return {"mode": "approximate" if out.mode else "consistent",
+                "status": _lib.STATUS_NAMES.get(out.status, out.status),
+                "t_resume": out.t_resume, "version": out.version}
