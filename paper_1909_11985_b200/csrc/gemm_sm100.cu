@@ -108,6 +108,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue above overlaps the previous kernel's tail (PDL); every CTA of this persistent
+  // grid is resident, so dependents may launch now and run their own prologue
+  griddep_wait();
+  griddep_launch();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -407,6 +411,8 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (warp == 1) TL(1);
+  griddep_wait();  // see gemm_bf16_tn_kernel
+  griddep_launch();
 
   // Producer and MMA loops run warp-uniform (all 32 lanes wait on the barriers; elect.sync
   // picks the issuing lane) so descriptors and coordinates stay in uniform registers and
@@ -836,6 +842,16 @@ int make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, ui
   return make_tmap_t(m, base, rows, cols, ld, 64, box_rows, false);
 }
 
+// Programmatic dependent launch of the GEMMs (EDL_PDL=0 disables, for comparisons).
+static bool gemm_pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("EDL_PDL");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on != 0;
+}
+
 int num_sms() {
   static int n = 0;  // identical B200s: the first device's count holds for all
   if (!n) {
@@ -861,8 +877,17 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
   }
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, kThreads, Cf::kSmemBytes, stream>>>(ta, tb, M, N, K, ep);
-  EDL_CUDA_TRY(cudaGetLastError());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cf::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = gemm_pdl_enabled() ? 1 : 0;
+  EDL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, ep));
   return EDL_OK;
 }
 
@@ -878,11 +903,13 @@ int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream, float scale = 0.f) {
   cfg.blockDim = dim3(Cf::kThreads2);
   cfg.dynamicSmemBytes = Cf::kSmemBytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2 * kMc;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (!(attr_set >> dev & 1)) {
@@ -901,6 +928,7 @@ int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream, float scale = 0.f) {
   if (units > max_units[dev]) units = max_units[dev];
   EpiParams ep = p.ep;
   ep.scale = scale;
+  cfg.numAttrs = gemm_pdl_enabled() ? 2 : 1;
   cfg.gridDim = dim3(2 * kMc * (work < units ? work : units));
   EDL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p.ta, p.tb, p.tc, p.tm, p.M, p.N, p.K, ep));
   return EDL_OK;

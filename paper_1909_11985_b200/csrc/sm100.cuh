@@ -87,6 +87,15 @@ __device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int c0, int c1
                : "memory");
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// wait: block until the grids this one depends on (stream predecessors launched with
+// programmatic serialization) have completed and their writes are visible.  launch: allow
+// the dependents to start launching (their CTAs run their prologue, then wait).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
