@@ -293,7 +293,7 @@ def run_b200(args, rank: int, world: int) -> None:
                      # DRAM read + write per GEMM launch (mean of the 23 GEMM launches of one
                      # mini-batch, ncu --set full, profiles/r01_ncu_full.md); algorithmic
                      # bytes: fwd/dgrad ~40 MB (W once), wgrad+sgd 168 MB (master RMW + W)
-                     "traffic": 67.46e6, "traffic_source": "profiles/r01_ncu_full.md",
+                     "traffic": _ncu_gemm_traffic(), "traffic_source": NCU_FULL,
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                      "per_step_ms": gemm_ms,
                      "algorithmic_gflop_per_step": flops * w["batch"] / 1e9},
@@ -310,6 +310,23 @@ def run_b200(args, rank: int, world: int) -> None:
     job.close()
     if dist is not None:
         dist.destroy_process_group()
+
+
+NCU_FULL = "profiles/r01_ncu_full.md"
+
+
+def _ncu_gemm_traffic():
+    """Mean DRAM read + write bytes per GEMM launch in the committed ncu --set full capture."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), NCU_FULL)
+    vals = []
+    try:
+        for line in open(path):
+            cells = [c.strip() for c in line.split("|")]
+            if len(cells) > 5 and "gemm_bf16" in cells[2]:
+                vals.append((float(cells[4]) + float(cells[5])) * 1e6)
+    except (OSError, ValueError):
+        return None
+    return sum(vals) / len(vals) if vals else None
 
 
 def main() -> None:

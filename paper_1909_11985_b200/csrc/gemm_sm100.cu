@@ -334,14 +334,28 @@ struct Cfg2 {
   static constexpr int kThreads2 = 64 + 32 * kEpiWarps;
   // epilogue staging per warp: plain 2 x 4 KB; fused SGD kSgdBufs x (8 KB master + 4 KB W)
   static constexpr uint32_t kSgdBufBytes = 3 * kEpiChunkBytes;
+#ifdef EDL_SGD_BUFS
+  static constexpr int kSgdBufs = EDL_SGD_BUFS;
+#else
   static constexpr int kSgdBufs = kEpiWarps == 8 ? 1 : 2;
+#endif
+  // master prefetch distance in chunks (1 .. kSgdBufs - 1)
+#ifdef EDL_SGD_PFD
+  static constexpr int kSgdPfd = EDL_SGD_PFD;
+#else
+  static constexpr int kSgdPfd = kSgdBufs > 1 ? kSgdBufs - 1 : 0;
+#endif
   static constexpr uint32_t kEpiBytes =
       kSgd ? kEpiWarps * kSgdBufs * kSgdBufBytes : 4 * 2 * kEpiChunkBytes;
 #ifndef EDL_GEMM2_MAX_STAGES
 #define EDL_GEMM2_MAX_STAGES 6
 #endif
   static constexpr int kFit = (224 * 1024 - kEpiBytes) / kStageBytes;
-  static constexpr int kStages = kFit > EDL_GEMM2_MAX_STAGES ? EDL_GEMM2_MAX_STAGES : kFit;
+#ifndef EDL_SGD_STAGES
+#define EDL_SGD_STAGES EDL_GEMM2_MAX_STAGES
+#endif
+  static constexpr int kMaxStages = kSgd ? EDL_SGD_STAGES : EDL_GEMM2_MAX_STAGES;
+  static constexpr int kStages = kFit > kMaxStages ? kMaxStages : kFit;
   static constexpr uint32_t kAccCols = BN;
   static constexpr uint32_t kTmemCols = (2 * kAccCols <= 256) ? 256 : 512;
   static constexpr uint32_t kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 512;
@@ -579,7 +593,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
     };
     if (lane == 0) {
       for (int i = 0; i < ep.pf_tiles; ++i) l2_prefetch_tile(unit + i * n_units);
-      for (int p0 = 0; p0 < (NB > 1 ? NB - 1 : 1) && !skip_epi; ++p0) prefetch(p0);
+      for (int p0 = 0; p0 < (NB > 1 ? C::kSgdPfd : 1) && !skip_epi; ++p0) prefetch(p0);
     }
     int j = 0;
     int local = 0;
@@ -600,9 +614,11 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
         const int b = j % NB;
         if (NB > 1 && lane == 0) {
           TRACE_T0(t_wr);
-          tma_store_wait_read<0>();  // chunk j-1's stores have read the buffer refilled next
+          // the buffer refilled next was last used by chunk j + PD - NB: its stores (and only
+          // those older) must have read it
+          tma_store_wait_read<(NB > 1 ? NB - C::kSgdPfd - 1 : 0)>();
           if (warp == 2) TRACE_ADD(6, t_wr);
-          prefetch(j + NB - 1);
+          prefetch(j + C::kSgdPfd);
         }
         TRACE_T0(t_ld);
         float g[64];
