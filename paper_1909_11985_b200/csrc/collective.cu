@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "collective.hpp"
 #include "edl_internal.hpp"
@@ -78,8 +79,39 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
   }
 }
 
-// 8 parameters per thread-iteration.
+// SGD / momentum on 8 parameters of this replica's shard + bf16 weights to every replica.
 template <bool kMomentum>
+__device__ __forceinline__ void apply8(const CollArgs& a, size_t i, const float (&gs)[8]) {
+  float4* mp = reinterpret_cast<float4*>(a.master) + 2 * i;
+  const float4 m0 = __ldcs(mp), m1 = __ldcs(mp + 1);
+  float m[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+  if (kMomentum) {
+    float4* vp = reinterpret_cast<float4*>(a.mom) + 2 * i;
+    const float4 v0 = __ldcs(vp), v1 = __ldcs(vp + 1);
+    float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      v[e] = __fadd_rn(__fmul_rn(a.mu, v[e]), __fmul_rn(gs[e], a.inv_count));
+      m[e] = __fsub_rn(m[e], __fmul_rn(a.eta, v[e]));
+    }
+    __stcs(vp, make_float4(v[0], v[1], v[2], v[3]));
+    __stcs(vp + 1, make_float4(v[4], v[5], v[6], v[7]));
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) m[e] = __fsub_rn(m[e], __fmul_rn(a.scale, gs[e]));
+  }
+  __stcs(mp, make_float4(m[0], m[1], m[2], m[3]));
+  __stcs(mp + 1, make_float4(m[4], m[5], m[6], m[7]));
+  uint4 o;
+  __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) oh[k] = __floats2bfloat162_rn(m[2 * k], m[2 * k + 1]);
+  for (int d = 0; d < a.n_dst; ++d) reinterpret_cast<uint4*>(a.w_dst[d])[i] = o;
+}
+
+// 8 parameters per thread and unrolled group; kU groups (a grid stride apart) keep kU loads
+// of every source in flight at once (the peer loads are NVLink-latency bound).
+template <bool kMomentum, int kU>
 __global__ void __launch_bounds__(256) allreduce_sgd_kernel(CollArgs a) {
   if (a.n_rep > 1) cross_replica_barrier(a, 0);
   if (a.loss_out && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -87,46 +119,42 @@ __global__ void __launch_bounds__(256) allreduce_sgd_kernel(CollArgs a) {
     for (int k = 0; k < a.n_loss; ++k) acc = __dadd_rn(acc, *a.losses[k]);
     *a.loss_out = acc;
   }
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   const int n_seg = a.update ? (a.n_seg > 0 ? a.n_seg : 1) : 0;
   for (int sg = 0; sg < n_seg; ++sg) {
-  const size_t lo = a.n_seg > 0 ? a.seg_lo8[sg] : a.lo8;
-  const size_t hi = a.n_seg > 0 ? a.seg_hi8[sg] : a.hi8;
-  for (size_t i = lo + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < hi;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    float gs[8];
-    bf16x8_to_f32(__ldcs(reinterpret_cast<const uint4*>(a.grads[0]) + i), gs);
-    for (int k = 1; k < a.n_src; ++k) {
-      float t[8];
-      bf16x8_to_f32(__ldcs(reinterpret_cast<const uint4*>(a.grads[k]) + i), t);
+    const size_t lo = a.n_seg > 0 ? a.seg_lo8[sg] : a.lo8;
+    const size_t hi = a.n_seg > 0 ? a.seg_hi8[sg] : a.hi8;
+    for (size_t i0 = lo + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i0 < hi;
+         i0 += stride * kU) {
+      float gs[kU][8];
+      uint4 t[kU];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) gs[e] = __fadd_rn(gs[e], t[e]);
-    }
-    float4* mp = reinterpret_cast<float4*>(a.master) + 2 * i;
-    const float4 m0 = __ldcs(mp), m1 = __ldcs(mp + 1);
-    float m[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
-    if (kMomentum) {
-      float4* vp = reinterpret_cast<float4*>(a.mom) + 2 * i;
-      const float4 v0 = __ldcs(vp), v1 = __ldcs(vp + 1);
-      float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        v[e] = __fadd_rn(__fmul_rn(a.mu, v[e]), __fmul_rn(gs[e], a.inv_count));
-        m[e] = __fsub_rn(m[e], __fmul_rn(a.eta, v[e]));
+      for (int u = 0; u < kU; ++u) {
+        const size_t i = i0 + u * stride;
+        if (i < hi) t[u] = __ldcs(reinterpret_cast<const uint4*>(a.grads[0]) + i);
       }
-      __stcs(vp, make_float4(v[0], v[1], v[2], v[3]));
-      __stcs(vp + 1, make_float4(v[4], v[5], v[6], v[7]));
-    } else {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) m[e] = __fsub_rn(m[e], __fmul_rn(a.scale, gs[e]));
+      for (int u = 0; u < kU; ++u)
+        if (i0 + u * stride < hi) bf16x8_to_f32(t[u], gs[u]);
+      for (int k = 1; k < a.n_src; ++k) {
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const size_t i = i0 + u * stride;
+          if (i < hi) t[u] = __ldcs(reinterpret_cast<const uint4*>(a.grads[k]) + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          if (i0 + u * stride >= hi) continue;
+          float f[8];
+          bf16x8_to_f32(t[u], f);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) gs[u][e] = __fadd_rn(gs[u][e], f[e]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (i0 + u * stride < hi) apply8<kMomentum>(a, i0 + u * stride, gs[u]);
     }
-    __stcs(mp, make_float4(m[0], m[1], m[2], m[3]));
-    __stcs(mp + 1, make_float4(m[4], m[5], m[6], m[7]));
-    uint4 o;
-    __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) oh[k] = __floats2bfloat162_rn(m[2 * k], m[2 * k + 1]);
-    for (int d = 0; d < a.n_dst; ++d) reinterpret_cast<uint4*>(a.w_dst[d])[i] = o;
-  }
   }
   if (a.n_rep > 1) cross_replica_barrier(a, 1);
 }
@@ -311,12 +339,28 @@ int allreduce_sgd(const CollArgs& a, cudaStream_t s) {
   if (a.n_src < 1 || a.n_src > kCollMaxSources) return fail(EDL_EINVAL, "allreduce_sgd: sources");
   if (a.n_dst < 0 || a.n_dst > kCollMaxReplicas || a.n_rep > kCollMaxReplicas)
     return fail(EDL_EINVAL, "allreduce_sgd: replicas");
-  const int blocks = a.blocks > 0 ? a.blocks : coll_blocks();
+  static int env_blocks = -1, unroll = -1;  // tuning knobs (EDL_COLL_BLOCKS / _UNROLL)
+  if (env_blocks < 0) {
+    const char* e = getenv("EDL_COLL_BLOCKS");
+    env_blocks = e ? atoi(e) : 0;
+    e = getenv("EDL_COLL_UNROLL");
+    unroll = e ? atoi(e) : 2;
+  }
+  int blocks = a.blocks > 0 ? a.blocks : (env_blocks > 0 ? env_blocks : coll_blocks());
   if (blocks > kCollMaxBlocks) return fail(EDL_EINVAL, "allreduce_sgd: grid");
-  if (a.mu != 0.0f)
-    allreduce_sgd_kernel<true><<<blocks, 256, 0, s>>>(a);
-  else
-    allreduce_sgd_kernel<false><<<blocks, 256, 0, s>>>(a);
+  if (a.mu != 0.0f) {
+    if (unroll >= 2)
+      allreduce_sgd_kernel<true, 2><<<blocks, 256, 0, s>>>(a);
+    else
+      allreduce_sgd_kernel<true, 1><<<blocks, 256, 0, s>>>(a);
+  } else {
+    if (unroll >= 4)
+      allreduce_sgd_kernel<false, 4><<<blocks, 256, 0, s>>>(a);
+    else if (unroll >= 2)
+      allreduce_sgd_kernel<false, 2><<<blocks, 256, 0, s>>>(a);
+    else
+      allreduce_sgd_kernel<false, 1><<<blocks, 256, 0, s>>>(a);
+  }
   EDL_CUDA_TRY(cudaGetLastError());
   return EDL_OK;
 }

@@ -10,7 +10,7 @@ namespace edl {
 
 constexpr int kCollMaxReplicas = 8;   // GPUs in one NVLink domain
 constexpr int kCollMaxSources = 16;   // ring members contributing gradients
-constexpr int kCollMaxBlocks = 1024;  // >= coll_blocks()
+constexpr int kCollMaxBlocks = 4096;  // >= coll_blocks() and EDL_COLL_BLOCKS
 constexpr int kCollMaxSegs = 64;      // owned parameter segments (one per MLP layer)
 // Flag buffer per replica: barrier flags [2 phases][kCollMaxBlocks][kCollMaxReplicas], then
 // copy-engine overlap flags [2 kinds][kCollMaxSegs layers][kCollMaxReplicas] (uint32 each).
