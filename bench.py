@@ -213,6 +213,7 @@ def run_b200(args, rank: int, world: int) -> None:
         e1.record(stream)
         torch.cuda.synchronize()
         job.set_profile(False)
+        counters = job.counters()  # phase times and launches of exactly the K timed steps
         barrier()
         t_load = time.time()
         while max_over_ranks(time.time() - t_load) < 0.5:
@@ -220,7 +221,6 @@ def run_b200(args, rank: int, world: int) -> None:
                 job.step()
             job.sync()
     ms = max_over_ranks(e0.elapsed_time(e1))
-    counters = job.counters()
     clocks = clk.summary()
     samples = w["batch"] * args.steps * world
     value = samples / (ms / 1e3)

@@ -38,11 +38,21 @@ struct EpiParams {
   // ahead in the fused-SGD epilogue.  Defaults from gemm_prefetch_defaults().
   int pf_kb;
   int pf_tiles;
+  // reduce-scatter routing of a weight-gradient GEMM (N > 1): output rows are owned in
+  // blocks of route_rows by replica row / route_rows; blocks owned by another replica are
+  // stored through PeerMaps::m[owner] (that replica's receive slot for this one, over NVLink)
+  int route_rows;
+  int route_me;
   int dbg;  // trace builds only: 1 = skip the K loop, 2 = skip the epilogue work
+};
+constexpr int kMaxPeerMaps = 8;
+struct PeerMaps {
+  CUtensorMap m[kMaxPeerMaps];
 };
 // Pre-encoded launch (TMA descriptors built once; launching costs one kernel launch).
 struct GemmPlan {
   CUtensorMap ta, tb, tc, tm;  // tm: fp32 master (fused-SGD plans)
+  PeerMaps pm;                 // reduce-scatter destinations (routed plans)
   int M = 0, N = 0, K = 0, a_mn = 0, b_mn = 0, bn = 0, cg = 1;
   int mc = 1;  // CTA-pair kernel: pairs per cluster sharing A by TMA multicast (1 or 2)
   EpiParams ep{};
@@ -57,6 +67,9 @@ int gemm_plan_run(const GemmPlan& p, cudaStream_t stream, float sgd_scale = 0.f)
 int gemm_plan_init_sgd(GemmPlan* p, const void* A, int lda, int a_mn, const void* B, int ldb,
                        int b_mn, float* master, __nv_bfloat16* W, int ldw, int M, int N, int K);
 int gemm_pick_bn(int M, int N, bool b_mn);
+// Turns a bf16-output CTA-pair plan into a reduce-scatter producer: rows owned by replica o
+// (blocks of rows_per_owner) go to dst[o] ([rows_per_owner][N], ld = N), o != me.
+int gemm_plan_route(GemmPlan* p, int rows_per_owner, int me, void* const* dst, int n_owner);
 int gemm_bf16(const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
               int ldc, int M, int N, int K, int relu, int out_f32, const void* mask, int ldm,
               int bn, cudaStream_t stream);

@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
                          const __grid_constant__ CUtensorMap tmap_b,
                          const __grid_constant__ CUtensorMap tmap_c,
                          const __grid_constant__ CUtensorMap tmap_m, int M, int N, int K,
-                         EpiParams ep) {
+                         EpiParams ep, const __grid_constant__ PeerMaps pm) {
   using C = Cfg2<BN, kSgd>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -784,7 +784,16 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&tmap_c, stage_buf + buf * kEpiChunkBytes, n0 + c, row0);
+          const CUtensorMap* dst = &tmap_c;
+          int drow = row0;
+          if (ep.route_rows > 0) {  // reduce-scatter: the owner's receive slot, over NVLink
+            const int owner = row0 / ep.route_rows;
+            if (owner != ep.route_me) {
+              dst = &pm.m[owner];
+              drow = row0 - owner * ep.route_rows;
+            }
+          }
+          tma_store_2d(dst, stage_buf + buf * kEpiChunkBytes, n0 + c, drow);
           tma_store_commit();
         }
         if (warp == 2 && local == 0) {
@@ -946,7 +955,7 @@ int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream, float scale = 0.f) {
   ep.scale = scale;
   cfg.numAttrs = gemm_pdl_enabled() ? 2 : 1;
   cfg.gridDim = dim3(2 * kMc * (work < units ? work : units));
-  EDL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p.ta, p.tb, p.tc, p.tm, p.M, p.N, p.K, ep));
+  EDL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p.ta, p.tb, p.tc, p.tm, p.M, p.N, p.K, ep, p.pm));
   return EDL_OK;
 }
 
@@ -1076,6 +1085,25 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B,
   p->b_mn = b_mn;
   p->bn = bn;
   p->ep = EpiParams{Cout, static_cast<const __nv_bfloat16*>(mask), ldc, ldm, relu, out_f32, 0, 0.f};
+  return EDL_OK;
+}
+
+int gemm_plan_route(GemmPlan* p, int rows_per_owner, int me, void* const* dst, int n_owner) {
+  if (p->cg != 2 || p->ep.out_f32 || p->ep.mask || p->ep.sgd)
+    return fail(EDL_EINVAL, "gemm route: needs a plain bf16 CTA-pair plan");
+  if (n_owner < 1 || n_owner > kMaxPeerMaps || rows_per_owner <= 0 || rows_per_owner % 32 ||
+      rows_per_owner * n_owner != p->M || me < 0 || me >= n_owner)
+    return fail(EDL_EINVAL, "gemm route: owner blocks must tile M in 32-row multiples");
+  for (int o = 0; o < n_owner; ++o) {
+    if (o == me) {
+      p->pm.m[o] = p->tc;
+      continue;
+    }
+    const int rc = make_tmap_t(&p->pm.m[o], dst[o], rows_per_owner, p->N, p->N, 64, 32, false);
+    if (rc) return fail(rc, "gemm route: tensor map of a peer receive slot");
+  }
+  p->ep.route_rows = rows_per_owner;
+  p->ep.route_me = me;
   return EDL_OK;
 }
 

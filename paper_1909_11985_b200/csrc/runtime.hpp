@@ -104,6 +104,9 @@ struct Worker {
   int64_t runs_cap = 0;
   std::vector<GemmPlan> wgrad;
   std::vector<GemmPlan> wgrad_sgd;  // fused weight-gradient + SGD (single-member ring)
+  std::vector<GemmPlan> wgrad_rs;   // weight gradient + reduce-scatter into the owners' recv
+  int64_t rs_plan_rows = -1;
+  uint64_t rs_plan_version = 0;
   int64_t plan_rows = -1;
   int64_t sgd_plan_rows = -1;
   Cursor cur;
@@ -223,7 +226,11 @@ class Job {
   // replicas, its NVLink reduce-scatter / all-gather) runs on the replica's side stream as
   // soon as layer l's weight gradients exist, under the rest of the backward pass.
   bool overlap_ = false;
-  int overlap_mode_ = 0;  // 1: side-stream collective kernels, 2: copy-engine transfers
+  int overlap_mode_ = 0;  // 1: side-stream collective kernels, 2: copy-engine transfers,
+                          // 3: reduce-scatter fused into the wgrad GEMMs (default, N > 1)
+  bool rs_eligible() const;
+  size_t rs_recv_off(int l) const;  // layer l's block in every replica's recv (mode 3)
+  int launch_layer_rs_update(Replica* r, Worker* w, int l);
   uint32_t ce_epoch_ = 0;
   int host_index(const std::string& id) const;  // peers_ index of the replica hosting id
   size_t shard8(int l, int p, size_t* lo) const;  // replica p's slice of layer l (units of 8)

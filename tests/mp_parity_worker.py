@@ -86,6 +86,37 @@ def main():
         failures.append(f"rank {rank}: mlp params max err {np.abs(wm - ref).max()}")
     job.close()
 
+    # 3. an MLP whose layers split into per-GPU row blocks: with the default EDL_OVERLAP the
+    #    reduce-scatter rides in the weight-gradient GEMM epilogues (TMA stores into the
+    #    owner's receive buffer over NVLink), then per-layer shard update + all-gather
+    dim, hidden, classes, layers, steps = 256, 512, 512, 3, 6
+    B = 64 * world
+    mspec = {"size": 4000, "dim": dim, "seed": 9}
+    cfg = rt.JobConfig(model=rt.MLP, size=4000, dim=dim, seed=9, noise=0.0, num_classes=classes,
+                       layers=layers, hidden=hidden, eta=0.1, decay=0.0, batch=B,
+                       lease_seed=13, partitions=64, init_seed=4)
+    job = rt.Job(cfg, ring, devices)
+    connect(job, world, rank)
+    got = []
+    for _ in range(steps):
+        job.step()
+        got.append(job.sync())
+    job.gather_master()
+    wm = job.params(ring[rank])
+    pj = api.Job(restated(), mspec, 2, 0.0, 0.0, B, 13, 64, ring)
+    orc = MLPOracle(dim, hidden, classes, layers, 9, 4, 0.1, 0.0)
+    for t in range(steps):
+        pj.step()
+        plan = [(wk, [i for _, i in s]) for wk, s in pj.plan()]
+        ref_loss = orc.step(plan, t)
+        if abs(got[t].loss - ref_loss) > 2e-3 * abs(ref_loss):
+            failures.append(f"rank {rank}: mlp-rs t={t} loss {got[t].loss} vs {ref_loss}")
+    ref = orc.flat_master()
+    err = np.abs(wm - ref)
+    if err.max() > 2 ** -8 * np.abs(ref).max() or err.mean() > 1e-4 * np.abs(ref).max():
+        failures.append(f"rank {rank}: mlp-rs params max err {err.max()} mean {err.mean()}")
+    job.close()
+
     allf = [None] * world
     dist.all_gather_object(allf, failures)
     dist.barrier()

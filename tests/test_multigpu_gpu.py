@@ -11,18 +11,23 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-# overlap: 0 = one fused collective kernel after the backward (default), 1 = per-layer
-# collective kernels on a side stream, 2 = per-layer copy-engine transfers + shard updates
+# overlap: "" = default (3 when the layers split into per-GPU row blocks, else 0), 0 = one
+# fused collective kernel after the backward, 1 = per-layer collective kernels on a side
+# stream, 2 = per-layer copy-engine transfers + shard updates, 3 = reduce-scatter in the
+# wgrad GEMM epilogues + per-layer shard update / all-gather
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("overlap", ["0", "1", "2"])
+@pytest.mark.parametrize("overlap", ["", "0", "1", "2", "3"])
 def test_two_or_more_gpus_match_oracle(overlap):
     n = min(torch.cuda.device_count(), 4)
     here = os.path.dirname(os.path.abspath(__file__))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", "29533",
            os.path.join(here, "mp_parity_worker.py")]
-    env = dict(os.environ, EDL_OVERLAP=overlap)
+    env = dict(os.environ)
+    env.pop("EDL_OVERLAP", None)
+    if overlap:
+        env["EDL_OVERLAP"] = overlap
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     assert "MP-PARITY OK" in p.stdout
