@@ -204,7 +204,6 @@ def run_b200(args, rank: int, world: int) -> None:
                 job.step()
             job.sync()
             n_pre += 1
-        job.set_profile(True)
         job.reset_counters()
         barrier()
         e0.record(stream)
@@ -212,8 +211,17 @@ def run_b200(args, rank: int, world: int) -> None:
             job.step()
         e1.record(stream)
         torch.cuda.synchronize()
+        launches = job.counters()["launches"]  # library kernels of exactly the K timed steps
+        barrier()
+        # phase breakdown in a separate K-step pass: the phase-boundary events are stream
+        # operations between kernels and would cost the timed steps their launch overlap
+        job.set_profile(True)
+        job.reset_counters()
+        for _ in range(args.steps):
+            job.step()
+        torch.cuda.synchronize()
         job.set_profile(False)
-        counters = job.counters()  # phase times and launches of exactly the K timed steps
+        counters = job.counters()
         barrier()
         t_load = time.time()
         while max_over_ranks(time.time() - t_load) < 0.5:
@@ -227,6 +235,8 @@ def run_b200(args, rank: int, world: int) -> None:
 
     ph = counters["phase_ms"]
     n = max(1, counters["steps"])
+    wgrad_ms = ph.get("wgrad", 0.0) / n  # the 8 weight-gradient GEMMs (sub-phase of backward)
+    ph_main = {k: v for k, v in ph.items() if k != "wgrad"}
     gemm_ms = (ph["forward"] + ph["backward"]) / n
     upd_ms = ph["update"] / n
     gemm_tflops = flops * w["batch"] / (gemm_ms / 1e3) / 1e12
@@ -246,6 +256,33 @@ def run_b200(args, rank: int, world: int) -> None:
                "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction",
                "kernel": "fused reduce-scatter + sharded SGD + all-gather over NVLink P2P"}
 
+    # ---- roofline of the dominant kernel (profiles/r01_kernel_shares.md): at N=1 the fused
+    # weight-gradient GEMM + SGD update (51% of the step), HBM-bound: per launch (one layer,
+    # SURVEY 8(d)'s 10 B/param update) 10 B x 16.8M params + its two bf16 operands
+    # dY [b][4096] and X [b][4096]; duration = the wgrad sub-phase / 8 launches, CUDA events
+    # on the job stream.  With several GPUs the weight-gradient GEMMs write bf16 gradients
+    # (tensor-bound) and the update moves to the NVLink collective (update_roofline).
+    n_wgrad = w["layers"]
+    per_launch_ms = wgrad_ms / n_wgrad if wgrad_ms > 0 else float("nan")
+    if world == 1:
+        alg = 10 * (P // n_wgrad) + 2 * 2 * w["batch"] * w["hidden"]
+        gbs = alg / (per_launch_ms / 1e3) / 1e9
+        dominant = {"bound": "hbm", "kernel": "gemm_bf16_2sm_kernel<128,MN,MN,sgd> "
+                    "(weight gradient + fused SGD update, one launch per layer)",
+                    "achieved": gbs, "peak": peak_h, "unit": "GB/s", "frac": gbs / peak_h,
+                    "traffic": _ncu_traffic("wgrad+sgd"), "traffic_source": NCU_FULL,
+                    "algorithmic_bytes_per_launch": alg, "launch_ms": per_launch_ms,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)"}
+    else:
+        tf = 2 * w["batch"] * (P // n_wgrad) / (per_launch_ms / 1e3) / 1e12
+        dominant = {"bound": "tensor", "kernel": "gemm_bf16_2sm_kernel<128,MN,MN> "
+                    "(weight gradient, bf16 out, one launch per layer)",
+                    "achieved": tf, "peak": peak_t, "unit": "TFLOP/s", "frac": tf / peak_t,
+                    "traffic": _ncu_traffic("wgrad]"), "traffic_source": NCU_FULL,
+                    "algorithmic_flop_per_launch": 2 * w["batch"] * (P // n_wgrad),
+                    "launch_ms": per_launch_ms,
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"}
+
     # ---- e2e: every step through the public API with a D2H read of its loss
     job.reset_counters()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -260,7 +297,6 @@ def run_b200(args, rank: int, world: int) -> None:
     ms_e2e = max_over_ranks(e2.elapsed_time(e3))
     e2e_value = samples / (ms_e2e / 1e3)
     runs_per_step = 2  # a 512-sample batch spans <= 2 shards of >= 4096 samples
-    launches = counters["launches"]
 
     # ---- CPU baseline (oracle port), bounded sample on this host, rank 0 at N=1 only
     cpu = None
@@ -287,18 +323,16 @@ def run_b200(args, rank: int, world: int) -> None:
                 "note": "job.step()+job.sync() per step: host lease draws, H2D lease runs, "
                         "D2H loss"},
         "gpu_launches": launches,
-        "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMMs (8 fwd + 7 dgrad + 8 wgrad)",
-                     "achieved": gemm_tflops, "peak": peak_t, "unit": "TFLOP/s",
-                     "frac": gemm_tflops / peak_t,
-                     # DRAM read + write per GEMM launch (mean of the 23 GEMM launches of one
-                     # mini-batch, ncu --set full, profiles/r01_ncu_full.md); algorithmic
-                     # bytes: fwd/dgrad ~40 MB (W once), wgrad+sgd 168 MB (master RMW + W)
-                     "traffic": _ncu_gemm_traffic(), "traffic_source": NCU_FULL,
-                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
-                     "per_step_ms": gemm_ms,
-                     "algorithmic_gflop_per_step": flops * w["batch"] / 1e9},
+        "roofline": dominant,
+        "gemm_roofline": {"bound": "tensor", "kernel": "tcgen05 GEMMs (8 fwd + 7 dgrad + 8 wgrad)",
+                          "achieved": gemm_tflops, "peak": peak_t, "unit": "TFLOP/s",
+                          "frac": gemm_tflops / peak_t,
+                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
+                          "per_step_ms": gemm_ms,
+                          "algorithmic_gflop_per_step": flops * w["batch"] / 1e9},
         "update_roofline": upd,
-        "phase_ms_per_step": {k: v / n for k, v in ph.items()},
+        "phase_ms_per_step": {k: v / n for k, v in ph_main.items()},
+        "wgrad_ms_per_step": wgrad_ms,
         "loss_first_last": [losses[0], losses[-1]] if losses else None,
         "clocks": clocks,
         "cpu_baseline": cpu,
@@ -315,14 +349,15 @@ def run_b200(args, rank: int, world: int) -> None:
 NCU_FULL = "profiles/r01_ncu_full.md"
 
 
-def _ncu_gemm_traffic():
-    """Mean DRAM read + write bytes per GEMM launch in the committed ncu --set full capture."""
+def _ncu_traffic(family: str):
+    """Mean DRAM read + write bytes per launch of a kernel family in the committed
+    ncu --set full capture (profiles/r01_ncu_full.md), or None."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), NCU_FULL)
     vals = []
     try:
         for line in open(path):
             cells = [c.strip() for c in line.split("|")]
-            if len(cells) > 5 and "gemm_bf16" in cells[2]:
+            if len(cells) > 5 and family in cells[2]:
                 vals.append((float(cells[4]) + float(cells[5])) * 1e6)
     except (OSError, ValueError):
         return None

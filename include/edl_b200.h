@@ -275,7 +275,8 @@ int edl_job_ring(const EdlJob* job, char* buf, size_t cap, size_t* len);
 int edl_job_lease_snapshot(const EdlJob* job, uint8_t* buf, size_t cap, size_t* len);
 /* Instrumentation (bench.py): the CUDA stream the job's kernels run on (cudaStream_t);
  * per-phase device time from CUDA events recorded on that stream while profiling is on
- * (phase_ms[5] = gather, forward GEMMs, loss, backward GEMMs, allreduce+update), the steps
+ * (phase_ms[6] = gather, forward GEMMs, loss, backward GEMMs, allreduce+update, and the
+ * weight-gradient GEMMs alone — a sub-phase of the backward), the steps
  * profiled and the number of library kernels launched since the last reset.            */
 void* edl_job_stream(const EdlJob* job);
 /* Multi-process data parallelism (one process per GPU, e.g. torchrun): every process

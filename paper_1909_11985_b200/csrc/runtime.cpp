@@ -690,9 +690,11 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
   m = mark(slot, 2, m, r->stream);
   for (int l = L_ - 1; l >= 0; --l) {
     if (l > 0) EDL_TRY(gemm_plan_run(r->dgrad[l], r->stream));
+    cudaEvent_t mw = prof ? mark_begin(r->stream) : nullptr;  // wgrad sub-phase
     if (fused_update_ && (!overlap_ || l == 0)) {
       // dW + sgd_step in one kernel (layer 0 ends the backward: nothing left to overlap)
       EDL_TRY(gemm_plan_run(w->wgrad_sgd[l], r->stream, step_scale_));
+      if (mw) mark(slot, 5, mw, r->stream);
     } else if (overlap_mode_ == 3) {
       // dW with the reduce-scatter in its epilogue (rows owned elsewhere are stored into
       // the owner's recv over NVLink), then this replica's shard update + all-gather
@@ -700,6 +702,7 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
       EDL_TRY(launch_layer_rs_update(r, w, l));
     } else {
       EDL_TRY(gemm_plan_run(w->wgrad[l], r->stream));
+      if (mw) mark(slot, 5, mw, r->stream);
       if (overlap_ && last) EDL_TRY(launch_layer_coll(r, l));
     }
   }

@@ -191,7 +191,7 @@ class Job {
     phase_steps_ = 0;
     launches_ = 0;
   }
-  static constexpr int kPhases = 5;
+  static constexpr int kPhases = 6;  // + 5: weight-gradient GEMMs (inside the backward)
   static constexpr int kMaxMarks = 64;
 
  private:

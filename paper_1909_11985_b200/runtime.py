@@ -205,10 +205,10 @@ class Job:
     def set_profile(self, on: bool) -> None:
         self._L.edl_job_set_profile(self._h, 1 if on else 0)
 
-    PHASES = ("gather", "forward", "loss", "backward", "update")
+    PHASES = ("gather", "forward", "loss", "backward", "update", "wgrad")
 
     def counters(self) -> dict:
-        ms = (C.c_double * 5)()
+        ms = (C.c_double * len(self.PHASES))()
         steps, launches = C.c_uint64(), C.c_uint64()
         self._L.edl_job_counters(self._h, ms, C.byref(steps), C.byref(launches))
         return {"phase_ms": dict(zip(self.PHASES, list(ms))), "steps": steps.value,
