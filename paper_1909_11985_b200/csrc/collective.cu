@@ -159,6 +159,93 @@ __global__ void __launch_bounds__(256) allreduce_sgd_kernel(CollArgs a) {
   if (a.n_rep > 1) cross_replica_barrier(a, 1);
 }
 
+// Push variant: replica r owns slice r/n of every layer (shard_range, as own_segments);
+// recv of owner o = [n-1 slots (sources in replica order, o skipped)][its shard, layers
+// concatenated].
+__device__ __forceinline__ void lay_shard(const CollArgs& a, int l, int r, size_t* lo,
+                                          size_t* hi) {
+  const size_t n8 = a.lay_len8[l];
+  *lo = a.lay_off8[l] + n8 * static_cast<size_t>(r) / static_cast<size_t>(a.n_rep);
+  *hi = a.lay_off8[l] + n8 * static_cast<size_t>(r + 1) / static_cast<size_t>(a.n_rep);
+}
+__device__ __forceinline__ size_t shard_prefix8(const CollArgs& a, int r, int l) {
+  size_t t = 0;
+  for (int k = 0; k < l; ++k) {
+    size_t lo, hi;
+    lay_shard(a, k, r, &lo, &hi);
+    t += hi - lo;
+  }
+  return t;
+}
+
+template <bool kMomentum>
+__global__ void __launch_bounds__(256) push_allreduce_sgd_kernel(CollArgs a) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  const size_t tid = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  const uint4* own = reinterpret_cast<const uint4*>(a.own_grad);
+  if (a.update) {
+    // phase A: my gradient slices -> their owners' recv (NVLink stores, 4 in flight)
+    for (int j = 1; j < a.n_rep; ++j) {
+      const int o = (a.me + j) % a.n_rep;  // rotated: every GPU pushes to a different owner
+      const size_t total = shard_prefix8(a, o, a.n_layer);
+      const size_t slot = static_cast<size_t>(a.me < o ? a.me : a.me - 1);
+      uint4* dst_o = reinterpret_cast<uint4*>(a.recv_peer[o]) + slot * total;
+      for (int l = 0; l < a.n_layer; ++l) {
+        size_t lo, hi;
+        lay_shard(a, l, o, &lo, &hi);
+        uint4* dst = dst_o + shard_prefix8(a, o, l);
+        const size_t len = hi - lo;
+        for (size_t i = tid; i < len; i += 4 * stride) {
+          uint4 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (i + u * stride < len) v[u] = __ldcs(own + lo + i + u * stride);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (i + u * stride < len) dst[i + u * stride] = v[u];
+        }
+      }
+    }
+  }
+  cross_replica_barrier(a, 0);  // every peer's slices of my shard have landed
+  if (a.loss_out && blockIdx.x == 0 && threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int k = 0; k < a.n_loss; ++k) acc = __dadd_rn(acc, *a.losses[k]);
+    *a.loss_out = acc;
+  }
+  if (a.update) {
+    // phase B: ring-order sum of my shard from local memory, SGD, weights to every replica
+    const size_t total = shard_prefix8(a, a.me, a.n_layer);
+    const uint4* rv = reinterpret_cast<const uint4*>(a.recv_me);
+    for (int l = 0; l < a.n_layer; ++l) {
+      size_t lo, hi;
+      lay_shard(a, l, a.me, &lo, &hi);
+      const size_t pre = shard_prefix8(a, a.me, l);
+      for (size_t i = lo + tid; i < hi; i += stride) {
+        float gs[8];
+        for (int k = 0; k < a.n_src; ++k) {
+          const int r = a.src_rep[k];
+          const uint4 v = r == a.me
+                              ? __ldcs(own + i)
+                              : __ldcs(rv + static_cast<size_t>(r < a.me ? r : r - 1) * total +
+                                       pre + (i - lo));
+          float f[8];
+          bf16x8_to_f32(v, f);
+          if (k == 0) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) gs[e] = f[e];
+          } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) gs[e] = __fadd_rn(gs[e], f[e]);
+          }
+        }
+        apply8<kMomentum>(a, i, gs);
+      }
+    }
+  }
+  cross_replica_barrier(a, 1);
+}
+
 __global__ void barrier_kernel(CollArgs a) { cross_replica_barrier(a, 0); }
 
 // One CTA: barrier, ring-order f64 reduction of every member's [grad_sum, count] (chunk c =
@@ -348,6 +435,16 @@ int allreduce_sgd(const CollArgs& a, cudaStream_t s) {
   }
   int blocks = a.blocks > 0 ? a.blocks : (env_blocks > 0 ? env_blocks : coll_blocks());
   if (blocks > kCollMaxBlocks) return fail(EDL_EINVAL, "allreduce_sgd: grid");
+  if (a.push) {
+    if (a.n_src != a.n_rep || a.n_layer < 1 || a.n_layer > kCollMaxSegs)
+      return fail(EDL_EINVAL, "allreduce_sgd: push variant needs one member per replica");
+    if (a.mu != 0.0f)
+      push_allreduce_sgd_kernel<true><<<blocks, 256, 0, s>>>(a);
+    else
+      push_allreduce_sgd_kernel<false><<<blocks, 256, 0, s>>>(a);
+    EDL_CUDA_TRY(cudaGetLastError());
+    return EDL_OK;
+  }
   if (a.mu != 0.0f) {
     if (unroll >= 2)
       allreduce_sgd_kernel<true, 2><<<blocks, 256, 0, s>>>(a);

@@ -42,6 +42,16 @@ struct CollArgs {
   const double* losses[kCollMaxSources];
   int n_loss = 0;
   double* loss_out = nullptr;
+  // push variant (one ring member per replica): every NVLink byte is a store.  Phase A
+  // pushes this replica's gradient slices to their owners' recv, phase B sums its own shard
+  // from local memory (own gradient + recv) and pushes the updated bf16 weights.
+  int push = 0;
+  int n_layer = 0;
+  size_t lay_off8[kCollMaxSegs], lay_len8[kCollMaxSegs];  // layer l: [off8, off8 + len8)
+  const __nv_bfloat16* own_grad = nullptr;
+  __nv_bfloat16* recv_me = nullptr;                     // this replica's recv
+  __nv_bfloat16* recv_peer[kCollMaxReplicas];           // replica r's recv (peer-mapped)
+  int src_rep[kCollMaxSources];                         // ring member k -> replica index
 };
 
 // f64 ring allreduce of [grad_sum, count] vectors + sgd_step, over peer pointers

@@ -818,6 +818,25 @@ bool Job::rs_eligible() const {
   return true;
 }
 
+// Push collective: one ring member per replica, every replica's recv mapped here.
+bool Job::push_eligible() const {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("EDL_COLL_PUSH");
+    env = e && *e ? atoi(e) : 1;
+  }
+  const int n = static_cast<int>(peers_.size());
+  if (!env || !mlp_ || n < 2 || ring_.size() != peers_.size()) return false;
+  std::vector<int> seen(static_cast<size_t>(n), 0);
+  for (const auto& id : ring_) {
+    const int h = host_index(id);
+    if (h < 0 || seen[static_cast<size_t>(h)]++) return false;
+  }
+  for (const auto& p : peers_)
+    if (!p.recv || !p.W || !p.flags) return false;
+  return true;
+}
+
 size_t Job::rs_recv_off(int l) const {
   const size_t n = peers_.size();
   size_t off = 0;
@@ -1459,6 +1478,19 @@ int Job::reduce_and_update(uint64_t count, uint64_t t, int slot) {
       a.mu = static_cast<float>(cfg_.momentum);
       a.update = (count > 0 && !fused_update_ && !overlap_) ? 1 : 0;
       a.loss_out = r->loss_sum;
+      if (a.update && push_eligible()) {  // every NVLink byte a store (measured faster)
+        a.push = 1;
+        a.n_layer = L_;
+        for (int l = 0; l < L_; ++l) {
+          a.lay_off8[l] = off_[l] / 8;
+          a.lay_len8[l] = static_cast<size_t>(in_[l]) * out_[l] / 8;
+        }
+        for (size_t k = 0; k < ring_.size(); ++k) a.src_rep[k] = host_index(ring_[k]);
+        for (int p = 0; p < n_rep; ++p) a.recv_peer[p] = peers_[p].recv;
+        a.recv_me = r->recv;
+        for (const auto& id : ring_)
+          if (host_index(id) == me) a.own_grad = workers_[id]->grad;
+      }
       EDL_TRY(allreduce_sgd(a, r->stream));
     } else {
       LinearCollArgs a;

@@ -229,6 +229,7 @@ class Job {
   int overlap_mode_ = 0;  // 1: side-stream collective kernels, 2: copy-engine transfers,
                           // 3: reduce-scatter fused into the wgrad GEMMs (default, N > 1)
   bool rs_eligible() const;
+  bool push_eligible() const;
   size_t rs_recv_off(int l) const;  // layer l's block in every replica's recv (mode 3)
   int launch_layer_rs_update(Replica* r, Worker* w, int l);
   uint32_t ce_epoch_ = 0;
