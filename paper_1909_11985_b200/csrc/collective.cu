@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(256) push_allreduce_sgd_kernel(CollArgs a) {
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   const size_t tid = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   const uint4* own = reinterpret_cast<const uint4*>(a.own_grad);
-  if (a.update) {
+  if (a.update && !a.skip_push) {
     // phase A: my gradient slices -> their owners' recv (NVLink stores, 4 in flight)
     for (int j = 1; j < a.n_rep; ++j) {
       const int o = (a.me + j) % a.n_rep;  // rotated: every GPU pushes to a different owner

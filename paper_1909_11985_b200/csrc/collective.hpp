@@ -46,6 +46,7 @@ struct CollArgs {
   // pushes this replica's gradient slices to their owners' recv, phase B sums its own shard
   // from local memory (own gradient + recv) and pushes the updated bf16 weights.
   int push = 0;
+  int skip_push = 0;  // phase A already done by the routed weight-gradient GEMMs
   int n_layer = 0;
   size_t lay_off8[kCollMaxSegs], lay_len8[kCollMaxSegs];  // layer l: [off8, off8 + len8)
   const __nv_bfloat16* own_grad = nullptr;

@@ -610,12 +610,12 @@ int Job::ensure_plans(Worker* w, int64_t rows) {
       EDL_TRY(gemm_plan_init(&w->wgrad_rs[l], dy, out_[l], 1, r->act[l], in_[l], 1,
                              w->grad + off_[l], in_[l], out_[l], in_[l], static_cast<int>(rows),
                              0, 0, nullptr, 0, 1000 + 128));
-      const size_t prow = static_cast<size_t>(out_[l]) / n, block = prow * in_[l];
+      const size_t prow = static_cast<size_t>(out_[l]) / n;
       void* dst[kMaxPeerMaps] = {};
-      for (int o = 0; o < n; ++o) {
+      for (int o = 0; o < n; ++o) {  // the push collective's recv layout (collective.cu)
         if (o == me) continue;
         const size_t slot = static_cast<size_t>(me < o ? me : me - 1);
-        dst[o] = peers_[o].recv + rs_recv_off(l) + slot * block;
+        dst[o] = peers_[o].recv + (slot * shard_total8(o) + seg_off8(o, l)) * 8;
       }
       EDL_TRY(gemm_plan_route(&w->wgrad_rs[l], static_cast<int>(prow), me, dst, n));
     }
@@ -696,10 +696,10 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
       EDL_TRY(gemm_plan_run(w->wgrad_sgd[l], r->stream, step_scale_));
       if (mw) mark(slot, 5, mw, r->stream);
     } else if (overlap_mode_ == 3) {
-      // dW with the reduce-scatter in its epilogue (rows owned elsewhere are stored into
-      // the owner's recv over NVLink), then this replica's shard update + all-gather
+      // dW with the reduce-scatter in its epilogue: rows owned elsewhere are stored into the
+      // owner's recv over NVLink while the backward continues; the shard update + all-gather
+      // run once, after the backward (the push collective with its phase A skipped)
       EDL_TRY(gemm_plan_run(w->wgrad_rs[l], r->stream));
-      EDL_TRY(launch_layer_rs_update(r, w, l));
     } else {
       EDL_TRY(gemm_plan_run(w->wgrad[l], r->stream));
       if (mw) mark(slot, 5, mw, r->stream);
@@ -835,59 +835,6 @@ bool Job::push_eligible() const {
   for (const auto& p : peers_)
     if (!p.recv || !p.W || !p.flags) return false;
   return true;
-}
-
-size_t Job::rs_recv_off(int l) const {
-  const size_t n = peers_.size();
-  size_t off = 0;
-  for (int k = 0; k < l; ++k) off += (n - 1) * (static_cast<size_t>(out_[k]) / n) * in_[k];
-  return off;
-}
-
-// Layer l's shard update after the reduce-scatter GEMM: the ring-order sum of this
-// replica's own gradient block and the peers' blocks in its recv, SGD on the fp32 master
-// shard, and the bf16 weights of the shard stored into every replica (the all-gather) —
-// the collective kernel with sources pointing at local memory only.
-int Job::launch_layer_rs_update(Replica* r, Worker* w, int l) {
-  const int n = static_cast<int>(peers_.size());
-  const int me = rep_index(r);
-  const size_t rows = static_cast<size_t>(out_[l]) / n, block = rows * in_[l];
-  size_t lo8, hi8;
-  shard_range(static_cast<size_t>(out_[l]) * in_[l] / 8, n, me, &lo8, &hi8);
-  const size_t first = off_[l] + lo8 * 8;  // flat index of this replica's first owned param
-  CollArgs a;
-  for (const auto& id : ring_) {
-    const int h = host_index(id);
-    if (h == me) {
-      a.grads[a.n_src++] = w->grad;
-    } else {
-      const size_t slot = static_cast<size_t>(h < me ? h : h - 1);
-      // pointer biased so that element `first` lands on the slot's first element
-      a.grads[a.n_src++] = r->recv + rs_recv_off(l) + slot * block - first;
-    }
-  }
-  for (const auto& p : peers_) {
-    a.flags[a.n_dst] = p.flags;
-    a.w_dst[a.n_dst++] = p.W;
-  }
-  a.me = me;
-  a.n_rep = n;
-  a.epoch = layer_epoch0_ + static_cast<uint32_t>(r->layer_colls);
-  a.n_seg = 1;
-  a.seg_lo8[0] = off_[l] / 8 + lo8;
-  a.seg_hi8[0] = off_[l] / 8 + hi8;
-  a.master = r->master;
-  a.mom = r->mom;
-  const double eta_t = cfg_.eta / (1.0 + cfg_.decay * static_cast<double>(t_));
-  a.scale = static_cast<float>(eta_t / static_cast<double>(step_count_));
-  a.inv_count = static_cast<float>(1.0 / static_cast<double>(step_count_));
-  a.eta = static_cast<float>(eta_t);
-  a.mu = static_cast<float>(cfg_.momentum);
-  a.update = 1;
-  EDL_TRY(allreduce_sgd(a, r->stream));
-  ++r->layer_colls;
-  launches_ += 1;
-  return EDL_OK;
 }
 
 bool Job::ce_fits() const {
@@ -1476,10 +1423,11 @@ int Job::reduce_and_update(uint64_t count, uint64_t t, int slot) {
       a.inv_count = count ? static_cast<float>(1.0 / static_cast<double>(count)) : 0.f;
       a.eta = static_cast<float>(eta_t);
       a.mu = static_cast<float>(cfg_.momentum);
-      a.update = (count > 0 && !fused_update_ && !overlap_) ? 1 : 0;
+      a.update = (count > 0 && !fused_update_ && (!overlap_ || overlap_mode_ == 3)) ? 1 : 0;
       a.loss_out = r->loss_sum;
-      if (a.update && push_eligible()) {  // every NVLink byte a store (measured faster)
+      if (a.update && (overlap_mode_ == 3 || push_eligible())) {  // every NVLink byte a store
         a.push = 1;
+        a.skip_push = overlap_mode_ == 3 ? 1 : 0;  // slices already pushed by the GEMMs
         a.n_layer = L_;
         for (int l = 0; l < L_; ++l) {
           a.lay_off8[l] = off_[l] / 8;
@@ -1716,7 +1664,7 @@ int Job::step(EdlStepReport* out) {
   static int overlap_env = -1;
   if (overlap_env < 0) {
     const char* e = getenv("EDL_OVERLAP");
-    overlap_env = e && *e ? atoi(e) : 0;
+    overlap_env = e && *e ? atoi(e) : -1;
   }
   // overlapped update (EDL_OVERLAP=1: side-stream collective kernels per layer, 2: copy-engine
   // transfers per layer).  Off by default: measured on B200 the
@@ -1728,13 +1676,15 @@ int Job::step(EdlStepReport* out) {
     if (overlap_mode_ == 2 && !ce_fits()) overlap_mode_ = 1;
     if (overlap_mode_ == 3 && !rs_eligible()) overlap_mode_ = 0;
   }
-  // EDL_OVERLAP=3: the reduce-scatter rides in the wgrad GEMM epilogues (TMA stores into the
-  // owners' recv over NVLink) and a per-layer shard update + all-gather follows each GEMM.
-  // Not the default: measured 0.90M vs 1.05M samples/s at N=2 and 1.30M vs 1.69M at N=4
-  // (eight barrier-bracketed update kernels cost more than the overlap wins).
+  // default with several GPUs (EDL_OVERLAP unset): the reduce-scatter rides in the wgrad GEMM
+  // epilogues (TMA stores into the owners' recv over NVLink, under the backward) and one push
+  // collective does the shard update + all-gather.  Measured on B200: 1.18M vs 1.10M
+  // samples/s at N=2, 1.89M vs 1.77M at N=4 over the single push collective.
+  if (mlp_ && count > 0 && overlap_env < 0 && peers_.size() > 1 && rs_eligible())
+    overlap_mode_ = 3;
   overlap_ = overlap_mode_ != 0;
   step_count_ = count;
-  if (overlap_mode_ == 1 || overlap_mode_ == 3) {  // same epochs on every process
+  if (overlap_mode_ == 1) {  // same epochs on every process
     layer_epoch0_ = coll_epoch_ + 1;
     coll_epoch_ += static_cast<uint32_t>(fused_update_ ? L_ - 1 : L_);
   }

@@ -227,11 +227,9 @@ class Job {
   // soon as layer l's weight gradients exist, under the rest of the backward pass.
   bool overlap_ = false;
   int overlap_mode_ = 0;  // 1: side-stream collective kernels, 2: copy-engine transfers,
-                          // 3: reduce-scatter fused into the wgrad GEMMs (default, N > 1)
+                          // 3: reduce-scatter fused into the wgrad GEMM epilogues
   bool rs_eligible() const;
   bool push_eligible() const;
-  size_t rs_recv_off(int l) const;  // layer l's block in every replica's recv (mode 3)
-  int launch_layer_rs_update(Replica* r, Worker* w, int l);
   uint32_t ce_epoch_ = 0;
   int host_index(const std::string& id) const;  // peers_ index of the replica hosting id
   size_t shard8(int l, int p, size_t* lo) const;  // replica p's slice of layer l (units of 8)
