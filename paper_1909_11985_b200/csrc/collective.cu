@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(256) push_allreduce_sgd_kernel(CollArgs a) {
   const size_t tid = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   const uint4* own = reinterpret_cast<const uint4*>(a.own_grad);
   if (a.update && !a.skip_push) {
-    // phase A: my gradient slices -> their owners' recv (NVLink stores, 4 in flight)
+    // phase A: my gradient slices -> their owners' recv (NVLink stores, 2 in flight)
     for (int j = 1; j < a.n_rep; ++j) {
       const int o = (a.me + j) % a.n_rep;  // rotated: every GPU pushes to a different owner
       const size_t total = shard_prefix8(a, o, a.n_layer);
@@ -195,13 +195,13 @@ __global__ void __launch_bounds__(256) push_allreduce_sgd_kernel(CollArgs a) {
         lay_shard(a, l, o, &lo, &hi);
         uint4* dst = dst_o + shard_prefix8(a, o, l);
         const size_t len = hi - lo;
-        for (size_t i = tid; i < len; i += 4 * stride) {
-          uint4 v[4];
+        for (size_t i = tid; i < len; i += 2 * stride) {
+          uint4 v[2];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int u = 0; u < 2; ++u)
             if (i + u * stride < len) v[u] = __ldcs(own + lo + i + u * stride);
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int u = 0; u < 2; ++u)
             if (i + u * stride < len) dst[i + u * stride] = v[u];
         }
       }

@@ -49,7 +49,8 @@ int mlp_init_weights(float* master, __nv_bfloat16* w, size_t n, uint64_t seed, u
 // Softmax cross-entropy over rows x classes fp32 logits; dlogits bf16 = softmax - onehot
 // (sum semantics, no 1/B); row_loss[r] = logsumexp - logit[label].
 int softmax_xent(const float* logits, const int32_t* labels, int rows, int classes,
-                 __nv_bfloat16* dlogits, float* row_loss, cudaStream_t s);
+                 __nv_bfloat16* dlogits, float* row_loss, double* loss_out, unsigned* done,
+                 cudaStream_t s);
 // loss_out[0] += sum(row_loss[0..rows)) (deterministic, one CTA).
 int sum_rows(const float* row_loss, int rows, double* loss_out, cudaStream_t s);
 // Fused gradient average + SGD(+momentum) over n params, reading n_src gradient buffers

@@ -53,10 +53,29 @@ __device__ __forceinline__ float warp_sum(float v) {
 // One CTA (256 threads) per row; classes <= 256 * kPer values held in registers.
 constexpr int kXentThreads = 256;
 constexpr int kPer = 16;
+// Ordered loss sum of `rows` per-row losses by one CTA: thread t sums rows t, t+256, ...
+// then thread 0 adds the 256 partials in order (the same order as sum_rows).
+__device__ void ordered_row_sum(const float* v, int rows, double* out, double* part) {
+  double acc = 0.0;
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) acc += static_cast<double>(v[r]);
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < static_cast<int>(blockDim.x); ++k) t += part[k];
+    *out += t;
+  }
+}
+
 __global__ void __launch_bounds__(kXentThreads)
     xent_kernel(const float* __restrict__ logits, const int32_t* __restrict__ labels, int classes,
-                __nv_bfloat16* __restrict__ dlogits, float* __restrict__ row_loss) {
+                __nv_bfloat16* __restrict__ dlogits, float* __restrict__ row_loss,
+                double* __restrict__ loss_out, unsigned* __restrict__ done) {
   __shared__ float red[kXentThreads / 32];
+  __shared__ double part[kXentThreads];
+  __shared__ bool last;
+  // launched with programmatic serialization after the last forward GEMM: wait for it here
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int row = blockIdx.x;
   const float* x = logits + static_cast<size_t>(row) * classes;
   float v[kPer];
@@ -96,19 +115,21 @@ __global__ void __launch_bounds__(kXentThreads)
     if (c < classes) d[c] = __float2bfloat16_rn(v[j] * inv - (c == label ? 1.0f : 0.0f));
   }
   if (threadIdx.x == 0) row_loss[row] = logf(s) + m - x[label];
+  if (!loss_out) return;
+  // the last CTA to finish adds the row losses into the worker's loss (fused sum_rows)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  ordered_row_sum(row_loss, gridDim.x, loss_out, part);
+  if (threadIdx.x == 0) *done = 0;  // ready for the next mini-batch
 }
 
 __global__ void sum_rows_kernel(const float* __restrict__ v, int rows, double* __restrict__ out) {
   __shared__ double part[256];
-  double acc = 0.0;
-  for (int r = threadIdx.x; r < rows; r += blockDim.x) acc += static_cast<double>(v[r]);
-  part[threadIdx.x] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int k = 0; k < static_cast<int>(blockDim.x); ++k) t += part[k];
-    *out += t;
-  }
+  ordered_row_sum(v, rows, out, part);
 }
 
 }  // namespace
@@ -121,11 +142,22 @@ int mlp_init_weights(float* master, __nv_bfloat16* w, size_t n, uint64_t seed, u
 }
 
 int softmax_xent(const float* logits, const int32_t* labels, int rows, int classes,
-                 __nv_bfloat16* dlogits, float* row_loss, cudaStream_t s) {
+                 __nv_bfloat16* dlogits, float* row_loss, double* loss_out, unsigned* done,
+                 cudaStream_t s) {
   if (classes > kXentThreads * kPer) return fail(EDL_EINVAL, "softmax_xent: classes > 4096");
   if (rows <= 0) return EDL_OK;
-  xent_kernel<<<rows, kXentThreads, 0, s>>>(logits, labels, classes, dlogits, row_loss);
-  EDL_CUDA_TRY(cudaGetLastError());
+  if (loss_out && !done) return fail(EDL_EINVAL, "softmax_xent: loss sum needs a counter");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(rows);
+  cfg.blockDim = dim3(kXentThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  EDL_CUDA_TRY(cudaLaunchKernelEx(&cfg, xent_kernel, logits, labels, classes, dlogits, row_loss,
+                                  loss_out, done));
   return EDL_OK;
 }
 

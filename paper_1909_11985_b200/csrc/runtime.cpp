@@ -285,6 +285,8 @@ int Job::build_replica(Replica* r) {
     EDL_TRY(dalloc(&r->dx[0], static_cast<size_t>(rows) * widest));
     EDL_TRY(dalloc(&r->dx[1], static_cast<size_t>(rows) * widest));
     EDL_TRY(dalloc(&r->row_loss, static_cast<size_t>(rows)));
+    EDL_CUDA_TRY(cudaMalloc(&r->xent_done, sizeof(unsigned)));
+    EDL_CUDA_TRY(cudaMemset(r->xent_done, 0, sizeof(unsigned)));
     EDL_TRY(dalloc(&r->labels, static_cast<size_t>(rows)));
   } else {
     const int dim = cfg_.data.dim;
@@ -351,6 +353,7 @@ void Job::free_replica(Replica* r) {
   cudaFree(r->dx[0]);
   cudaFree(r->dx[1]);
   cudaFree(r->row_loss);
+  cudaFree(r->xent_done);
   cudaFree(r->labels);
   cudaFree(r->w);
   cudaFree(r->xb);
@@ -684,9 +687,9 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
   m = mark(slot, 0, m, r->stream);
   for (int l = 0; l < L_; ++l) EDL_TRY(gemm_plan_run(r->fwd[l], r->stream));
   m = mark(slot, 1, m, r->stream);
+  // softmax cross-entropy + the worker's ordered loss sum in one kernel
   EDL_TRY(softmax_xent(r->logits, r->labels, static_cast<int>(rows), cfg_.num_classes, r->dlog,
-                       r->row_loss, r->stream));
-  EDL_TRY(sum_rows(r->row_loss, static_cast<int>(rows), w->loss, r->stream));
+                       r->row_loss, w->loss, r->xent_done, r->stream));
   m = mark(slot, 2, m, r->stream);
   for (int l = L_ - 1; l >= 0; --l) {
     if (l > 0) EDL_TRY(gemm_plan_run(r->dgrad[l], r->stream));
@@ -714,7 +717,7 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
   if (overlap_ && last && overlap_mode_ != 3) EDL_TRY(finish_layer_colls(r));
   m = mark(slot, 3, m, r->stream);
   (void)m;
-  launches_ += 1 + static_cast<uint64_t>(L_) + 2 + static_cast<uint64_t>(2 * L_ - 1);
+  launches_ += 1 + static_cast<uint64_t>(L_) + 1 + static_cast<uint64_t>(2 * L_ - 1);
   return EDL_OK;
 }
 

@@ -54,6 +54,7 @@ struct Replica {
   __nv_bfloat16* dlog = nullptr;
   __nv_bfloat16* dx[2] = {nullptr, nullptr};
   float* row_loss = nullptr;
+  unsigned* xent_done = nullptr;  // CTA counter of the fused softmax + loss-sum kernel
   int32_t* labels = nullptr;
   int64_t plan_rows = -1;
   std::vector<GemmPlan> fwd, dgrad;
