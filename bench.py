@@ -320,8 +320,8 @@ def run_b200(args, rank: int, world: int) -> None:
                    "l2": "inputs > L2 (weights 268 MB + fp32 master 537 MB streamed per step)"},
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": 16 * runs_per_step, "d2h_bytes_per_step": 8,
-                "note": "job.step()+job.sync() per step: host lease draws, H2D lease runs, "
-                        "D2H loss"},
+                "note": "job.step()+job.sync() per step: host lease draws, the lease runs "
+                        "H2D as gather-kernel launch parameters, D2H loss"},
         "gpu_launches": launches,
         "roofline": dominant,
         "gemm_roofline": {"bound": "tensor", "kernel": "tcgen05 GEMMs (8 fwd + 7 dgrad + 8 wgrad)",

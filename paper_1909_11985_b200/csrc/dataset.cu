@@ -231,6 +231,58 @@ int dataset_get(const Dataset* ds, uint64_t index, double* features, double* lab
   return EDL_OK;
 }
 
+// Same gather with the (few) leased runs passed as kernel parameters, and the worker's
+// loss accumulator zeroed by the first thread: no H2D copy or memset before the step.
+__global__ void gather_inline_kernel(const uint8_t* __restrict__ src,
+                                     const void* __restrict__ labels, int label_bytes,
+                                     const __grid_constant__ InlineRuns runs, int64_t n_rows,
+                                     size_t row_bytes, uint8_t* __restrict__ dst,
+                                     uint8_t* __restrict__ dst_labels, double* zero) {
+  if (zero && blockIdx.x == 0 && threadIdx.x == 0) *zero = 0.0;
+  for (int64_t r = blockIdx.x; r < n_rows; r += gridDim.x) {
+    int64_t k = r;
+    uint64_t id = 0;
+    for (int j = 0; j < runs.n; ++j) {
+      const int64_t c = static_cast<int64_t>(runs.r[j].count);
+      if (k < c) {
+        id = runs.r[j].first + static_cast<uint64_t>(k);
+        break;
+      }
+      k -= c;
+    }
+    const uint8_t* s = src + id * row_bytes;
+    uint8_t* d = dst + static_cast<size_t>(r) * row_bytes;
+    if ((row_bytes & 15) == 0) {
+      for (size_t off = threadIdx.x * 16; off < row_bytes; off += blockDim.x * 16)
+        *reinterpret_cast<uint4*>(d + off) = __ldg(reinterpret_cast<const uint4*>(s + off));
+    } else {
+      for (size_t off = threadIdx.x; off < row_bytes; off += blockDim.x) d[off] = s[off];
+    }
+    if (threadIdx.x == 0 && dst_labels) {
+      if (label_bytes == 8)
+        reinterpret_cast<uint64_t*>(dst_labels)[r] = reinterpret_cast<const uint64_t*>(labels)[id];
+      else
+        reinterpret_cast<uint32_t*>(dst_labels)[r] = reinterpret_cast<const uint32_t*>(labels)[id];
+    }
+  }
+}
+
+int gather_inline(const Dataset* ds, const EdlRun* runs, int n_runs, int64_t n_rows, void* x_out,
+                  void* y_out, double* zero, cudaStream_t stream) {
+  if (n_runs < 0 || n_runs > kInlineRuns) return fail(EDL_EINVAL, "gather_inline: too many runs");
+  InlineRuns ir{};
+  ir.n = n_runs;
+  for (int j = 0; j < n_runs; ++j) ir.r[j] = runs[j];
+  const int threads = ds->row_bytes >= 4096 ? 256 : 64;
+  int64_t blocks = n_rows < 4 * 148 ? n_rows : 4 * 148;
+  if (blocks < 1) blocks = 1;
+  gather_inline_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
+      static_cast<const uint8_t*>(ds->x), ds->y, ds->label_bytes, ir, n_rows, ds->row_bytes,
+      static_cast<uint8_t*>(x_out), static_cast<uint8_t*>(y_out), zero);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
+
 int gather(const Dataset* ds, const EdlRun* runs_dev, int n_runs, int64_t n_rows, void* x_out,
            void* y_out, cudaStream_t stream) {
   if (n_rows <= 0) return EDL_OK;

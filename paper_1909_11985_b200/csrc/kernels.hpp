@@ -29,6 +29,14 @@ void dataset_destroy(Dataset* ds);
 int dataset_get(const Dataset* ds, uint64_t index, double* features, double* label);
 int gather(const Dataset* ds, const EdlRun* runs_dev, int n_runs, int64_t n_rows, void* x_out,
            void* y_out, cudaStream_t stream);
+constexpr int kInlineRuns = 32;
+struct InlineRuns {
+  EdlRun r[kInlineRuns];
+  int n;
+};
+// gather with <= kInlineRuns runs as kernel parameters; *zero = 0 (the worker's loss) first.
+int gather_inline(const Dataset* ds, const EdlRun* runs, int n_runs, int64_t n_rows, void* x_out,
+                  void* y_out, double* zero, cudaStream_t stream);
 
 // ---- linear model, f64, bit-identical to trainer.cpp
 int linear_local_gradient(int kind, const double* w, const double* x, const double* y, int64_t n,

@@ -671,8 +671,8 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
   const bool prof = profile_ && r == primary();
   const int64_t rows = static_cast<int64_t>(w->plan.size());
   EDL_CUDA_TRY(cudaEventRecord(w->ev_w0[slot], r->stream));
-  EDL_CUDA_TRY(cudaMemsetAsync(w->loss, 0, sizeof(double), r->stream));
   if (rows == 0) {  // ShardPending for the whole step: contributes a zero gradient
+    EDL_CUDA_TRY(cudaMemsetAsync(w->loss, 0, sizeof(double), r->stream));
     EDL_CUDA_TRY(cudaMemsetAsync(w->grad, 0, sizeof(__nv_bfloat16) * P_, r->stream));
     if (overlap_ && last) EDL_TRY(finish_layer_colls(r));  // mode 3 needs rows > 0
     EDL_CUDA_TRY(cudaEventRecord(w->ev_w1[slot], r->stream));
@@ -681,9 +681,15 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
   EDL_TRY(ensure_plans(w, rows));
   cudaEvent_t m = prof ? mark_begin(r->stream) : nullptr;
   EdlRun* host = w->runs_host + static_cast<size_t>(slot) * w->runs_cap;
-  EDL_CUDA_TRY(cudaMemcpyAsync(w->runs_dev, host, sizeof(EdlRun) * w->n_runs,
-                               cudaMemcpyHostToDevice, r->stream));
-  EDL_TRY(gather(r->ds, w->runs_dev, w->n_runs, rows, r->act[0], r->labels, r->stream));
+  if (w->n_runs <= kInlineRuns) {  // runs ride in the launch parameters; loss zeroed there
+    EDL_TRY(gather_inline(r->ds, host, w->n_runs, rows, r->act[0], r->labels, w->loss,
+                          r->stream));
+  } else {
+    EDL_CUDA_TRY(cudaMemsetAsync(w->loss, 0, sizeof(double), r->stream));
+    EDL_CUDA_TRY(cudaMemcpyAsync(w->runs_dev, host, sizeof(EdlRun) * w->n_runs,
+                                 cudaMemcpyHostToDevice, r->stream));
+    EDL_TRY(gather(r->ds, w->runs_dev, w->n_runs, rows, r->act[0], r->labels, r->stream));
+  }
   m = mark(slot, 0, m, r->stream);
   for (int l = 0; l < L_; ++l) EDL_TRY(gemm_plan_run(r->fwd[l], r->stream));
   m = mark(slot, 1, m, r->stream);
