@@ -58,7 +58,7 @@ def launches(path: str, tag: str) -> None:
         us = v / 1000.0 if unit in ("ns", "nsecond") else (v * 1000.0 if unit in ("ms", "msecond") else v)
         rows.append((r["Kernel Name"], us))
     # one mini-batch = the launches between two consecutive gather kernels (last full one)
-    idx = [i for i, (n, _) in enumerate(rows) if "gather_kernel" in n]
+    idx = [i for i, (n, _) in enumerate(rows) if "gather_kernel" in n or "gather_inline_kernel" in n]
     step = rows[idx[-2]:idx[-1]] if len(idx) >= 2 else rows
     agg = collections.OrderedDict()
     for n, us in step:
@@ -81,7 +81,8 @@ def launches(path: str, tag: str) -> None:
     print("\n".join(out))
 
 
-def full(path: str, tag: str) -> None:
+def full(path: str, tag: str, skip: str = "-s 75 -c 25") -> None:
+    SKIP = skip
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     r = list(csv.reader(io.StringIO(raw)))
@@ -98,7 +99,7 @@ def full(path: str, tag: str) -> None:
     ki = hdr.index("Kernel Name")
     out = [f"# {tag}: ncu --set full, one mini-batch (N=1, configs[1] model)\n",
            f"Source: `{os.path.basename(path)}` (`ncu --set full --clock-control none "
-           f"--import-source on -k regex:\"gemm_bf16|allreduce_sgd|xent|gather\" -s 78 -c 26 "
+           f"--import-source on -k regex:\"gemm_bf16|allreduce_sgd|xent|gather\" {SKIP} "
            f"python tools/profile_step.py --size 65536`).  `traffic` per launch = DRAM read + "
            f"write.\n",
            "| # | kernel | " + " | ".join(f"{lab} ({u})" if u else lab for _, lab, u in idx) + " |",
@@ -115,12 +116,13 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--full")
     ap.add_argument("--tag", default="r01")
+    ap.add_argument("--skip", default="-s 75 -c 25", help="the ncu -s/-c flags of the capture")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     if a.launches:
         launches(a.launches, a.tag)
     if a.full:
-        full(a.full, a.tag)
+        full(a.full, a.tag, a.skip)
 
 
 if __name__ == "__main__":
