@@ -27,7 +27,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = "samples/sec at 1/2/4/8 B200; scale-out/in stall ms vs stop-resume"
 UNIT = "samples/s"
-WORKLOAD = dict(dim=4096, hidden=4096, classes=4096, layers=8, batch=512, size=1 << 20)
+WORKLOAD = dict(dim=4096, hidden=4096, classes=4096, layers=8, batch=512, size=1 << 20,
+                name="mlp4096x8_bf16_b512_sgd")
+# BASELINE.json configs[4]: ~1B-param wide MLP (8 x Linear(11264 -> 11264) = 1,015,021,568
+# parameters), the allreduce-bound regime; dataset 2^18 samples (5.9 GB bf16) per GPU
+WIDE = dict(dim=11264, hidden=11264, classes=11264, layers=8, batch=512, size=1 << 18,
+            name="mlp11264x8_bf16_b512_sgd")
+WORKLOADS = {"mlp4096x8": WORKLOAD, "wide11264x8": WIDE}
 
 
 def flops_per_sample(w=WORKLOAD) -> float:
@@ -157,7 +163,7 @@ def run_b200(args, rank: int, world: int) -> None:
         dist.init_process_group("gloo")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    w = WORKLOAD
+    w = WORKLOADS[args.workload]
     cfg = rt.JobConfig(model=rt.MLP, size=w["size"], dim=w["dim"], seed=1, noise=0.0,
                        num_classes=w["classes"], layers=w["layers"], hidden=w["hidden"],
                        eta=0.05, decay=0.0, batch=w["batch"], per_worker_batch=w["batch"],
@@ -191,7 +197,7 @@ def run_b200(args, rank: int, world: int) -> None:
     job.sync()
     barrier()
 
-    flops, P = flops_per_sample()
+    flops, P = flops_per_sample(w)
     # ---- value: K pipelined steps (inputs HBM-resident), device-timed on the job stream
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -249,12 +255,33 @@ def run_b200(args, rank: int, world: int) -> None:
         upd = {"bound": "hbm", "where": "fused into wgrad GEMM epilogue (backward phase)",
                "bytes_per_step": 10 * P}
     else:
-        nv = 2.0 * (world - 1) / world * 2 * P  # bf16 RS + AG bytes per GPU per direction
-        upd = {"bound": "nvlink", "achieved": nv / (upd_ms / 1e3) / 1e9, "peak": 770.0,
-               "unit": "GB/s", "frac": nv / (upd_ms / 1e3) / 1e9 / 770.0,
-               "bytes_per_step": nv, "per_step_ms": upd_ms,
-               "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction",
-               "kernel": "fused reduce-scatter + sharded SGD + all-gather over NVLink P2P"}
+        # allreduce bus bytes per GPU per direction (bf16 reduce-scatter + all-gather,
+        # 2(N-1)/N x 2P); the exchange's halves are timed where they run
+        mode = job.exchange_mode()
+        half = (world - 1) / world * 2 * P
+        if mode == 3:
+            # reduce-scatter stored from the wgrad GEMM epilogues (inside the backward): only
+            # the all-gather half (push collective: shard sum + SGD + weight stores) is exposed
+            upd = {"bound": "nvlink", "achieved": half / (upd_ms / 1e3) / 1e9, "peak": 770.0,
+                   "unit": "GB/s", "frac": half / (upd_ms / 1e3) / 1e9 / 770.0,
+                   "bytes_per_step": half, "per_step_ms": upd_ms,
+                   "allreduce_bus_bytes_per_step": 2 * half,
+                   "exposed_allreduce_bus_gbs": 2 * half / (upd_ms / 1e3) / 1e9,
+                   "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction "
+                                  "(900 GB/s NVLink 5 nominal)",
+                   "kernel": "push all-gather + sharded SGD (reduce-scatter routed from the "
+                             "wgrad GEMM epilogues, overlapped with the backward)"}
+        else:
+            nv = 2 * half
+            upd = {"bound": "nvlink", "achieved": nv / (upd_ms / 1e3) / 1e9, "peak": 770.0,
+                   "unit": "GB/s", "frac": nv / (upd_ms / 1e3) / 1e9 / 770.0,
+                   "bytes_per_step": nv, "per_step_ms": upd_ms,
+                   "allreduce_bus_bytes_per_step": nv,
+                   "exposed_allreduce_bus_gbs": nv / (upd_ms / 1e3) / 1e9,
+                   "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction "
+                                  "(900 GB/s NVLink 5 nominal)",
+                   "kernel": "fused reduce-scatter + sharded SGD + all-gather over NVLink P2P"}
+        upd["exchange_mode"] = mode
 
     # ---- roofline of the dominant kernel (profiles/r01_kernel_shares.md): at N=1 the fused
     # weight-gradient GEMM + SGD update (51% of the step), HBM-bound: per launch (one layer,
@@ -270,7 +297,8 @@ def run_b200(args, rank: int, world: int) -> None:
         dominant = {"bound": "hbm", "kernel": "gemm_bf16_2sm_kernel<128,MN,MN,sgd> "
                     "(weight gradient + fused SGD update, one launch per layer)",
                     "achieved": gbs, "peak": peak_h, "unit": "GB/s", "frac": gbs / peak_h,
-                    "traffic": _ncu_traffic("wgrad+sgd"), "traffic_source": NCU_FULL,
+                    "traffic": _ncu_traffic("wgrad+sgd") if w is WORKLOAD else None,
+                    "traffic_source": NCU_FULL,
                     "algorithmic_bytes_per_launch": alg, "launch_ms": per_launch_ms,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)"}
     else:
@@ -278,7 +306,8 @@ def run_b200(args, rank: int, world: int) -> None:
         dominant = {"bound": "tensor", "kernel": "gemm_bf16_2sm_kernel<128,MN,MN> "
                     "(weight gradient, bf16 out, one launch per layer)",
                     "achieved": tf, "peak": peak_t, "unit": "TFLOP/s", "frac": tf / peak_t,
-                    "traffic": _ncu_traffic("wgrad]"), "traffic_source": NCU_FULL,
+                    "traffic": _ncu_traffic("wgrad]") if w is WORKLOAD else None,
+                    "traffic_source": NCU_FULL,
                     "algorithmic_flop_per_launch": 2 * w["batch"] * (P // n_wgrad),
                     "launch_ms": per_launch_ms,
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"}
@@ -300,7 +329,7 @@ def run_b200(args, rank: int, world: int) -> None:
 
     # ---- CPU baseline (oracle port), bounded sample on this host, rank 0 at N=1 only
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and w is WORKLOAD:
         batch = int(os.environ.get("EDL_CPU_BATCH", "64"))
         t = cpu_reference_step(batch, 2)
         cpu = {"value": batch / min(t), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
@@ -312,7 +341,7 @@ def run_b200(args, rank: int, world: int) -> None:
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (HBM-resident 2^20 x 4096 bf16 splitmix64 dataset, random-init MLP)",
-        "config": {"workload": "mlp4096x8_bf16_b512_sgd", "layers": w["layers"],
+        "config": {"workload": w["name"], "layers": w["layers"],
                    "width": w["hidden"], "classes": w["classes"],
                    "global_batch": samples // args.steps, "per_gpu_batch": w["batch"],
                    "dataset_samples": w["size"], "parallelism": f"dp{world}",
@@ -371,6 +400,9 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="mlp4096x8",
+                    help="mlp4096x8 = BASELINE configs[1] (the headline); wide11264x8 = "
+                         "configs[4], the ~1B-param allreduce-bound MLP")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))

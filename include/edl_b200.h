@@ -279,6 +279,11 @@ int edl_job_lease_snapshot(const EdlJob* job, uint8_t* buf, size_t cap, size_t* 
  * weight-gradient GEMMs alone — a sub-phase of the backward), the steps
  * profiled and the number of library kernels launched since the last reset.            */
 void* edl_job_stream(const EdlJob* job);
+/* How the N>1 gradient exchange of this job runs (valid after the first step): 0 one fused
+ * reduce-scatter + SGD + all-gather kernel after the backward, 1 per-layer side-stream
+ * collectives, 2 per-layer copy-engine transfers, 3 reduce-scatter routed from the
+ * weight-gradient GEMM epilogues + push all-gather (the default with one member per GPU). */
+int edl_job_exchange_mode(const EdlJob* job);
 /* Multi-process data parallelism (one process per GPU, e.g. torchrun): every process
  * creates the job with the full ring, device = its GPU for its own worker and -1 for
  * workers hosted elsewhere; exports a blob of CUDA IPC handles (gradients, weights, flags,

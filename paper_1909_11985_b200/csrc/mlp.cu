@@ -50,29 +50,34 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// One CTA (256 threads) per row; classes <= 256 * kPer values held in registers.
+// One CTA (256 threads) per row; classes <= 256 * kPer values held in registers
+// (kPer = 16: <= 4096 classes, the configs[1] model; kPer = 64: <= 16384, configs[4]).
 constexpr int kXentThreads = 256;
-constexpr int kPer = 16;
-// Ordered loss sum of `rows` per-row losses by one CTA: thread t sums rows t, t+256, ...
-// then thread 0 adds the 256 partials in order (the same order as sum_rows).
+constexpr int kXentMaxClasses = kXentThreads * 64;
+// Deterministic loss sum of `rows` per-row losses by one CTA: thread t sums rows t, t+256, ...
+// in order, a fixed warp-shuffle tree combines the lanes and thread 0 adds the 8 warp
+// partials in order (a serial 256-term tail here cost ~4 us per mini-batch).
 __device__ void ordered_row_sum(const float* v, int rows, double* out, double* part) {
   double acc = 0.0;
   for (int r = threadIdx.x; r < rows; r += blockDim.x) acc += static_cast<double>(v[r]);
-  part[threadIdx.x] = acc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x / 32] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int k = 0; k < static_cast<int>(blockDim.x); ++k) t += part[k];
+    for (int k = 0; k < static_cast<int>(blockDim.x / 32); ++k) t += part[k];
     *out += t;
   }
 }
 
+template <int kPer>
 __global__ void __launch_bounds__(kXentThreads)
     xent_kernel(const float* __restrict__ logits, const int32_t* __restrict__ labels, int classes,
                 __nv_bfloat16* __restrict__ dlogits, float* __restrict__ row_loss,
                 double* __restrict__ loss_out, unsigned* __restrict__ done) {
   __shared__ float red[kXentThreads / 32];
-  __shared__ double part[kXentThreads];
+  __shared__ double part[kXentThreads / 32];
   __shared__ bool last;
   // launched with programmatic serialization after the last forward GEMM: wait for it here
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -128,7 +133,7 @@ __global__ void __launch_bounds__(kXentThreads)
 }
 
 __global__ void sum_rows_kernel(const float* __restrict__ v, int rows, double* __restrict__ out) {
-  __shared__ double part[256];
+  __shared__ double part[8];
   ordered_row_sum(v, rows, out, part);
 }
 
@@ -144,7 +149,7 @@ int mlp_init_weights(float* master, __nv_bfloat16* w, size_t n, uint64_t seed, u
 int softmax_xent(const float* logits, const int32_t* labels, int rows, int classes,
                  __nv_bfloat16* dlogits, float* row_loss, double* loss_out, unsigned* done,
                  cudaStream_t s) {
-  if (classes > kXentThreads * kPer) return fail(EDL_EINVAL, "softmax_xent: classes > 4096");
+  if (classes > kXentMaxClasses) return fail(EDL_EINVAL, "softmax_xent: classes > 16384");
   if (rows <= 0) return EDL_OK;
   if (loss_out && !done) return fail(EDL_EINVAL, "softmax_xent: loss sum needs a counter");
   cudaLaunchConfig_t cfg = {};
@@ -156,8 +161,12 @@ int softmax_xent(const float* logits, const int32_t* labels, int rows, int class
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  EDL_CUDA_TRY(cudaLaunchKernelEx(&cfg, xent_kernel, logits, labels, classes, dlogits, row_loss,
-                                  loss_out, done));
+  if (classes <= kXentThreads * 16)
+    EDL_CUDA_TRY(cudaLaunchKernelEx(&cfg, xent_kernel<16>, logits, labels, classes, dlogits,
+                                    row_loss, loss_out, done));
+  else
+    EDL_CUDA_TRY(cudaLaunchKernelEx(&cfg, xent_kernel<64>, logits, labels, classes, dlogits,
+                                    row_loss, loss_out, done));
   return EDL_OK;
 }
 

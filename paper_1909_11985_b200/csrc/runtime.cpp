@@ -94,7 +94,7 @@ int Job::init(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
     if (L_ > kCollMaxSegs) return fail(EDL_EINVAL, "job: too many MLP layers");
     if (cfg.data.dim % 8 || cfg.hidden % 8 || cfg.num_classes % 8)
       return fail(EDL_EINVAL, "job: MLP widths must be multiples of 8 (16-byte TMA rows)");
-    if (cfg.num_classes > 4096) return fail(EDL_EINVAL, "job: num_classes > 4096");
+    if (cfg.num_classes > 16384) return fail(EDL_EINVAL, "job: num_classes > 16384");
     for (int l = 0; l < L_; ++l) {
       in_.push_back(l == 0 ? cfg.data.dim : cfg.hidden);
       out_.push_back(l == L_ - 1 ? cfg.num_classes : cfg.hidden);

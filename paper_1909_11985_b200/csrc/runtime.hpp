@@ -181,6 +181,10 @@ class Job {
   // all-gather of the sharded fp32 master across replicas (collective: every process calls)
   int gather_master();
   void set_profile(bool on) { profile_ = on; }
+  // how the N>1 gradient exchange runs (fixed at the first step after the peers are known):
+  // 0 one fused collective after the backward, 1 per-layer side-stream collectives,
+  // 2 per-layer copy-engine transfers, 3 reduce-scatter routed from the wgrad GEMM epilogues
+  int exchange_mode() const { return overlap_mode_; }
   // accumulated device ms per phase (gather, forward, loss, backward, update) + launches
   void phase_totals(double* ms, uint64_t* steps, uint64_t* launches) const {
     for (int k = 0; k < kPhases; ++k) ms[k] = phase_ms_[k];

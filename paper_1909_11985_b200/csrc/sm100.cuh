@@ -161,7 +161,11 @@ __device__ __forceinline__ void cluster_sync() {
 __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+  // default semantics (.release.cta, as CUTLASS's ClusterBarrier::arrive): the barriers this
+  // signals order TMEM reads / smem reuse (tcgen05 fences, async-proxy waits), not generic
+  // memory; .release.cluster lowered to MEMBAR.GPU + ERRBAR, which waited for the caller's
+  // outstanding bulk stores (~20% of the fused-SGD epilogue's stall samples)
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote)
                : "memory");
 }
 // 2-SM TMA load: bytes land in this CTA's smem, completion is counted on the pair leader's

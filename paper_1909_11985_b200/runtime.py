@@ -205,6 +205,11 @@ class Job:
     def set_profile(self, on: bool) -> None:
         self._L.edl_job_set_profile(self._h, 1 if on else 0)
 
+    def exchange_mode(self) -> int:
+        """0 fused collective after the backward, 1/2 per-layer overlap, 3 reduce-scatter
+        routed from the wgrad GEMM epilogues (include/edl_b200.h edl_job_exchange_mode)."""
+        return int(self._L.edl_job_exchange_mode(self._h))
+
     PHASES = ("gather", "forward", "loss", "backward", "update", "wgrad")
 
     def counters(self) -> dict:
