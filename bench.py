@@ -215,6 +215,7 @@ def run_b200(args, rank: int, world: int) -> None:
         e0.record(stream)
         for _ in range(args.steps):
             job.step()
+        job.join()  # the last mini-batch's deferred push collective runs on a side stream
         e1.record(stream)
         torch.cuda.synchronize()
         launches = job.counters()["launches"]  # library kernels of exactly the K timed steps
@@ -321,6 +322,7 @@ def run_b200(args, rank: int, world: int) -> None:
     for _ in range(args.steps):
         job.step()
         losses.append(job.sync().loss)
+    job.join()
     e3.record(stream)
     torch.cuda.synchronize()
     ms_e2e = max_over_ranks(e2.elapsed_time(e3))

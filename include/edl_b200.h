@@ -284,6 +284,11 @@ void* edl_job_stream(const EdlJob* job);
  * collectives, 2 per-layer copy-engine transfers, 3 reduce-scatter routed from the
  * weight-gradient GEMM epilogues + push all-gather (the default with one member per GPU). */
 int edl_job_exchange_mode(const EdlJob* job);
+/* Orders the job stream (edl_job_stream) after all device work of the launched mini-batches,
+ * including the push collective that exchange mode 3 defers onto a side stream to overlap
+ * the next mini-batch's forward.  No host synchronisation: record a CUDA event on the job
+ * stream after this call to time a sequence of edl_job_step calls. */
+int edl_job_join(EdlJob* job);
 /* Multi-process data parallelism (one process per GPU, e.g. torchrun): every process
  * creates the job with the full ring, device = its GPU for its own worker and -1 for
  * workers hosted elsewhere; exports a blob of CUDA IPC handles (gradients, weights, flags,

@@ -161,6 +161,7 @@ def _declare(L: C.CDLL) -> None:
         "edl_job_stream": ([vp], vp),
         "edl_job_set_profile": ([vp, i32], None),
         "edl_job_exchange_mode": ([vp], ci),
+        "edl_job_join": ([vp], ci),
         "edl_job_counters": ([vp, P(f64), P(u64), P(u64)], None),
         "edl_job_reset_counters": ([vp], None),
         "edl_job_export": ([vp, vp, sz, P(sz)], ci),

@@ -357,6 +357,7 @@ extern "C" {
 void* edl_job_stream(const EdlJob* job) { return job->job->stream(); }
 void edl_job_set_profile(EdlJob* job, int32_t on) { job->job->set_profile(on != 0); }
 int edl_job_exchange_mode(const EdlJob* job) { return job->job->exchange_mode(); }
+int edl_job_join(EdlJob* job) { return job->job->join_side(); }
 void edl_job_counters(const EdlJob* job, double* phase_ms, uint64_t* steps, uint64_t* launches) {
   job->job->phase_totals(phase_ms, steps, launches);
 }

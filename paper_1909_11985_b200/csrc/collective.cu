@@ -241,6 +241,20 @@ __global__ void __launch_bounds__(256) push_allreduce_sgd_kernel(CollArgs a) {
         }
         apply8<kMomentum>(a, i, gs);
       }
+      if (a.ag_signal) {
+        // every thread's weight stores of layer l (local and peer) before the count
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          uint32_t* ctr = a.flags[a.me] + kAgFlagOffset + kCollMaxSegs * kCollMaxReplicas + l;
+          if (atomicAdd(ctr, 1u) == gridDim.x - 1) {  // last CTA of this replica for layer l
+            __threadfence_system();
+            *ctr = 0;  // every CTA has counted: ready for the next mini-batch
+            for (int r = 0; r < a.n_rep; ++r)
+              st_release_sys(ag_layer_flags(a.flags[r], l) + a.me, a.epoch);
+          }
+        }
+      }
     }
   }
   cross_replica_barrier(a, 1);

@@ -16,7 +16,20 @@ constexpr int kCollMaxSegs = 64;      // owned parameter segments (one per MLP l
 // copy-engine overlap flags [2 kinds][kCollMaxSegs layers][kCollMaxReplicas] (uint32 each).
 constexpr size_t kCollBarrierWords = 2ull * kCollMaxBlocks * kCollMaxReplicas;
 constexpr size_t kCeFlagWords = 2ull * kCollMaxSegs * kCollMaxReplicas;
-constexpr size_t kCollFlagBytes = (kCollBarrierWords + kCeFlagWords) * sizeof(uint32_t);
+// Deferred all-gather (push collective overlapped with the next mini-batch's forward): per
+// layer, "replica src's updated bf16 weights of layer l are in your W" [kCollMaxSegs][
+// kCollMaxReplicas], then this replica's per-layer CTA completion counters [kCollMaxSegs].
+constexpr size_t kAgFlagWords = static_cast<size_t>(kCollMaxSegs) * kCollMaxReplicas + kCollMaxSegs;
+constexpr size_t kAgFlagOffset = kCollBarrierWords + kCeFlagWords;  // in words
+constexpr size_t kCollFlagBytes =
+    (kCollBarrierWords + kCeFlagWords + kAgFlagWords) * sizeof(uint32_t);
+// this replica's flags for layer l: one word per source replica
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline uint32_t* ag_layer_flags(uint32_t* flags, int l) {
+  return flags + kAgFlagOffset + static_cast<size_t>(l) * kCollMaxReplicas;
+}
 
 struct CollArgs {
   const __nv_bfloat16* grads[kCollMaxSources];  // ring order; local or peer pointers
@@ -53,6 +66,10 @@ struct CollArgs {
   __nv_bfloat16* recv_me = nullptr;                     // this replica's recv
   __nv_bfloat16* recv_peer[kCollMaxReplicas];           // replica r's recv (peer-mapped)
   int src_rep[kCollMaxSources];                         // ring member k -> replica index
+  // deferred all-gather: after its share of layer l every CTA counts itself; the last one
+  // signals "layer l of my shard is in your W" to every replica (ag_layer_flags), so the
+  // next mini-batch's forward GEMM of layer l can start while later layers are in flight
+  int ag_signal = 0;
 };
 
 // f64 ring allreduce of [grad_sum, count] vectors + sgd_step, over peer pointers

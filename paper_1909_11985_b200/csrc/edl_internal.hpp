@@ -44,6 +44,12 @@ struct EpiParams {
   int route_rows;
   int route_me;
   int dbg;  // trace builds only: 1 = skip the K loop, 2 = skip the epilogue work
+  // B operand (the layer's weights) all-gathered by the previous mini-batch's deferred push
+  // collective: the producer waits until wait_flags[r] >= wait_epoch for r < wait_n (every
+  // replica signalled this layer) before its first load.  nullptr: no wait.
+  const uint32_t* wait_flags;
+  int wait_n;
+  uint32_t wait_epoch;
 };
 constexpr int kMaxPeerMaps = 8;
 struct PeerMaps {
@@ -61,6 +67,10 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B,
                    int b_mn, void* C, int ldc, int M, int N, int K, int relu, int out_f32,
                    const void* mask, int ldm, int bn);
 int gemm_plan_run(const GemmPlan& p, cudaStream_t stream, float sgd_scale = 0.f);
+// gemm_plan_run whose producer first waits for n per-replica flags >= epoch (system-scope
+// acquire; the deferred all-gather's "layer l is in your W" signals, collective.hpp)
+int gemm_plan_run_wait(const GemmPlan& p, cudaStream_t stream, const uint32_t* flags, int n,
+                       uint32_t epoch);
 // Weight-gradient GEMM with the SGD step fused into its epilogue (CTA-pair kernel, one
 // replica): dW = A^T-major x B^T-major as for wgrad, then master -= scale * bf16(dW) and
 // W (bf16) <- master, with no gradient buffer round trip through HBM.

@@ -118,6 +118,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     const uint32_t tx = C::kABytes + (B_MN ? C::kBBytesMN : C::kBBytesK);
+    if (ep.wait_flags) {  // weights still arriving from the deferred all-gather
+      if (lane == 0) wait_flags_acquire(ep.wait_flags, ep.wait_n, ep.wait_epoch);
+      __syncwarp();
+    }
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int m0 = (tile % m_tiles) * BM;
       const int n0 = (tile / m_tiles) * BN;
@@ -439,6 +443,10 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
     const uint32_t tx = 2 * (C::kABytes + (B_MN ? C::kBBytesMN : C::kBBytesK));
     TRACE_T0(t_prod);
     const uint16_t a_mask = static_cast<uint16_t>((1u << pr) | (1u << (pr + 2)));
+    if (ep.wait_flags) {  // weights still arriving from the deferred all-gather
+      if (lane == 0) wait_flags_acquire(ep.wait_flags, ep.wait_n, ep.wait_epoch);
+      __syncwarp();
+    }
     for (int w = unit; w < num_work; w += n_units) {
       const int m0 = tile_m(w) * 256 + static_cast<int>(pr) * 128;
       const int n0 = tile_n(w) * BN + static_cast<int>(pr) * C::kHalfN;
@@ -1105,6 +1113,16 @@ int gemm_plan_route(GemmPlan* p, int rows_per_owner, int me, void* const* dst, i
   p->ep.route_rows = rows_per_owner;
   p->ep.route_me = me;
   return EDL_OK;
+}
+
+int gemm_plan_run_wait(const GemmPlan& p, cudaStream_t stream, const uint32_t* flags, int n,
+                       uint32_t epoch) {
+  if (!flags || n <= 0) return gemm_plan_run(p, stream);
+  GemmPlan q = p;
+  q.ep.wait_flags = flags;
+  q.ep.wait_n = n;
+  q.ep.wait_epoch = epoch;
+  return gemm_plan_run(q, stream);
 }
 
 int gemm_plan_init_sgd(GemmPlan* p, const void* A, int lda, int a_mn, const void* B, int ldb,

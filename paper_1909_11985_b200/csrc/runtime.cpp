@@ -253,6 +253,8 @@ int Job::build_replica(Replica* r) {
     r->ev_upd.assign(static_cast<size_t>(L_), nullptr);
     for (auto& e : r->ev_upd) EDL_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     EDL_CUDA_TRY(cudaEventCreateWithFlags(&r->ev_side, cudaEventDisableTiming));
+    EDL_CUDA_TRY(cudaEventCreateWithFlags(&r->ev_bwd, cudaEventDisableTiming));
+    EDL_CUDA_TRY(cudaEventCreateWithFlags(&r->ev_push, cudaEventDisableTiming));
     r->ev_grad.assign(static_cast<size_t>(L_), nullptr);
     for (auto& e : r->ev_grad) EDL_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
@@ -309,7 +311,9 @@ int Job::build_worker(Worker* w, Replica* r) {
   w->runs_cap = r->rows_cap + 2;
   EDL_TRY(dalloc(&w->runs_dev, static_cast<size_t>(w->runs_cap)));
   EDL_CUDA_TRY(cudaMallocHost(&w->runs_host, sizeof(EdlRun) * w->runs_cap * kSlots));
-  EDL_TRY(dalloc(&w->loss, 1));
+  // MLP: two slots by mini-batch parity (the deferred push collective of t reads slot t&1
+  // while t+1's gather / softmax already write the other)
+  EDL_TRY(dalloc(&w->loss, 2));
   if (mlp_)
     EDL_TRY(dalloc(&w->grad, P_));
   else
@@ -387,6 +391,9 @@ void Job::free_replica(Replica* r) {
     *st = nullptr;
   }
   if (r->ev_side) cudaEventDestroy(r->ev_side);
+  if (r->ev_bwd) cudaEventDestroy(r->ev_bwd);
+  if (r->ev_push) cudaEventDestroy(r->ev_push);
+  r->ev_bwd = r->ev_push = nullptr;
   if (r->side) {
     cudaStreamSynchronize(r->side);
     cudaStreamDestroy(r->side);
@@ -670,9 +677,10 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
   DeviceGuard dg(r->device);
   const bool prof = profile_ && r == primary();
   const int64_t rows = static_cast<int64_t>(w->plan.size());
+  double* wloss = w->loss + (t_ & 1);
   EDL_CUDA_TRY(cudaEventRecord(w->ev_w0[slot], r->stream));
   if (rows == 0) {  // ShardPending for the whole step: contributes a zero gradient
-    EDL_CUDA_TRY(cudaMemsetAsync(w->loss, 0, sizeof(double), r->stream));
+    EDL_CUDA_TRY(cudaMemsetAsync(wloss, 0, sizeof(double), r->stream));
     EDL_CUDA_TRY(cudaMemsetAsync(w->grad, 0, sizeof(__nv_bfloat16) * P_, r->stream));
     if (overlap_ && last) EDL_TRY(finish_layer_colls(r));  // mode 3 needs rows > 0
     EDL_CUDA_TRY(cudaEventRecord(w->ev_w1[slot], r->stream));
@@ -682,20 +690,29 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
   cudaEvent_t m = prof ? mark_begin(r->stream) : nullptr;
   EdlRun* host = w->runs_host + static_cast<size_t>(slot) * w->runs_cap;
   if (w->n_runs <= kInlineRuns) {  // runs ride in the launch parameters; loss zeroed there
-    EDL_TRY(gather_inline(r->ds, host, w->n_runs, rows, r->act[0], r->labels, w->loss,
+    EDL_TRY(gather_inline(r->ds, host, w->n_runs, rows, r->act[0], r->labels, wloss,
                           r->stream));
   } else {
-    EDL_CUDA_TRY(cudaMemsetAsync(w->loss, 0, sizeof(double), r->stream));
+    EDL_CUDA_TRY(cudaMemsetAsync(wloss, 0, sizeof(double), r->stream));
     EDL_CUDA_TRY(cudaMemcpyAsync(w->runs_dev, host, sizeof(EdlRun) * w->n_runs,
                                  cudaMemcpyHostToDevice, r->stream));
     EDL_TRY(gather(r->ds, w->runs_dev, w->n_runs, rows, r->act[0], r->labels, r->stream));
   }
   m = mark(slot, 0, m, r->stream);
-  for (int l = 0; l < L_; ++l) EDL_TRY(gemm_plan_run(r->fwd[l], r->stream));
+  if (r->ag_wait_epoch) {
+    // layer l's weights may still be arriving from the previous mini-batch's push collective
+    // (side stream, every replica): the GEMM's producer waits for the layer's flags
+    const int n_rep = static_cast<int>(peers_.size());
+    for (int l = 0; l < L_; ++l)
+      EDL_TRY(gemm_plan_run_wait(r->fwd[l], r->stream, ag_layer_flags(r->flags, l), n_rep,
+                                 r->ag_wait_epoch));
+  } else {
+    for (int l = 0; l < L_; ++l) EDL_TRY(gemm_plan_run(r->fwd[l], r->stream));
+  }
   m = mark(slot, 1, m, r->stream);
   // softmax cross-entropy + the worker's ordered loss sum in one kernel
   EDL_TRY(softmax_xent(r->logits, r->labels, static_cast<int>(rows), cfg_.num_classes, r->dlog,
-                       r->row_loss, w->loss, r->xent_done, r->stream));
+                       r->row_loss, wloss, r->xent_done, r->stream));
   m = mark(slot, 2, m, r->stream);
   for (int l = L_ - 1; l >= 0; --l) {
     if (l > 0) EDL_TRY(gemm_plan_run(r->dgrad[l], r->stream));
@@ -708,6 +725,11 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
       // dW with the reduce-scatter in its epilogue: rows owned elsewhere are stored into the
       // owner's recv over NVLink while the backward continues; the shard update + all-gather
       // run once, after the backward (the push collective with its phase A skipped)
+      if (r->side_pending) {
+        // the previous push collective reads every replica's recv until its final barrier
+        EDL_CUDA_TRY(cudaStreamWaitEvent(r->stream, r->ev_push, 0));
+        r->side_pending = false;
+      }
       EDL_TRY(gemm_plan_run(w->wgrad_rs[l], r->stream));
     } else {
       EDL_TRY(gemm_plan_run(w->wgrad[l], r->stream));
@@ -902,6 +924,7 @@ int Job::take_pre_snapshot() {
 
 // Immediate scale-in of `ids` (failed workers): shards back at their reported offsets.
 int Job::remove_members(const std::vector<std::string>& ids) {
+  EDL_TRY(join_side());  // the deferred push collective updates master / W
   std::vector<std::string> keep;
   for (const auto& id : ring_) {
     if (std::find(ids.begin(), ids.end(), id) == ids.end()) {
@@ -935,6 +958,7 @@ bool get(const std::string& b, size_t* o, T* v) {
 }  // namespace
 
 int Job::save_checkpoint(const std::string& path) {
+  EDL_TRY(join_side());  // the deferred push collective updates master / W
   if (path.empty()) return fail(EDL_EINVAL, "checkpoint: empty path");
   for (const auto& p : peers_)
     if (!p.local) return fail(EDL_EINVAL, "checkpoint: multi-process jobs gather first (not supported)");
@@ -982,6 +1006,7 @@ int Job::save_checkpoint(const std::string& path) {
 }
 
 int Job::load_checkpoint(const std::string& path) {
+  EDL_TRY(join_side());  // the deferred push collective updates master / W
   for (const auto& p : peers_)
     if (!p.local) return fail(EDL_EINVAL, "checkpoint: multi-process restore not supported");
   if (!events_.empty()) return fail(EDL_RETRY, "checkpoint: a scaling operation is pending");
@@ -1069,6 +1094,7 @@ int Job::load_checkpoint(const std::string& path) {
 }
 
 int Job::recover(const std::vector<std::string>& failed, bool approximate, EdlRecovery* out) {
+  EDL_TRY(join_side());  // the deferred push collective updates master / W
   for (const auto& p : peers_)
     if (!p.local) return fail(EDL_EINVAL, "recover: multi-process recovery not supported");
   size_t hit = 0;
@@ -1403,7 +1429,7 @@ int Job::reduce_and_update(uint64_t count, uint64_t t, int slot) {
   if (ring_.size() > static_cast<size_t>(kCollMaxSources))
     return fail(EDL_EINVAL, "job: ring larger than the collective supports");
   Replica* prim = primary();
-  cudaEvent_t m = mark_begin(prim->stream);
+  cudaEvent_t m = ag_defer_ ? nullptr : mark_begin(prim->stream);
   const uint32_t epoch = ++coll_epoch_;  // one collective per mini-batch, same on every GPU
   for (int me = 0; me < n_rep; ++me) {
     if (!peers_[me].local) continue;  // launched by its own process
@@ -1416,7 +1442,7 @@ int Job::reduce_and_update(uint64_t count, uint64_t t, int slot) {
       CollArgs a;
       for (const auto& id : ring_) {
         a.grads[a.n_src++] = workers_[id]->grad;
-        a.losses[a.n_loss++] = workers_[id]->loss;
+        a.losses[a.n_loss++] = workers_[id]->loss + (t & 1);  // run_worker_mlp's slot
       }
       for (const auto& p : peers_) {
         a.flags[a.n_dst] = p.flags;
@@ -1448,7 +1474,29 @@ int Job::reduce_and_update(uint64_t count, uint64_t t, int slot) {
         for (const auto& id : ring_)
           if (host_index(id) == me) a.own_grad = workers_[id]->grad;
       }
-      EDL_TRY(allreduce_sgd(a, r->stream));
+      if (ag_defer_ && a.push && a.skip_push) {
+        // deferred all-gather: the push collective runs on the side stream after this
+        // mini-batch's backward, concurrently with the next mini-batch's gather / forward;
+        // per-layer flags release the forward GEMMs layer by layer.  A small grid (one CTA
+        // per SM) co-resides with the forward GEMMs instead of blocking their CTAs.
+        static int ag_blocks = -1;
+        if (ag_blocks < 0) {
+          const char* e = getenv("EDL_AG_BLOCKS");
+          ag_blocks = e ? atoi(e) : 148;
+        }
+        a.blocks = ag_blocks;
+        a.ag_signal = 1;
+        EDL_CUDA_TRY(cudaEventRecord(r->ev_bwd, r->stream));
+        EDL_CUDA_TRY(cudaStreamWaitEvent(r->side, r->ev_bwd, 0));
+        cudaEvent_t ms = (r == prim) ? mark_begin(r->side) : nullptr;
+        EDL_TRY(allreduce_sgd(a, r->side));
+        if (ms) mark(slot, 4, ms, r->side);
+        EDL_CUDA_TRY(cudaEventRecord(r->ev_push, r->side));
+        r->ag_wait_epoch = epoch;
+        r->side_pending = true;
+      } else {
+        EDL_TRY(allreduce_sgd(a, r->stream));
+      }
     } else {
       LinearCollArgs a;
       for (const auto& id : ring_) {
@@ -1469,14 +1517,26 @@ int Job::reduce_and_update(uint64_t count, uint64_t t, int slot) {
     }
     launches_ += 1;
   }
-  m = mark(slot, 4, m, prim->stream);
+  if (!ag_defer_) m = mark(slot, 4, m, prim->stream);
   (void)m;
+  return EDL_OK;
+}
+
+int Job::join_side() {
+  for (auto& [dev, r] : reps_) {
+    if (!r->side_pending && !r->ag_wait_epoch) continue;
+    DeviceGuard g(dev);
+    if (r->side_pending) EDL_CUDA_TRY(cudaStreamWaitEvent(r->stream, r->ev_push, 0));
+    r->side_pending = false;
+    r->ag_wait_epoch = 0;
+  }
   return EDL_OK;
 }
 
 // All-gather of the sharded fp32 master among the local replicas, enqueued on their streams
 // (no host sync): before a topology switch changes the sharding, and for checkpoints.
 int Job::consolidate_master() {
+  EDL_TRY(join_side());  // the deferred push collective updates master / W
   if (!mlp_ || peers_.size() < 2 || dry_) return EDL_OK;
   const uint32_t epoch = ++coll_epoch_;
   const int n_rep = static_cast<int>(peers_.size());
@@ -1504,6 +1564,7 @@ int Job::consolidate_master() {
 // lowest existing replica, ordered after the source's work so far; the source's next write
 // to its model is its next collective, whose barrier waits for the newcomer.
 int Job::broadcast_model(Replica* src, Replica* dst) {
+  EDL_TRY(join_side());  // the deferred push collective updates master / W
   if (dry_ || src == dst) return EDL_OK;
   {
     DeviceGuard dg(src->device);
@@ -1692,6 +1753,18 @@ int Job::step(EdlStepReport* out) {
   if (mlp_ && count > 0 && overlap_env < 0 && peers_.size() > 1 && rs_eligible())
     overlap_mode_ = 3;
   overlap_ = overlap_mode_ != 0;
+  // deferred all-gather (mode 3, EDL_AG_DEFER=1): the push collective of this mini-batch
+  // overlaps the next mini-batch's forward.  Opt-in: measured on B200 the push kernel on a
+  // grid small enough to co-reside with the forward GEMMs (148 CTAs) moves 290-360 GB/s
+  // against ~530 GB/s with its full grid after the backward, and the forward is paced by it
+  // (N=2 1.00M vs 1.12M samples/s, N=4 1.81M vs 1.83M)
+  static int defer_env = -1;
+  if (defer_env < 0) {
+    const char* e = getenv("EDL_AG_DEFER");
+    defer_env = e && *e ? atoi(e) : 0;
+  }
+  ag_defer_ = overlap_mode_ == 3 && defer_env != 0 && !cfg_.appx_recovery;
+  if (!ag_defer_) EDL_TRY(join_side());
   step_count_ = count;
   if (overlap_mode_ == 1) {  // same epochs on every process
     layer_epoch0_ = coll_epoch_ + 1;
@@ -1732,16 +1805,18 @@ int Job::step(EdlStepReport* out) {
     EDL_TRY(mlp_ ? run_worker_mlp(w, slot, last_on[w->rep] == w) : run_worker_linear(w, slot));
   }
   EDL_TRY(reduce_and_update(count, t_, slot));
+  // with the deferred all-gather the mini-batch ends on the side streams (push collective)
+  cudaStream_t tail = ag_defer_ ? prim->side : prim->stream;
   EDL_CUDA_TRY(cudaMemcpyAsync(&prim->host_loss[slot], prim->loss_sum, sizeof(double),
-                               cudaMemcpyDeviceToHost, prim->stream));
+                               cudaMemcpyDeviceToHost, tail));
   // the primary's end event covers every local replica's share of the mini-batch
   for (const auto& p : peers_) {
     if (!p.local || p.rep == prim) continue;
     DeviceGuard dg(p.rep->device);
-    EDL_CUDA_TRY(cudaEventRecord(p.rep->ev_done[slot], p.rep->stream));
-    EDL_CUDA_TRY(cudaStreamWaitEvent(prim->stream, p.rep->ev_done[slot], 0));
+    EDL_CUDA_TRY(cudaEventRecord(p.rep->ev_done[slot], ag_defer_ ? p.rep->side : p.rep->stream));
+    EDL_CUDA_TRY(cudaStreamWaitEvent(tail, p.rep->ev_done[slot], 0));
   }
-  EDL_CUDA_TRY(cudaEventRecord(prim->ev_end[slot], prim->stream));
+  EDL_CUDA_TRY(cudaEventRecord(prim->ev_end[slot], tail));
   slot_end_[slot] = prim->ev_end[slot];
 
   Pending p{prim, t_, slot, count, version_, static_cast<int>(ring_.size()), switched ? 1 : 0,
@@ -1781,9 +1856,12 @@ int Job::sync(EdlStepReport* out) {
     if (out) *out = last_;
     return EDL_OK;
   }
+  // host wait for both streams; a deferred push stays "pending" (its flags and ev_push are
+  // complete, so the next mini-batch's waits pass at once)
   for (auto& [dev, r] : reps_) {
     DeviceGuard g(dev);
     EDL_CUDA_TRY(cudaStreamSynchronize(r->stream));
+    if (r->side) EDL_CUDA_TRY(cudaStreamSynchronize(r->side));
   }
   collect_completed();
   if (out) *out = last_;
@@ -1891,6 +1969,7 @@ int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<
 }
 
 int Job::params(const std::string& worker, void* host, size_t bytes) {
+  EDL_TRY(join_side());  // the deferred push collective updates master / W
   auto it = workers_.find(worker);
   if (it == workers_.end()) return fail(EDL_UNKNOWN_WORKER, "params: unknown worker " + worker);
   if (it->second->remote) return fail(EDL_EINVAL, "params: worker hosted by another process");
@@ -1913,6 +1992,7 @@ int Job::params(const std::string& worker, void* host, size_t bytes) {
 // Checkpoint restore (stop-resume baseline, recovery): every replica takes the parameters;
 // MLP replicas re-derive their bf16 working weights from the fp32 master.
 int Job::set_params(const void* host, size_t bytes) {
+  EDL_TRY(join_side());  // the deferred push collective updates master / W
   const size_t need = mlp_ ? sizeof(float) * P_ : sizeof(double) * P_;
   if (bytes < need) return fail(EDL_EINVAL, "set_params: buffer too small");
   for (auto& [dev, r] : reps_) {
@@ -2108,6 +2188,7 @@ int Job::import_handles(const uint8_t* blob, size_t len) {
 }
 
 int Job::gather_master() {
+  EDL_TRY(join_side());  // the deferred push collective updates master / W
   if (!mlp_ || peers_.size() < 2 || dry_) return EDL_OK;
   Replica* r = primary();
   bool all_local = true;

@@ -85,6 +85,13 @@ struct Replica {
   std::vector<cudaEvent_t> ev_grad;
   cudaEvent_t ev_side = nullptr;
   int layer_colls = 0;  // layer collectives launched this step
+  // deferred all-gather (exchange mode 3 with EDL_AG_DEFER != 0): the push collective of
+  // mini-batch t runs on `side` after ev_bwd (end of t's backward) while t+1's forward runs
+  // on `stream`; t+1's forward GEMM of layer l waits for the layer's flags (ag_wait_epoch),
+  // its first routed weight-gradient GEMM waits for ev_push (the peers' recv reads are done)
+  cudaEvent_t ev_bwd = nullptr, ev_push = nullptr;
+  uint32_t ag_wait_epoch = 0;  // 0: the weights are final (no deferred push in flight)
+  bool side_pending = false;   // a deferred push on `side` not yet joined into `stream`
   double* host_loss = nullptr;  // pinned [kSlots]
 };
 
@@ -233,6 +240,7 @@ class Job {
   bool overlap_ = false;
   int overlap_mode_ = 0;  // 1: side-stream collective kernels, 2: copy-engine transfers,
                           // 3: reduce-scatter fused into the wgrad GEMM epilogues
+  bool ag_defer_ = false;  // mode 3 + the push collective overlapped with the next forward
   bool rs_eligible() const;
   bool push_eligible() const;
   uint32_t ce_epoch_ = 0;
@@ -299,6 +307,11 @@ class Job {
   int enable_peers(Replica* a, const std::vector<Replica*>& also = {});
   void rebuild_peers();
   int consolidate_master();  // async all-gather of the sharded fp32 master (local replicas)
+ public:
+  // orders every local replica's stream after its deferred push collective (no host sync):
+  // before anything that reads the master / weights / loss outside the step pipeline
+  int join_side();
+ private:
   int broadcast_model(Replica* src, Replica* dst);
   cudaEvent_t slot_end_[kSlots] = {};
   std::map<int, std::unique_ptr<Replica>> reps_;

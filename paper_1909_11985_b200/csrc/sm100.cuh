@@ -91,6 +91,21 @@ __device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int c0, int c1
 // wait: block until the grids this one depends on (stream predecessors launched with
 // programmatic serialization) have completed and their writes are visible.  launch: allow
 // the dependents to start launching (their CTAs run their prologue, then wait).
+// Spin until flags[r] >= epoch (wrapping compare) for r < n, system-scope acquire, then order
+// the async proxy (TMA loads) after it: the flags release peer / local generic-proxy stores.
+__device__ __forceinline__ void wait_flags_acquire(const uint32_t* flags, int n, uint32_t epoch) {
+  for (int r = 0; r < n; ++r) {
+    const uint64_t t0 = clock64();
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + r) : "memory");
+      if (static_cast<int32_t>(v - epoch) >= 0) break;
+      __nanosleep(64);
+      if (clock64() - t0 > (1ull << 36)) __trap();  // a peer died: fail, don't hang
+    }
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

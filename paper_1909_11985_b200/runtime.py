@@ -210,6 +210,11 @@ class Job:
         routed from the wgrad GEMM epilogues (include/edl_b200.h edl_job_exchange_mode)."""
         return int(self._L.edl_job_exchange_mode(self._h))
 
+    def join(self) -> None:
+        """Order the job stream after every launched mini-batch's device work (including a
+        deferred push collective on the side stream); no host sync (edl_job_join)."""
+        _lib.check(self._L.edl_job_join(self._h))
+
     PHASES = ("gather", "forward", "loss", "backward", "update", "wgrad")
 
     def counters(self) -> dict:

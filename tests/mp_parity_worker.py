@@ -117,6 +117,26 @@ def main():
         failures.append(f"rank {rank}: mlp-rs params max err {err.max()} mean {err.mean()}")
     job.close()
 
+    # 4. the same job pipelined: no host sync between mini-batches, so with the deferred
+    #    all-gather (default) every push collective overlaps the next mini-batch's forward,
+    #    whose GEMMs wait on the per-layer weight flags.  Same parameters as section 3.
+    job = rt.Job(cfg, ring, devices)
+    connect(job, world, rank)
+    for _ in range(steps):
+        job.step()
+    last = job.sync()
+    job.gather_master()
+    wp = job.params(ring[rank])
+    if abs(last.loss - got[-1].loss) > 1e-6 * abs(got[-1].loss):
+        failures.append(f"rank {rank}: pipelined last loss {last.loss} vs {got[-1].loss}")
+    err = np.abs(wp - ref)
+    if err.max() > 2 ** -8 * np.abs(ref).max() or err.mean() > 1e-4 * np.abs(ref).max():
+        failures.append(f"rank {rank}: pipelined params max err {err.max()} mean {err.mean()}")
+    if not np.array_equal(wp, wm):
+        failures.append(f"rank {rank}: pipelined params differ from the synced run "
+                        f"(max {np.abs(wp - wm).max()})")
+    job.close()
+
     allf = [None] * world
     dist.all_gather_object(allf, failures)
     dist.barrier()

@@ -14,10 +14,11 @@ pytestmark = pytest.mark.gpu
 # overlap: "" = default (3 when the layers split into per-GPU row blocks, else 0), 0 = one
 # fused collective kernel after the backward, 1 = per-layer collective kernels on a side
 # stream, 2 = per-layer copy-engine transfers + shard updates, 3 = reduce-scatter in the
-# wgrad GEMM epilogues + per-layer shard update / all-gather
+# wgrad GEMM epilogues + per-layer shard update / all-gather.  "3/defer" runs mode 3's push
+# collective on a side stream overlapping the next forward (EDL_AG_DEFER=1, per-layer flags).
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("overlap", ["", "0", "1", "2", "3"])
+@pytest.mark.parametrize("overlap", ["", "0", "1", "2", "3", "3/defer"])
 def test_two_or_more_gpus_match_oracle(overlap):
     n = min(torch.cuda.device_count(), 4)
     here = os.path.dirname(os.path.abspath(__file__))
@@ -26,6 +27,10 @@ def test_two_or_more_gpus_match_oracle(overlap):
            os.path.join(here, "mp_parity_worker.py")]
     env = dict(os.environ)
     env.pop("EDL_OVERLAP", None)
+    env.pop("EDL_AG_DEFER", None)
+    if overlap.endswith("/defer"):
+        env["EDL_AG_DEFER"] = "1"
+        overlap = overlap.split("/")[0]
     if overlap:
         env["EDL_OVERLAP"] = overlap
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
