@@ -61,6 +61,7 @@ struct GemmPlan {
   PeerMaps pm;                 // reduce-scatter destinations (routed plans)
   int M = 0, N = 0, K = 0, a_mn = 0, b_mn = 0, bn = 0, cg = 1;
   int mc = 1;  // CTA-pair kernel: pairs per cluster sharing A by TMA multicast (1 or 2)
+  int sk = 1;  // CTA-pair kernel: 2 = split-K over two pairs, 256-wide tiles (gemm_sm100.cu)
   EpiParams ep{};
 };
 int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B, int ldb,

@@ -365,7 +365,14 @@ struct Cfg2 {
   static constexpr uint32_t kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 512;
 };
 
-template <int BN, bool A_MN, bool B_MN, bool kSgd, int kMc>
+// kSk = 2 (split-K): a cluster of 4 CTAs = 2 pairs computes ONE 256 x BN tile, pair p over
+// k-blocks [p * nkb/2, ...) of K.  256 x 256 pair tiles halve the shared-memory bytes per MAC
+// of 256 x 128 (the M = 512 GEMMs of the step are shared-memory-bound at 256 x 128: measured
+// 55% of the MMA rate vs 95% at 256 x 256), and the K split keeps 128 SMs busy.  After the
+// mainloop each CTA owns one column half of the tile: it sends the other half of its fp32
+// partial to the matching CTA of the other pair through DSMEM (into that CTA's idle stage
+// buffers), receives that CTA's partial of its own half, adds, and runs the epilogue.
+template <int BN, bool A_MN, bool B_MN, bool kSgd, int kMc, int kSk = 1>
 __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                          const __grid_constant__ CUtensorMap tmap_b,
@@ -373,6 +380,10 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
                          const __grid_constant__ CUtensorMap tmap_m, int M, int N, int K,
                          EpiParams ep, const __grid_constant__ PeerMaps pm) {
   using C = Cfg2<BN, kSgd>;
+  static_assert(kSk == 1 || (kSk == 2 && kMc == 1 && !kSgd && BN == 256),
+                "split-K: 256-wide plain tiles, no multicast");
+  // kMc = 4 (8-CTA clusters, K-major A) compiles and was measured: slower than 2 on B200
+  static_assert(kMc == 1 || kMc == 2 || (kMc == 4 && !A_MN), "A multicast: 2 pairs, or 4 (K-major A)");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -391,18 +402,22 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
   const uint32_t pidx = rank >> 1;  // pair inside the cluster (kMc = 2)
   const bool leader = pr == 0;
   const uint16_t pair_mask = static_cast<uint16_t>(0x3u << (2 * pidx));
-  const int unit = blockIdx.x / (2 * kMc), n_units = gridDim.x / (2 * kMc);
+  const int unit = blockIdx.x / (2 * kMc * kSk), n_units = gridDim.x / (2 * kMc * kSk);
   const int m_tiles = (M + 255) / 256;
   const int n_tiles = (N + BN - 1) / BN;  // the host guarantees n_tiles % kMc == 0
   const int num_work = m_tiles * (n_tiles / kMc);
   const int num_kb = (K + BK - 1) / BK;
   auto tile_m = [&](int w) { return w % m_tiles; };
-  auto tile_n = [&](int w) { return (w / m_tiles) * kMc + static_cast<int>(pidx); };
+  auto tile_n = [&](int w) {
+    return (w / m_tiles) * kMc + (kMc >= 2 ? static_cast<int>(pidx) : 0);
+  };
+  // split-K: this pair's k-blocks (the host guarantees one tile per cluster)
+  const int kb_begin = kSk == 2 ? static_cast<int>(pidx) * (num_kb / 2) : 0;
 #ifdef EDL_GEMM_TRACE
-  const int kb_end = (ep.dbg & 1) ? 0 : num_kb;
+  const int kb_end = (ep.dbg & 1) ? kb_begin : (kSk == 2 && pidx == 0 ? num_kb / 2 : num_kb);
   const bool skip_epi = (ep.dbg & 2) != 0;
 #else
-  const int kb_end = num_kb;
+  const int kb_end = kSk == 2 && pidx == 0 ? num_kb / 2 : num_kb;
   constexpr bool skip_epi = false;
 #endif
 
@@ -420,7 +435,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 2 * C::kEpiWarps);  // lane 0 of every epilogue warp, both CTAs
     }
-    for (int a = 0; a < 16; ++a) mbar_init(&sgd_bar[a], 1);
+    for (int a = 0; a < 16; ++a) mbar_init(&sgd_bar[a], kSk == 2 && a < 2 ? 4 : 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_2sm<C::kTmemCols>(tmem_slot);
@@ -442,7 +457,8 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
     // both CTAs' bytes (full boxes, OOB included) are counted on the leader's barrier
     const uint32_t tx = 2 * (C::kABytes + (B_MN ? C::kBBytesMN : C::kBBytesK));
     TRACE_T0(t_prod);
-    const uint16_t a_mask = static_cast<uint16_t>((1u << pr) | (1u << (pr + 2)));
+    uint16_t a_mask = 0;  // the CTA with my rank-in-pair in every pair of the cluster
+    for (int p2 = 0; p2 < kMc; ++p2) a_mask |= static_cast<uint16_t>(1u << (pr + 2 * p2));
     if (ep.wait_flags) {  // weights still arriving from the deferred all-gather
       if (lane == 0) wait_flags_acquire(ep.wait_flags, ep.wait_n, ep.wait_epoch);
       __syncwarp();
@@ -450,7 +466,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
     for (int w = unit; w < num_work; w += n_units) {
       const int m0 = tile_m(w) * 256 + static_cast<int>(pr) * 128;
       const int n0 = tile_n(w) * BN + static_cast<int>(pr) * C::kHalfN;
-      for (int kb = 0; kb < kb_end; ++kb) {
+      for (int kb = kb_begin; kb < kb_end; ++kb) {
         TRACE_T0(t_w);
         mbar_wait(&empty_bar[stage], phase ^ 1);
         TRACE_ADD(3, t_w);
@@ -458,13 +474,14 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
           uint8_t* sa = smem + stage * C::kStageBytes;
           uint8_t* sb = sa + C::kABytes;
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], tx);
-          if (kMc == 2) {  // my half of the A slice, to me and my twin in the other pair
+          if (kMc >= 2) {  // my 1/kMc of the A slice, to me and my twins in the other pairs
+            constexpr int kRows = 128 / kMc;
             if (A_MN)
               tma_load_2d_2sm_mc(sa + pidx * kMnBlockBytes, &tmap_a, &full_bar[stage],
                                  m0 + 64 * static_cast<int>(pidx), kb * BK, a_mask);
             else
-              tma_load_2d_2sm_mc(sa + pidx * (64 * 128), &tmap_a, &full_bar[stage], kb * BK,
-                                 m0 + 64 * static_cast<int>(pidx), a_mask);
+              tma_load_2d_2sm_mc(sa + pidx * (kRows * 128), &tmap_a, &full_bar[stage], kb * BK,
+                                 m0 + kRows * static_cast<int>(pidx), a_mask);
           } else if (A_MN) {
             tma_load_2d_2sm(sa, &tmap_a, &full_bar[stage], m0, kb * BK);
             tma_load_2d_2sm(sa + kMnBlockBytes, &tmap_a, &full_bar[stage], m0 + 64, kb * BK);
@@ -482,7 +499,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
           // pull k-block kb + pf_kb into L2 now so its TMA load above (kStages later) does
           // not pay the HBM latency the stage ring is too shallow to cover
           const int kp = kb + ep.pf_kb;
-          if (ep.pf_kb > 0 && kp < num_kb) {
+          if (ep.pf_kb > 0 && kp < kb_end) {
             if (A_MN) {
               tma_prefetch_2d(&tmap_a, m0, kp * BK);
               tma_prefetch_2d(&tmap_a, m0 + 64, kp * BK);
@@ -531,7 +548,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
         TRACE_ADD(1, t_te);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * C::kAccCols;
-        for (int kb = 0; kb < kb_end; ++kb) {
+        for (int kb = kb_begin; kb < kb_end; ++kb) {
           TRACE_T0(t_f);
           mbar_wait(&full_bar[stage], phase);
           TRACE_ADD(0, t_f);
@@ -542,9 +559,10 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
   #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
               umma_bf16_2sm(d_tmem, a0 + so + ((k * kStepA) >> 4), b0 + so + ((k * kStepB) >> 4),
-                            idesc, (kb | k) != 0 ? 1u : 0u);
+                            idesc, (kb != kb_begin || k != 0) ? 1u : 0u);
             // kMc = 2: the stage also holds A multicast by the other pair -> free it there too
-            umma_commit_2sm(&empty_bar[stage], kMc == 2 ? 0xF : pair_mask);
+            umma_commit_2sm(&empty_bar[stage],
+                            kMc >= 2 ? static_cast<uint16_t>((1u << (2 * kMc)) - 1) : pair_mask);
           }
           __syncwarp();
           if (++stage == C::kStages) {
@@ -729,8 +747,44 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
       const uint32_t t_row =
           tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::kAccCols;
       const int cw = ep.out_f32 ? 32 : 64;  // columns per 128-byte staging row
+      int c_lo = 0, c_hi = BN;
+      const float* xrow = nullptr;
+      if constexpr (kSk == 2) {
+        // split-K reduction through DSMEM (see the kernel comment).  xbuf = this CTA's stage
+        // buffers, idle once this pair's MMAs have completed: [128 rows][kXs] fp32
+        constexpr int kHalf = BN / 2;
+        constexpr int kXs = kHalf + 4;  // padded row: 16-byte accesses of a warp hit all banks
+        static_assert(128 * kXs * 4 <= C::kStages * C::kStageBytes, "split-K exchange buffer");
+        float* xbuf = reinterpret_cast<float*>(smem);
+        uint64_t* xready = sgd_bar;     // arrived by the partner: its stage buffers are free
+        uint64_t* xfull = sgd_bar + 1;  // arrived by the partner: my half of its partial is in
+        const uint32_t partner = rank ^ 2u;
+        if (lane == 0) mbar_arrive_remote(xready, partner);
+        mbar_wait(xready, 0);
+        if (warp == 2) TL(8);
+        const int c_send = (1 - static_cast<int>(pidx)) * kHalf;
+        const uint32_t xdst = mapa_u32(xbuf, partner) + static_cast<uint32_t>((q * 32 + lane) * kXs * 4);
 #pragma unroll 1
-      for (int c = 0; c < BN; c += cw) {
+        for (int c = 0; c < kHalf; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(t_row + c_send + c, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            st_cluster_v4(xdst + static_cast<uint32_t>((c + j) * 4), r[j], r[j + 1], r[j + 2],
+                          r[j + 3]);
+        }
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote_release(xfull, partner);
+        mbar_wait_cluster(xfull, 0);
+        if (warp == 2) TL(15);
+        c_lo = static_cast<int>(pidx) * kHalf;
+        c_hi = c_lo + kHalf;
+        xrow = xbuf + (q * 32 + lane) * kXs - c_lo;
+      }
+#pragma unroll 1
+      for (int c = c_lo; c < c_hi; c += cw) {
         float v[64];
         {
           uint32_t r[32], r2[32];
@@ -742,6 +796,18 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
           if (!ep.out_f32) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[32 + j] = __uint_as_float(r2[j]);
+          }
+        }
+        if constexpr (kSk == 2) {  // + the other pair's partial (fp32 add: commutative)
+          const float4* xp = reinterpret_cast<const float4*>(xrow + c);
+#pragma unroll
+          for (int j4 = 0; j4 < 16; ++j4) {
+            if (j4 >= 8 && ep.out_f32) break;
+            const float4 x = xp[j4];
+            v[4 * j4] += x.x;
+            v[4 * j4 + 1] += x.y;
+            v[4 * j4 + 2] += x.z;
+            v[4 * j4 + 3] += x.w;
           }
         }
         if (ep.relu) {
@@ -924,10 +990,11 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
   return EDL_OK;
 }
 
-template <int BN, bool A_MN, bool B_MN, bool kSgd = false, int kMc = 1>
+template <int BN, bool A_MN, bool B_MN, bool kSgd = false, int kMc = 1, int kSk = 1>
 int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream, float scale = 0.f) {
   using Cf = Cfg2<BN, kSgd>;
-  auto kern = gemm_bf16_2sm_kernel<BN, A_MN, B_MN, kSgd, kMc>;
+  auto kern = gemm_bf16_2sm_kernel<BN, A_MN, B_MN, kSgd, kMc, kSk>;
+  constexpr int kCl = 2 * kMc * kSk;  // CTAs per cluster
   static uint64_t attr_set = 0;  // per device: the attribute lives in each context
   static int max_units[64];      // co-resident clusters per device (persistent grid size)
   int dev = 0;
@@ -938,7 +1005,7 @@ int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream, float scale = 0.f) {
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2 * kMc;
+  attr[0].val.clusterDim.x = kCl;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -950,19 +1017,21 @@ int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream, float scale = 0.f) {
                                       Cf::kSmemBytes));
     // a persistent grid must not exceed what the GPCs can hold at once (4-CTA clusters
     // need two TPCs of one GPC)
-    cfg.gridDim = dim3(num_sms());
+    cfg.gridDim = dim3((num_sms() / kCl) * kCl);  // a whole number of clusters
     int n = 0;
     EDL_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
     max_units[dev] = n > 0 ? n : 1;
     attr_set |= 1ull << dev;
   }
   const int work = ((p.M + 255) / 256) * ((p.N + BN - 1) / BN / kMc);
-  int units = num_sms() / (2 * kMc);
+  int units = num_sms() / kCl;
   if (units > max_units[dev]) units = max_units[dev];
+  // split-K clusters run exactly one tile (the DSMEM exchange reuses the stage buffers)
+  if (kSk == 2 && work > units) return fail(EDL_EINVAL, "gemm: split-K needs one tile per cluster");
   EpiParams ep = p.ep;
   ep.scale = scale;
   cfg.numAttrs = gemm_pdl_enabled() ? 2 : 1;
-  cfg.gridDim = dim3(2 * kMc * (work < units ? work : units));
+  cfg.gridDim = dim3(kCl * (work < units ? work : units));
   EDL_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p.ta, p.tb, p.tc, p.tm, p.M, p.N, p.K, ep, p.pm));
   return EDL_OK;
 }
@@ -1009,15 +1078,29 @@ int gemm_pick_bn(int M, int N, bool b_mn) {
   return best;
 }
 
+// Split-K 256-wide tiles for few-tile GEMMs (EDL_GEMM_SPLITK=1).  Off by default: measured
+// on B200 the M = 512 GEMMs keep the same mainloop time at 256 x 256 split over K as at
+// 256 x 128 (both read ~8.3 TB/s of operands from L2, which is the bound, not shared memory)
+// and the DSMEM exchange of the fp32 partials adds ~4 us.
+static bool gemm_splitk_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("EDL_GEMM_SPLITK");
+    on = e ? atoi(e) != 0 : 0;
+  }
+  return on != 0;
+}
+
 // A-operand multicast across two CTA pairs (EDL_GEMM_MC=0 disables, for comparisons).
 static bool gemm_multicast_enabled() {
   static int on = -1;
   if (on < 0) {
     const char* e = getenv("EDL_GEMM_MC");
-    on = e ? atoi(e) != 0 : 1;
+    on = e ? atoi(e) : 2;
   }
   return on != 0;
 }
+
 
 // L2 prefetch distances; EDL_GEMM_PF_KB / EDL_GEMM_PF_TILES override (tuning runs).
 static void gemm_prefetch_defaults(EpiParams* ep) {
@@ -1039,15 +1122,29 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B,
                    const void* mask, int ldm, int bn) {
   if (M <= 0 || N <= 0 || K <= 0) return fail(EDL_EINVAL, "gemm: empty shape");
   if ((lda * 2) % 16 || (ldb * 2) % 16) return fail(EDL_EINVAL, "gemm: 16-byte row alignment");
-  // bn: 0 = auto, 1..256 = 1-SM kernel with that N tile, 1000 + x = CTA-pair kernel, N tile x
-  int cg = 1;
-  if (bn >= 1000) {
+  // bn: 0 = auto, 1..256 = 1-SM kernel with that N tile, 1000 + x = CTA-pair kernel, N tile x,
+  // 2256 = CTA-pair kernel with 256-wide tiles split over K between two pairs
+  int cg = 1, sk = 1;
+  if (bn >= 2000) {
+    cg = 2;
+    sk = 2;
+    bn -= 2000;
+    if (bn != 256) return fail(EDL_EINVAL, "gemm: split-K uses 256-wide tiles");
+  } else if (bn >= 1000) {
     cg = 2;
     bn -= 1000;
   } else if (bn <= 0) {
     if (M >= 256 && (ldc * (out_f32 ? 4 : 2)) % 16 == 0) {
       cg = 2;
       bn = gemm_pick_bn_2sm(M, N);
+      // few output tiles (the M = 512 GEMMs of the step): 256-wide tiles split over K keep
+      // 128+ SMs busy at half the shared-memory bytes per MAC of 256 x 128 tiles
+      const int t256 = ((M + 255) / 256) * ((N + 255) / 256);
+      if (gemm_splitk_enabled() && t256 <= num_sms() / 4 && 4 * t256 >= (num_sms() * 3) / 4 &&
+          (K + BK - 1) / BK >= 8) {
+        bn = 256;
+        sk = 2;
+      }
     } else {
       bn = gemm_pick_bn(M, N, b_mn != 0);
     }
@@ -1058,12 +1155,15 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B,
     // pairs of N tiles share A through multicast when the N tiles pair up and the grid is a
     // single wave (persistent multi-wave grids lose more to 4-CTA cluster placement)
     const int n_tiles = (N + bn - 1) / bn, m_tiles = (M + 255) / 256;
-    const int mc = (n_tiles % 2 == 0 && m_tiles * n_tiles <= num_sms() / 2 &&
-                    gemm_multicast_enabled())
-                       ? 2
-                       : 1;
+    if (sk == 2 && m_tiles * n_tiles > num_sms() / 4)
+      return fail(EDL_EINVAL, "gemm: split-K needs one tile per 4-CTA cluster");
+    int mc = (sk == 1 && n_tiles % 2 == 0 && m_tiles * n_tiles <= num_sms() / 2 &&
+              gemm_multicast_enabled())
+                 ? 2
+                 : 1;
+    p->sk = sk;
     int rc = a_mn ? make_tmap(&p->ta, A, K, M, lda, 64)
-                  : make_tmap(&p->ta, A, M, K, lda, mc == 2 ? 64 : 128);
+                  : make_tmap(&p->ta, A, M, K, lda, static_cast<uint32_t>(128 / mc));
     if (rc) return fail(rc, "gemm: tensor map A");
     p->mc = mc;
     rc = b_mn ? make_tmap(&p->tb, B, K, N, ldb, 64) : make_tmap(&p->tb, B, N, K, ldb, bn / 2);
@@ -1140,7 +1240,13 @@ int gemm_plan_init_sgd(GemmPlan* p, const void* A, int lda, int a_mn, const void
   int rc = gemm_plan_init(p, A, lda, a_mn, B, ldb, b_mn, W, ldw, M, N, K, 0, 0, nullptr, 0,
                           1000 + bn);
   if (rc) return rc;
-  p->mc = 1;
+  // EDL_SGD_MC=1: 4-CTA clusters multicast the shared A (dY) slice across two pairs
+  static int sgd_mc = -1;
+  if (sgd_mc < 0) {
+    const char* e = getenv("EDL_SGD_MC");
+    sgd_mc = e ? atoi(e) : 0;
+  }
+  p->mc = (sgd_mc && ((N + bn - 1) / bn) % 2 == 0) ? 2 : 1;
   rc = make_tmap_t(&p->tm, master, M, N, ldw, 32, 32, true);
   if (rc) return fail(rc, "fused SGD: tensor map master");
   p->ep.sgd = 1;
@@ -1150,10 +1256,18 @@ int gemm_plan_init_sgd(GemmPlan* p, const void* A, int lda, int a_mn, const void
 int gemm_plan_run(const GemmPlan& p, cudaStream_t stream, float sgd_scale) {
   const int a_mn = p.a_mn, b_mn = p.b_mn;
   if (p.ep.sgd) {
-    if (p.cg != 2 || (p.bn != 128 && p.bn != 256) || !a_mn || !b_mn || p.mc != 1)
+    if (p.cg != 2 || (p.bn != 128 && p.bn != 256) || !a_mn || !b_mn)
       return fail(EDL_EINVAL, "gemm: fused SGD plans are CTA-pair, N tile 128/256, MN-major A/B");
+    if (p.mc == 2 && p.bn == 128) return launch_gemm_2sm<128, true, true, true, 2>(p, stream, sgd_scale);
     if (p.bn == 256) return launch_gemm_2sm<256, true, true, true, 1>(p, stream, sgd_scale);
     return launch_gemm_2sm<128, true, true, true, 1>(p, stream, sgd_scale);
+  }
+  if (p.cg == 2 && p.sk == 2) {
+    if (p.bn != 256 || p.mc != 1) return fail(EDL_EINVAL, "gemm: split-K plan");
+    if (!a_mn && !b_mn) return launch_gemm_2sm<256, false, false, false, 1, 2>(p, stream);
+    if (!a_mn && b_mn) return launch_gemm_2sm<256, false, true, false, 1, 2>(p, stream);
+    if (a_mn && !b_mn) return launch_gemm_2sm<256, true, false, false, 1, 2>(p, stream);
+    return launch_gemm_2sm<256, true, true, false, 1, 2>(p, stream);
   }
   if (p.cg == 2) {
 #define EDL_GEMM2_MC(BNV, AM, BM_, MC) \

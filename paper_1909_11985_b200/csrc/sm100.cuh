@@ -87,10 +87,6 @@ __device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int c0, int c1
                : "memory");
 }
 
-// ---------------------------------------------------------------- programmatic dependent launch
-// wait: block until the grids this one depends on (stream predecessors launched with
-// programmatic serialization) have completed and their writes are visible.  launch: allow
-// the dependents to start launching (their CTAs run their prologue, then wait).
 // Spin until flags[r] >= epoch (wrapping compare) for r < n, system-scope acquire, then order
 // the async proxy (TMA loads) after it: the flags release peer / local generic-proxy stores.
 __device__ __forceinline__ void wait_flags_acquire(const uint32_t* flags, int n, uint32_t epoch) {
@@ -106,6 +102,11 @@ __device__ __forceinline__ void wait_flags_acquire(const uint32_t* flags, int n,
   }
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// wait: block until the grids this one depends on (stream predecessors launched with
+// programmatic serialization) have completed and their writes are visible.  launch: allow
+// the dependents to start launching (their CTAs run their prologue, then wait).
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -181,6 +182,43 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank)
   // memory; .release.cluster lowered to MEMBAR.GPU + ERRBAR, which waited for the caller's
   // outstanding bulk stores (~20% of the fused-SGD epilogue's stall samples)
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+// Arrive with cluster-scope release: the caller's generic-proxy stores into the target CTA's
+// shared memory (st.shared::cluster) become visible to a cluster-scope acquire of the phase.
+__device__ __forceinline__ void mbar_arrive_remote_release(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+// Phase wait with cluster-scope acquire (pairs with mbar_arrive_remote_release).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+  const uint32_t addr = smem_u32(bar);
+  const uint64_t t0 = globaltimer_ns();
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(phase)
+        : "memory");
+    if (ok) return;
+    if (globaltimer_ns() - t0 > 5000000000ull) __trap();
+  }
+}
+// Address of this CTA's shared-memory object p in CTA `rank` of the cluster (DSMEM).
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(p)), "r"(rank));
+  return remote;
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                              uint32_t d) {
+  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b),
+               "r"(c), "r"(d)
                : "memory");
 }
 // 2-SM TMA load: bytes land in this CTA's smem, completion is counted on the pair leader's

@@ -1,0 +1,2 @@
+export PYTHONUNBUFFERED=1
+timeout 200 python scratch/timeline.py scratch/var/trace/libedl_b200.so 2>&1 | grep -A8 "chain bn"

@@ -6,7 +6,7 @@ L = _lib.lib()
 L.edl_debug_gemm_timeline.argtypes = [C.c_void_p]
 tl = np.zeros((296, 16), dtype=np.uint64)
 s = lambda: C.c_void_p(torch.cuda.current_stream().cuda_stream)
-names = ["entry", "setup_done", "mma_first_full", "mma_end", "epi_first_tfull", "epi_drained", "prod_end", "exit", "w2_chunk0_tmem", "w2_chunk0_store", "w2_chunk1_store", "w2_before_wait", "w5_drained", "w0_final", "w1_final"]
+names = ["entry", "setup_done", "mma_first_full", "mma_end", "epi_first_tfull", "epi_drained", "prod_end", "exit", "xready_seen", "w2_chunk0_store", "w2_chunk1_store", "w2_before_wait", "w5_drained", "w0_final", "w1_final", "xfull_seen"]
 def show(tag, ctas):
     tl[:] = 0
     L.edl_debug_gemm_timeline(tl.ctypes.data)
@@ -30,17 +30,17 @@ def chain(fn, n=8):
     return e0.elapsed_time(e1) * 1e3
 Ws = [torch.randn(4096, 4096).to(torch.bfloat16).cuda() for _ in range(8)]
 acts = [torch.randn(512, 4096).to(torch.bfloat16).cuda() for _ in range(9)]
-for bn in (1128,):
+for bn in (1128, 1256, 2256):
     def fwd():
         for i in range(8):
             L.edl_gemm_bf16(acts[i].data_ptr(), 4096, 0, Ws[i].data_ptr(), 4096, 0, acts[i + 1].data_ptr(), 4096, 512, 4096, 4096, 1, 0, None, 0, bn, s())
     us = chain(fwd)
-    show(f"fwd chain bn={bn}: {us/8:.1f} us per GEMM (graph)", 128 if bn == 1128 else 64)
+    show(f"fwd chain bn={bn}: {us/8:.1f} us per GEMM (graph)", 128 if bn in (1128, 2256) else 64)
     def dgrad():
         for i in range(8):
             L.edl_gemm_bf16(acts[i].data_ptr(), 4096, 0, Ws[i].data_ptr(), 4096, 1, acts[i + 1].data_ptr(), 4096, 512, 4096, 4096, 0, 0, None, 0, bn, s())
     us = chain(dgrad)
-    show(f"dgrad chain bn={bn}: {us/8:.1f} us per GEMM (graph)", 128 if bn == 1128 else 64)
+    show(f"dgrad chain bn={bn}: {us/8:.1f} us per GEMM (graph)", 128 if bn in (1128, 2256) else 64)
 master = [torch.randn(4096, 4096, device='cuda') for _ in range(2)]
 def wg():
     for i in range(8):

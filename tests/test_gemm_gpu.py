@@ -29,14 +29,17 @@ def _ref(A, a_mn, B, b_mn):
 
 
 # bn: 0 = auto (CTA-pair kernel when M >= 256), 1..256 = 1-SM kernel with that N tile,
-# 1000 + x = CTA-pair (cta_group::2) kernel with N tile x
+# 1000 + x = CTA-pair (cta_group::2) kernel with N tile x, 2256 = CTA-pair kernel with 256-wide
+# tiles split over K between two pairs (fp32 partials exchanged through DSMEM)
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("M,N,K,bn", [(128, 128, 64, 128), (256, 256, 512, 0),
                                       (512, 4096, 4096, 0), (512, 4096, 4096, 128),
                                       (384, 448, 320, 112), (4096, 1024, 512, 256),
                                       (256, 256, 128, 1128), (512, 512, 256, 1256),
                                       (384, 320, 200, 1192), (4096, 1024, 512, 1128),
-                                      (512, 4096, 4096, 1256)])
+                                      (512, 4096, 4096, 1256), (512, 4096, 4096, 2256),
+                                      (256, 256, 512, 2256), (384, 768, 1000, 2256),
+                                      (512, 1024, 200, 2256)])
 def test_gemm_layouts(a_mn, b_mn, M, N, K, bn):
     torch.manual_seed(0)
     A = (torch.randn(K, M) if a_mn else torch.randn(M, K)).to(torch.bfloat16).cuda()
@@ -48,7 +51,7 @@ def test_gemm_layouts(a_mn, b_mn, M, N, K, bn):
     assert err <= 1e-3 * scale + 1e-3, (err, scale)
 
 
-@pytest.mark.parametrize("bn", [0, 128, 1128, 1256])
+@pytest.mark.parametrize("bn", [0, 128, 1128, 1256, 2256])
 def test_gemm_relu_mask_bf16(bn):
     torch.manual_seed(1)
     M, N, K = 512, 1024, 768
@@ -84,3 +87,4 @@ def test_wgrad_sgd_fused(M, N, K):
     tol = scale * g.abs().max().item() * 2 ** -7 + 1e-6
     assert (master - ref).abs().max().item() <= tol
     assert torch.equal(W, master.bfloat16())
+
