@@ -1109,7 +1109,7 @@ static void gemm_prefetch_defaults(EpiParams* ep) {
     const char* e = getenv("EDL_GEMM_PF_KB");
     kb = e ? atoi(e) : 8;
     e = getenv("EDL_GEMM_PF_TILES");
-    tiles = e ? atoi(e) : 1;
+    tiles = e ? atoi(e) : 0;  // measured: 38.9 us per fused wgrad+SGD at 0, 40.2 at 1
   }
   ep->pf_kb = kb;
   ep->pf_tiles = tiles;
