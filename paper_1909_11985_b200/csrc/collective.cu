@@ -178,6 +178,29 @@ __device__ __forceinline__ size_t shard_prefix8(const CollArgs& a, int r, int l)
   return t;
 }
 
+// Phase B of one layer with a compile-time source count: every source's 16-byte load of a
+// thread's 8 parameters is in flight before the first is used (the runtime-count loop issued
+// them one at a time).  src[k][i - lo] = ring member k's gradient of parameter group i.
+template <bool kMomentum, int kS>
+__device__ __forceinline__ void push_phase_b(const CollArgs& a, const uint4* const (&src)[kS],
+                                             size_t lo, size_t hi, size_t tid, size_t stride) {
+  for (size_t i = lo + tid; i < hi; i += stride) {
+    uint4 v[kS];
+#pragma unroll
+    for (int k = 0; k < kS; ++k) v[k] = __ldcs(src[k] + (i - lo));
+    float gs[8];
+    bf16x8_to_f32(v[0], gs);
+#pragma unroll
+    for (int k = 1; k < kS; ++k) {
+      float f[8];
+      bf16x8_to_f32(v[k], f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) gs[e] = __fadd_rn(gs[e], f[e]);
+    }
+    apply8<kMomentum>(a, i, gs);
+  }
+}
+
 template <bool kMomentum>
 __global__ void __launch_bounds__(256) push_allreduce_sgd_kernel(CollArgs a) {
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
@@ -221,6 +244,24 @@ __global__ void __launch_bounds__(256) push_allreduce_sgd_kernel(CollArgs a) {
       size_t lo, hi;
       lay_shard(a, l, a.me, &lo, &hi);
       const size_t pre = shard_prefix8(a, a.me, l);
+      auto src_of = [&](int k) -> const uint4* {
+        const int r = a.src_rep[k];
+        return r == a.me ? own + lo : rv + static_cast<size_t>(r < a.me ? r : r - 1) * total + pre;
+      };
+      if (a.n_src == 2 || a.n_src == 4 || a.n_src == 8) {
+        if (a.n_src == 2) {
+          const uint4* s[2] = {src_of(0), src_of(1)};
+          push_phase_b<kMomentum, 2>(a, s, lo, hi, tid, stride);
+        } else if (a.n_src == 4) {
+          const uint4* s[4] = {src_of(0), src_of(1), src_of(2), src_of(3)};
+          push_phase_b<kMomentum, 4>(a, s, lo, hi, tid, stride);
+        } else {
+          const uint4* s[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) s[k] = src_of(k);
+          push_phase_b<kMomentum, 8>(a, s, lo, hi, tid, stride);
+        }
+      } else {
       for (size_t i = lo + tid; i < hi; i += stride) {
         float gs[8];
         for (int k = 0; k < a.n_src; ++k) {
@@ -240,6 +281,7 @@ __global__ void __launch_bounds__(256) push_allreduce_sgd_kernel(CollArgs a) {
           }
         }
         apply8<kMomentum>(a, i, gs);
+      }
       }
       if (a.ag_signal) {
         // every thread's weight stores of layer l (local and peer) before the count
