@@ -1421,9 +1421,16 @@ int Job::run_worker_linear(Worker* w, int slot) {
 }
 
 // Protocol step 3.
-int Job::reduce_and_update(uint64_t count, uint64_t t, int slot) {
+int Job::reduce_and_update(uint64_t count, uint64_t t, int slot, const double** loss_src) {
   const double eta_t = cfg_.eta / (1.0 + cfg_.decay * static_cast<double>(t));  // trainer.hpp:27
   const int n_rep = static_cast<int>(peers_.size());
+  *loss_src = primary()->loss_sum;
+  if (mlp_ && fused_update_ && n_rep == 1 && ring_.size() == 1) {
+    // one ring member on one GPU: the update ran inside the wgrad GEMMs and the ordered loss
+    // sum over one member is its own loss -- nothing to launch (read that loss directly)
+    *loss_src = workers_[ring_[0]]->loss + (t & 1);
+    return EDL_OK;
+  }
   if (n_rep > 1 && !peers_ready())
     return fail(EDL_EINVAL, "job: peer handles missing (call edl_job_import for every peer)");
   if (ring_.size() > static_cast<size_t>(kCollMaxSources))
@@ -1804,10 +1811,11 @@ int Job::step(EdlStepReport* out) {
     if (w->remote) continue;  // computed by its own process
     EDL_TRY(mlp_ ? run_worker_mlp(w, slot, last_on[w->rep] == w) : run_worker_linear(w, slot));
   }
-  EDL_TRY(reduce_and_update(count, t_, slot));
+  const double* loss_src = nullptr;
+  EDL_TRY(reduce_and_update(count, t_, slot, &loss_src));
   // with the deferred all-gather the mini-batch ends on the side streams (push collective)
   cudaStream_t tail = ag_defer_ ? prim->side : prim->stream;
-  EDL_CUDA_TRY(cudaMemcpyAsync(&prim->host_loss[slot], prim->loss_sum, sizeof(double),
+  EDL_CUDA_TRY(cudaMemcpyAsync(&prim->host_loss[slot], loss_src, sizeof(double),
                                cudaMemcpyDeviceToHost, tail));
   // the primary's end event covers every local replica's share of the mini-batch
   for (const auto& p : peers_) {

@@ -223,7 +223,8 @@ class Job {
   std::vector<std::pair<uint64_t, uint64_t>> draw(Worker* w, int64_t need);
   int run_worker_mlp(Worker* w, int slot, bool last);
   int run_worker_linear(Worker* w, int slot);
-  int reduce_and_update(uint64_t count, uint64_t t, int slot);
+  // *loss_src: device double holding the mini-batch's loss sum for the D2H read
+  int reduce_and_update(uint64_t count, uint64_t t, int slot, const double** loss_src);
   int step_dry(EdlStepReport* out);
   void collect_completed();
 
