@@ -329,6 +329,35 @@ def run_b200(args, rank: int, world: int) -> None:
     e2e_value = samples / (ms_e2e / 1e3)
     runs_per_step = 2  # a 512-sample batch spans <= 2 shards of >= 4096 samples
 
+    # ---- NCCL baseline for the exchange (N > 1): a library allreduce of the same bf16
+    # gradient bytes on the same GPUs, timed like the step (device events, max over ranks);
+    # the product path never calls it -- it is the yardstick for the fused NVLink exchange
+    if world > 1 and not args.no_nccl:
+        try:
+            import torch.distributed as dist_
+            g = dist_.new_group(backend="nccl")
+            buf = torch.zeros(P, dtype=torch.bfloat16, device=f"cuda:{local}")
+            for _ in range(3):
+                dist_.all_reduce(buf, group=g)
+            barrier()
+            n_it = 10
+            e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e4.record()
+            for _ in range(n_it):
+                dist_.all_reduce(buf, group=g)
+            e5.record()
+            torch.cuda.synchronize()
+            nms = max_over_ranks(e4.elapsed_time(e5)) / n_it
+            upd["nccl_allreduce_same_bytes"] = {
+                "ms": nms, "bytes": 2 * P,
+                "bus_gbs": 2.0 * (world - 1) / world * 2 * P / (nms / 1e3) / 1e9,
+                "note": "torch.distributed NCCL all_reduce(sum) of the bf16 gradient (2P bytes) "
+                        "on the same GPUs; compare with the exposed exchange per_step_ms"}
+            del buf
+            dist_.destroy_process_group(g)
+        except Exception as e:  # noqa: BLE001 -- a missing NCCL must not fail the bench
+            upd["nccl_allreduce_same_bytes"] = {"unavailable": str(e)[:200]}
+
     # ---- CPU baseline (oracle port), bounded sample on this host, rank 0 at N=1 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and w is WORKLOAD:
@@ -402,6 +431,8 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-nccl", action="store_true",
+                    help="skip the NCCL allreduce yardstick at N > 1")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="mlp4096x8",
                     help="mlp4096x8 = BASELINE configs[1] (the headline); wide11264x8 = "
                          "configs[4], the ~1B-param allreduce-bound MLP")

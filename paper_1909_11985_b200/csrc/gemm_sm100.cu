@@ -336,12 +336,19 @@ struct Cfg2 {
 #endif
   static constexpr int kEpiWarps = kSgd ? EDL_SGD_EPI_WARPS : 4;
   static constexpr int kThreads2 = 64 + 32 * kEpiWarps;
-  // epilogue staging per warp: plain 2 x 4 KB; fused SGD kSgdBufs x (8 KB master + 4 KB W)
-  static constexpr uint32_t kSgdBufBytes = 3 * kEpiChunkBytes;
+  // epilogue staging per warp: plain 2 x 4 KB; fused SGD kSgdBufs x (8 KB master + 4 KB W).
+  // EDL_SGD_WDIRECT: the bf16 weights go from registers straight to global memory (each lane
+  // its row's 128 contiguous bytes), so a buffer is the 8 KB master chunk only and two of them
+  // per warp fit: the next tile's master load is issued a whole tile ahead
+#ifndef EDL_SGD_WDIRECT
+#define EDL_SGD_WDIRECT 0
+#endif
+  static constexpr bool kWDirect = kSgd && EDL_SGD_WDIRECT;
+  static constexpr uint32_t kSgdBufBytes = (kWDirect ? 2 : 3) * kEpiChunkBytes;
 #ifdef EDL_SGD_BUFS
   static constexpr int kSgdBufs = EDL_SGD_BUFS;
 #else
-  static constexpr int kSgdBufs = kEpiWarps == 8 ? 1 : 2;
+  static constexpr int kSgdBufs = kEpiWarps == 8 && !kWDirect ? 1 : 2;
 #endif
   // master prefetch distance in chunks (1 .. kSgdBufs - 1)
 #ifdef EDL_SGD_PFD
@@ -691,6 +698,21 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
         }
         if (warp == 2) TRACE_ADD(11, t_cs);
         TRACE_T0(t_w8);
+        if constexpr (C::kWDirect) {
+          int r0, c0;
+          coords(j, &r0, &c0);
+          uint4* wp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.C) +
+                                               static_cast<size_t>(r0 + lane) * ep.ldc + c0);
+#pragma unroll
+          for (int j8 = 0; j8 < 8; ++j8) {
+            uint4 o;
+            o.x = pack_bf16(g[8 * j8 + 0], g[8 * j8 + 1]);
+            o.y = pack_bf16(g[8 * j8 + 2], g[8 * j8 + 3]);
+            o.z = pack_bf16(g[8 * j8 + 4], g[8 * j8 + 5]);
+            o.w = pack_bf16(g[8 * j8 + 6], g[8 * j8 + 7]);
+            wp[j8] = o;
+          }
+        } else {
 #pragma unroll
         for (int j8 = 0; j8 < 8; ++j8) {
           uint4 o;
@@ -699,6 +721,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
           o.z = pack_bf16(g[8 * j8 + 4], g[8 * j8 + 5]);
           o.w = pack_bf16(g[8 * j8 + 6], g[8 * j8 + 7]);
           *reinterpret_cast<uint4*>(wrow + ((j8 ^ (lane & 7)) << 4)) = o;
+        }
         }
         if (warp == 2) TRACE_ADD(12, t_w8);
         TRACE_T0(t_fe);
@@ -710,7 +733,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
           coords(j, &r0, &c0);
           tma_store_2d(&tmap_m, buf, c0, r0);
           tma_store_2d(&tmap_m, buf + kEpiChunkBytes, c0 + 32, r0);
-          tma_store_2d(&tmap_c, buf + 2 * kEpiChunkBytes, c0, r0);
+          if (!C::kWDirect) tma_store_2d(&tmap_c, buf + 2 * kEpiChunkBytes, c0, r0);
           tma_store_commit();
           if (NB == 1) {  // single buffer: refill it for this warp's next chunk (next tile)
             TRACE_T0(t_wr);
