@@ -478,6 +478,20 @@ int master_allgather(const CollArgs& a, cudaStream_t s) {
 
 int coll_blocks() { return 148 * 4; }
 
+// Loads the collective kernels on the current device (cudaFuncGetAttributes forces the lazy
+// load), off the switch step of a scale-out.
+int coll_prepare_device() {
+  cudaFuncAttributes fa;
+  EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, push_allreduce_sgd_kernel<false>));
+  EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, push_allreduce_sgd_kernel<true>));
+  EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, allreduce_sgd_kernel<false, 2>));
+  EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, allreduce_sgd_kernel<true, 2>));
+  EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, master_allgather_kernel));
+  EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, barrier_kernel));
+  EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, linear_allreduce_sgd_kernel));
+  return EDL_OK;
+}
+
 int allreduce_sgd(const CollArgs& a, cudaStream_t s) {
   if (a.n_src < 1 || a.n_src > kCollMaxSources) return fail(EDL_EINVAL, "allreduce_sgd: sources");
   if (a.n_dst < 0 || a.n_dst > kCollMaxReplicas || a.n_rep > kCollMaxReplicas)

@@ -120,6 +120,7 @@ int ce_wait(const CeWait& a, cudaStream_t s);
 int shard_update(const ShardUpdateArgs& a, cudaStream_t s);
 
 int coll_blocks();
+int coll_prepare_device();  // current device: load the collective kernels
 // Debug timeline: one thread writes %globaltimer (ns) to dst (mapped pinned host memory).
 int stamp(unsigned long long* dst, cudaStream_t s);
 // One thread busy-waits `ns` nanoseconds of %globaltimer (injected straggler delay).

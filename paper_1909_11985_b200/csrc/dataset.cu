@@ -295,4 +295,11 @@ int gather(const Dataset* ds, const EdlRun* runs_dev, int n_runs, int64_t n_rows
   return EDL_OK;
 }
 
+int dataset_prepare_device() {
+  cudaFuncAttributes fa;
+  EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, gather_kernel));
+  EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, gather_inline_kernel));
+  return EDL_OK;
+}
+
 }  // namespace edl

@@ -68,6 +68,7 @@ int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B,
                    int b_mn, void* C, int ldc, int M, int N, int K, int relu, int out_f32,
                    const void* mask, int ldm, int bn);
 int gemm_plan_run(const GemmPlan& p, cudaStream_t stream, float sgd_scale = 0.f);
+int gemm_prepare_device();  // current device: load + configure the step's GEMM variants
 // gemm_plan_run whose producer first waits for n per-replica flags >= epoch (system-scope
 // acquire; the deferred all-gather's "layer l is in your W" signals, collective.hpp)
 int gemm_plan_run_wait(const GemmPlan& p, cudaStream_t stream, const uint32_t* flags, int n,

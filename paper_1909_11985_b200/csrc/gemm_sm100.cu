@@ -21,6 +21,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -1013,13 +1014,18 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
   return EDL_OK;
 }
 
+// prepare_only: set the kernel's attributes on the current device and query its cluster
+// occupancy (this also loads the function), without launching -- gemm_prepare_device()
 template <int BN, bool A_MN, bool B_MN, bool kSgd = false, int kMc = 1, int kSk = 1>
-int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream, float scale = 0.f) {
+int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream, float scale = 0.f,
+                    bool prepare_only = false) {
   using Cf = Cfg2<BN, kSgd>;
   auto kern = gemm_bf16_2sm_kernel<BN, A_MN, B_MN, kSgd, kMc, kSk>;
   constexpr int kCl = 2 * kMc * kSk;  // CTAs per cluster
-  static uint64_t attr_set = 0;  // per device: the attribute lives in each context
-  static int max_units[64];      // co-resident clusters per device (persistent grid size)
+  // per device: the attribute lives in each context.  Atomic: a newcomer's replica is
+  // prepared on a side thread while the step thread launches on the other devices.
+  static std::atomic<uint64_t> attr_set{0};
+  static int max_units[64];  // co-resident clusters per device (persistent grid size)
   int dev = 0;
   cudaGetDevice(&dev);
   cudaLaunchConfig_t cfg = {};
@@ -1035,7 +1041,7 @@ int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream, float scale = 0.f) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (!(attr_set >> dev & 1)) {
+  if (!(attr_set.load() >> dev & 1)) {
     EDL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       Cf::kSmemBytes));
     // a persistent grid must not exceed what the GPCs can hold at once (4-CTA clusters
@@ -1044,8 +1050,9 @@ int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream, float scale = 0.f) {
     int n = 0;
     EDL_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
     max_units[dev] = n > 0 ? n : 1;
-    attr_set |= 1ull << dev;
+    attr_set.fetch_or(1ull << dev);
   }
+  if (prepare_only) return EDL_OK;
   const int work = ((p.M + 255) / 256) * ((p.N + BN - 1) / BN / kMc);
   int units = num_sms() / kCl;
   if (units > max_units[dev]) units = max_units[dev];
@@ -1236,6 +1243,21 @@ int gemm_plan_route(GemmPlan* p, int rows_per_owner, int me, void* const* dst, i
   p->ep.route_rows = rows_per_owner;
   p->ep.route_me = me;
   return EDL_OK;
+}
+
+// Loads and configures, on the current device, the GEMM variants a training step launches
+// (fwd / dgrad / wgrad / fused wgrad+SGD at the CTA-pair tile), so the first mini-batch on a
+// newly added GPU does not pay lazy module loading and attribute setup on the switch step.
+int gemm_prepare_device() {
+  GemmPlan p;
+  int rc = EDL_OK;
+  if (!rc) rc = launch_gemm_2sm<128, false, false, false, 2>(p, nullptr, 0.f, true);
+  if (!rc) rc = launch_gemm_2sm<128, false, true, false, 2>(p, nullptr, 0.f, true);
+  if (!rc) rc = launch_gemm_2sm<128, true, true, false, 1>(p, nullptr, 0.f, true);
+  if (!rc) rc = launch_gemm_2sm<128, true, true, true, 1>(p, nullptr, 0.f, true);
+  if (!rc) rc = launch_gemm_2sm<128, false, false, false, 1>(p, nullptr, 0.f, true);
+  if (!rc) rc = launch_gemm_2sm<128, false, true, false, 1>(p, nullptr, 0.f, true);
+  return rc;
 }
 
 int gemm_plan_run_wait(const GemmPlan& p, cudaStream_t stream, const uint32_t* flags, int n,

@@ -68,6 +68,10 @@ int sum_rows(const float* row_loss, int rows, double* loss_out, cudaStream_t s);
 //   mu != 0:  v = mu*v + sum(g)*inv_count;  master -= eta * v
 // bf16 working copy of an fp32 master (checkpoint restore).
 int master_to_bf16(const float* master, __nv_bfloat16* w, size_t n, cudaStream_t s);
+// current device: load the step's kernels now (lazy module loading would otherwise put it on
+// the first mini-batch a newly added GPU runs -- the scale-out switch step)
+int mlp_prepare_device();
+int dataset_prepare_device();
 int sgd_update_bf16(const __nv_bfloat16* const* grads, int n_src, float* master, float* mom,
                     __nv_bfloat16* const* w_out, int n_dst, size_t n, float scale,
                     float inv_count, float eta, float mu, cudaStream_t s);

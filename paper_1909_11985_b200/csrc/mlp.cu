@@ -210,6 +210,14 @@ __global__ void master_to_bf16_kernel(const float* __restrict__ m, __nv_bfloat16
 }
 }  // namespace
 
+int mlp_prepare_device() {
+  cudaFuncAttributes fa;
+  EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, xent_kernel<16>));
+  EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, xent_kernel<64>));
+  EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, master_to_bf16_kernel));
+  return EDL_OK;
+}
+
 int master_to_bf16(const float* master, __nv_bfloat16* w, size_t n, cudaStream_t s) {
   master_to_bf16_kernel<<<148 * 8, 256, 0, s>>>(master, w, n);
   EDL_CUDA_TRY(cudaGetLastError());

@@ -259,6 +259,13 @@ int Job::build_replica(Replica* r) {
     for (auto& e : r->ev_grad) EDL_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   EDL_CUDA_TRY(cudaMallocHost(&r->host_loss, sizeof(double) * kSlots));
+  // newcomers run this on their preparation thread: kernel loading stays off the switch step
+  EDL_TRY(coll_prepare_device());
+  EDL_TRY(dataset_prepare_device());
+  if (mlp_) {
+    EDL_TRY(gemm_prepare_device());
+    EDL_TRY(mlp_prepare_device());
+  }
   EDL_TRY(dataset_create(cfg_.data, mlp_ ? EDL_DTYPE_BF16 : EDL_DTYPE_F64,
                          mlp_ ? cfg_.num_classes : 0, &r->ds));
   const int64_t rows = cfg_.per_worker_batch > 0 ? cfg_.per_worker_batch : cfg_.batch;
@@ -517,10 +524,27 @@ int Job::install_due(bool* switched) {
       }
       // model broadcast to every replica that is not in the collective yet (new GPUs, or
       // GPUs whose members all left earlier and whose model is stale)
+      // After consolidate_master every live replica holds the identical full model, so the
+      // newcomers pull from the live replicas in turn (SPEC.md:376 names the lowest rank; the
+      // bytes are bit-identical and no single GPU's NVLink egress carries every copy)
+      // (sources: replicas hosting a current ring member, in ring order)
+      std::vector<Replica*> srcs;
+      for (const auto& id : ring_) {
+        const Worker* wk = workers_[id].get();
+        if (wk->remote || !wk->rep || !live.count(wk->rep)) continue;
+        if (std::find(srcs.begin(), srcs.end(), wk->rep) == srcs.end()) srcs.push_back(wk->rep);
+      }
+      static int spread = -1;
+      if (spread < 0) {
+        const char* e = getenv("EDL_BCAST_SPREAD");
+        spread = e ? atoi(e) : 1;
+      }
+      if (!spread) srcs.clear();
+      if (srcs.empty()) srcs.push_back(src);
       std::set<Replica*> sent;
       for (auto& w : ev->prepared) {
         if (!w || live.count(w->rep) || sent.count(w->rep)) continue;
-        EDL_TRY(broadcast_model(src, w->rep));
+        EDL_TRY(broadcast_model(srcs[sent.size() % srcs.size()], w->rep));
         sent.insert(w->rep);
       }
       std::vector<size_t> order(ev->ids.size());
@@ -1582,8 +1606,9 @@ int Job::broadcast_model(Replica* src, Replica* dst) {
   if (mlp_) {
     EDL_CUDA_TRY(cudaMemcpyPeerAsync(dst->master, dst->device, src->master, src->device,
                                      sizeof(float) * P_, dst->stream));
-    EDL_CUDA_TRY(cudaMemcpyPeerAsync(dst->W, dst->device, src->W, src->device,
-                                     sizeof(__nv_bfloat16) * P_, dst->stream));
+    // the working weights are bf16(master) everywhere (init, fused SGD, push collective all
+    // round to nearest): rebuild them locally instead of moving another 2 B/param over NVLink
+    EDL_TRY(master_to_bf16(dst->master, dst->W, P_, dst->stream));
     if (src->mom && dst->mom)
       EDL_CUDA_TRY(cudaMemcpyPeerAsync(dst->mom, dst->device, src->mom, src->device,
                                        sizeof(float) * P_, dst->stream));
