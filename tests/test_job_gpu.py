@@ -154,6 +154,32 @@ def test_mlp_elastic_vs_numpy_oracle(momentum):
     assert np.linalg.norm((w - w0) - (ref - w0)) <= 2e-2 * np.linalg.norm(ref - w0)
 
 
+@pytest.mark.parametrize("classes", [4096, 5000])
+def test_mlp_wide_softmax_vs_numpy_oracle(classes):
+    """Softmax-CE over more than 4096 classes (64 values per thread, BASELINE configs[4] uses
+    11264) and the single-member path that reads the loss without a collective launch."""
+    from oracle.mlp import MLPOracle
+    from paper_1909_11985_b200 import runtime as rt
+    dim, hidden, layers, B, steps, eta = 256, 256, 2, 64, 4, 0.1
+    spec = {"size": 2000, "dim": dim, "seed": 7, "noise": 0.0, "sign_labels": False}
+    cfg = rt.JobConfig(model=rt.MLP, size=spec["size"], dim=dim, seed=7, noise=0.0,
+                       num_classes=classes, layers=layers, hidden=hidden, eta=eta, decay=0.0,
+                       batch=B, lease_seed=3, partitions=64, init_seed=2)
+    job = rt.Job(cfg, ["w00"])
+    got = []
+    for _ in range(steps):
+        job.step()
+        got.append(job.sync())
+    plans, _ = _oracle_plan_steps(spec, B, 3, 64, ["w00"], [], steps)
+    orc = MLPOracle(dim, hidden, classes, layers, 7, 2, eta, 0.0)
+    for t, p in enumerate(plans):
+        ref = orc.step(p, t)
+        assert abs(got[t].loss - ref) <= 2e-3 * abs(ref), (t, got[t].loss, ref)
+    w = job.params("w00")
+    ref = orc.flat_master()
+    assert np.abs(w - ref).max() <= 1e-3 * np.abs(ref).max()
+
+
 def test_mlp_init_matches_oracle():
     from oracle.mlp import MLPOracle
     from paper_1909_11985_b200 import runtime as rt

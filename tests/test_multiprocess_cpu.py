@@ -75,3 +75,55 @@ def test_two_process_replicated_protocol():
     assert c0 == ocounts
     ok, fe, detail = api.check_coverage(restated(), log0, SPEC["size"])
     assert ok, detail
+
+
+def _worker_static(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1909_11985_b200 import runtime as rt
+    # bench.py's N-GPU shape: one member per process, fixed per-worker batch
+    cfg = rt.JobConfig(model=rt.MLP, size=1 << 16, dim=64, seed=1, noise=0.0, num_classes=64,
+                       layers=2, hidden=64, batch=512, per_worker_batch=512, lease_seed=7,
+                       partitions=0, max_workers=world, init_seed=0, dry_run=True)
+    ring = [f"w{r:02d}" for r in range(world)]
+    job = rt.Job(cfg, ring, [0 if i == rank else -1 for i in range(world)])
+    blobs = [None] * world
+    dist.all_gather_object(blobs, job.export_handles())
+    for r, b in enumerate(blobs):
+        if r != rank:
+            job.import_handles(b)
+    counts = [job.step().count for _ in range(STEPS)]
+    logs = [None] * world
+    dist.all_gather_object(logs, (job.log_text(), counts))
+    if rank == 0:
+        out.put(logs)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_eight_process_static_ring_protocol():
+    """The driver's 8-GPU scaling run: eight processes, one ring member each, replay the same
+    lease protocol (every mini-batch 8 x 512 samples) and agree with the oracle."""
+    world = 8
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_static, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    logs = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert all(lg == logs[0] for lg in logs)
+    log0, c0 = logs[0]
+    assert c0 == [8 * 512] * STEPS
+
+    from oracle import api, restated
+    spec = {"size": 1 << 16, "dim": 64, "seed": 1, "noise": 0.0, "sign_labels": False}
+    ring = [f"w{r:02d}" for r in range(world)]
+    oj = api.Job(restated(), spec, 2, 0.0, 0.0, 512 * world, 7, 64, ring, per_worker=512)
+    for _ in range(STEPS):
+        oj.step()
+    assert log0 == oj.log_text()
