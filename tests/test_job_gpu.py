@@ -177,7 +177,13 @@ def test_mlp_wide_softmax_vs_numpy_oracle(classes):
         assert abs(got[t].loss - ref) <= 2e-3 * abs(ref), (t, got[t].loss, ref)
     w = job.params("w00")
     ref = orc.flat_master()
-    assert np.abs(w - ref).max() <= 1e-3 * np.abs(ref).max()
+    w0 = MLPOracle(dim, hidden, classes, layers, 7, 2, eta, 0.0).flat_master()
+    err = np.abs(w - ref)
+    # bf16 activations / gradients: single-ulp rounding flips between the GPU and numpy are
+    # expected, so bound the max by one bf16 ulp of max|w| and the mean tightly (as the
+    # multi-GPU parity test does), and require the trained change itself to agree
+    assert err.max() <= 2 ** -8 * np.abs(ref).max() and err.mean() <= 1e-4 * np.abs(ref).max()
+    assert np.linalg.norm((w - w0) - (ref - w0)) <= 2e-2 * np.linalg.norm(ref - w0)
 
 
 def test_mlp_init_matches_oracle():
