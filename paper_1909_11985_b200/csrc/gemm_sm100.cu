@@ -607,6 +607,19 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
       *c0 = tile_n(t) * BN + (half * kCPW + j % kCPW) * 64;
       return true;
     };
+    // fused exchange: does this replica own the rows of chunk j's tile?  (the host keeps
+    // whole 256-row tiles inside one owner block and NB == 1)
+    auto owner_of = [&](int j) -> int {
+      const int t = unit + (j / kCPW) * n_units;
+      return ep.xchg ? (tile_m(t) * 256) / ep.route_rows : ep.route_me;
+    };
+    auto next_own = [&](int j) -> int {  // first chunk >= j whose master this warp loads
+      if (!ep.xchg) return j;
+      for (;; ++j) {
+        if (unit + (j / kCPW) * n_units >= num_work) return j;  // past the end: no load
+        if (owner_of(j) == ep.route_me) return j;
+      }
+    };
     auto prefetch = [&](int j) {
       int r0, c0;
       if (!coords(j, &r0, &c0)) return;
@@ -627,9 +640,14 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
     };
     if (lane == 0) {
       for (int i = 0; i < ep.pf_tiles; ++i) l2_prefetch_tile(unit + i * n_units);
-      for (int p0 = 0; p0 < (NB > 1 ? C::kSgdPfd : 1) && !skip_epi; ++p0) prefetch(p0);
+      if (NB == 1) {
+        if (!skip_epi) prefetch(next_own(0));
+      } else {
+        for (int p0 = 0; p0 < C::kSgdPfd && !skip_epi; ++p0) prefetch(p0);
+      }
     }
     int j = 0;
+    int n_used = 0;  // master chunks consumed (NB == 1: barrier phase n_used & 1)
     int local = 0;
     TRACE_T0(t_epi);
     for (int w = unit; w < num_work; w += n_units, ++local) {
@@ -672,12 +690,77 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
 #pragma unroll
         for (int e = 0; e < 64; ++e) g[e] = __bfloat162float(__float2bfloat16_rn(g[e]));
         if (warp == 2) TRACE_ADD(9, t_ld);
-        TRACE_T0(t_ml);
-        mbar_wait(&mb[b], (j / NB) & 1);
-        if (warp == 2) TRACE_ADD(7, t_ml);
-        TRACE_T0(t_cs);
         uint8_t* buf = wbase + b * C::kSgdBufBytes;
         uint8_t* wrow = buf + 2 * kEpiChunkBytes + lane * 128;
+        if (ep.xchg) {
+          int r0, c0;
+          coords(j, &r0, &c0);
+          const int owner = owner_of(j);
+          const int tile = unit + (j / kCPW) * n_units;
+          if (owner != ep.route_me) {
+            // reduce-scatter: my bf16 gradient chunk -> the owner's receive slot, then count it
+            // on the owner's arrival counter once the bulk store has completed
+#pragma unroll
+            for (int j8 = 0; j8 < 8; ++j8) {
+              uint4 o;
+              o.x = pack_bf16(g[8 * j8 + 0], g[8 * j8 + 1]);
+              o.y = pack_bf16(g[8 * j8 + 2], g[8 * j8 + 3]);
+              o.z = pack_bf16(g[8 * j8 + 4], g[8 * j8 + 5]);
+              o.w = pack_bf16(g[8 * j8 + 6], g[8 * j8 + 7]);
+              *reinterpret_cast<uint4*>(wrow + ((j8 ^ (lane & 7)) << 4)) = o;
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&pm.m[owner], buf + 2 * kEpiChunkBytes, c0, r0 - owner * ep.route_rows);
+              tma_store_commit();
+              tma_store_wait<0>();  // written (not just read): the owner may consume it now
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+              __threadfence_system();
+              asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(ep.x_ctr[owner] + tile)
+                           : "memory");
+            }
+            __syncwarp();
+            continue;
+          }
+          // my rows: wait for every peer's share of this tile, then the ring-order sum of the
+          // members' bf16 gradients (the push collective's order, collective.cu)
+          if (lane == 0) wait_flags_acquire(ep.x_ctr[ep.route_me] + tile, 1, ep.x_target);
+          __syncwarp();
+          const size_t rrow = static_cast<size_t>(r0 - ep.route_me * ep.route_rows + lane);
+#pragma unroll
+          for (int j8 = 0; j8 < 8; ++j8) {
+            float s8[8];
+#pragma unroll 1
+            for (int k = 0; k < ep.x_n; ++k) {
+              const int r = ep.x_order[k];
+              float v[8];
+              if (r == ep.route_me) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[e] = g[8 * j8 + e];
+              } else {
+                const uint4 u = *reinterpret_cast<const uint4*>(ep.x_recv[r] + rrow * ep.x_ldr +
+                                                                c0 + 8 * j8);
+                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f2 = __bfloat1622float2(h2[e]);
+                  v[2 * e] = f2.x;
+                  v[2 * e + 1] = f2.y;
+                }
+              }
+#pragma unroll
+              for (int e = 0; e < 8; ++e) s8[e] = k == 0 ? v[e] : __fadd_rn(s8[e], v[e]);
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) g[8 * j8 + e] = s8[e];
+          }
+        }
+        TRACE_T0(t_ml);
+        mbar_wait(&mb[b], NB == 1 ? (n_used & 1) : ((j / NB) & 1));
+        ++n_used;
+        if (warp == 2) TRACE_ADD(7, t_ml);
+        TRACE_T0(t_cs);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint8_t* mrow = buf + h * kEpiChunkBytes + lane * 128;
@@ -735,12 +818,16 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
           tma_store_2d(&tmap_m, buf, c0, r0);
           tma_store_2d(&tmap_m, buf + kEpiChunkBytes, c0 + 32, r0);
           if (!C::kWDirect) tma_store_2d(&tmap_c, buf + 2 * kEpiChunkBytes, c0, r0);
+          if (ep.xchg) {  // all-gather: the updated weights into every other replica
+            for (int o = 0; o < ep.x_n; ++o)
+              if (o != ep.route_me) tma_store_2d(&pm.w[o], buf + 2 * kEpiChunkBytes, c0, r0);
+          }
           tma_store_commit();
           if (NB == 1) {  // single buffer: refill it for this warp's next chunk (next tile)
             TRACE_T0(t_wr);
             tma_store_wait_read<0>();
             if (warp == 2) TRACE_ADD(6, t_wr);
-            prefetch(j + 1);
+            prefetch(next_own(j + 1));
           }
         }
         if (warp == 2) TRACE_ADD(10, t_cs);
@@ -1243,6 +1330,45 @@ int gemm_plan_route(GemmPlan* p, int rows_per_owner, int me, void* const* dst, i
   p->ep.route_rows = rows_per_owner;
   p->ep.route_me = me;
   return EDL_OK;
+}
+
+int gemm_plan_exchange(GemmPlan* p, int rows_per_owner, int me, int n, void* const* recv_dst,
+                       __nv_bfloat16* const* w_dst, uint32_t* const* ctr,
+                       const __nv_bfloat16* const* recv_src, int ld_recv, const int* order) {
+  if (!p->ep.sgd || p->cg != 2 || p->bn != 128 || p->mc != 1)
+    return fail(EDL_EINVAL, "gemm exchange: needs a fused-SGD CTA-pair plan (N tile 128)");
+  if (Cfg2<128, true>::kSgdBufs != 1)
+    return fail(EDL_EINVAL, "gemm exchange: single-buffer fused-SGD epilogue only");
+  if (n < 2 || n > kMaxPeerMaps || me < 0 || me >= n || rows_per_owner <= 0 ||
+      rows_per_owner % 256 || rows_per_owner * n != p->M || p->N % 128)
+    return fail(EDL_EINVAL, "gemm exchange: owner blocks must tile M in 256-row multiples");
+  for (int o = 0; o < n; ++o) {
+    p->ep.x_ctr[o] = ctr[o];
+    p->ep.x_recv[o] = recv_src[o];
+    p->ep.x_order[o] = order[o];
+    if (o == me) {
+      p->pm.m[o] = p->tc;
+      p->pm.w[o] = p->tc;
+      continue;
+    }
+    int rc = make_tmap_t(&p->pm.m[o], recv_dst[o], rows_per_owner, p->N, p->N, 64, 32, false);
+    if (rc) return fail(rc, "gemm exchange: tensor map of a peer receive slot");
+    rc = make_tmap_t(&p->pm.w[o], w_dst[o], p->M, p->N, p->N, 64, 32, false);
+    if (rc) return fail(rc, "gemm exchange: tensor map of a peer's weights");
+  }
+  p->ep.route_rows = rows_per_owner;
+  p->ep.route_me = me;
+  p->ep.xchg = 1;
+  p->ep.x_n = n;
+  p->ep.x_ldr = ld_recv;
+  return EDL_OK;
+}
+
+int gemm_plan_run_exchange(const GemmPlan& p, cudaStream_t stream, float sgd_scale,
+                           uint32_t target) {
+  GemmPlan q = p;
+  q.ep.x_target = target;
+  return gemm_plan_run(q, stream, sgd_scale);
 }
 
 // Loads and configures, on the current device, the GEMM variants a training step launches

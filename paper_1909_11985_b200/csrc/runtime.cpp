@@ -656,6 +656,37 @@ int Job::ensure_plans(Worker* w, int64_t rows) {
     w->rs_plan_rows = rows;
     w->rs_plan_version = version_;
   }
+  if (overlap_mode_ == 4 && (w->x_plan_rows != rows || w->x_plan_version != version_)) {
+    const int n = static_cast<int>(peers_.size());
+    const int me = rep_index(r);
+    w->wgrad_x.assign(static_cast<size_t>(L_), GemmPlan{});
+    int order[kMaxPeerMaps] = {};
+    for (size_t k = 0; k < ring_.size(); ++k) order[k] = host_index(ring_[k]);
+    for (int l = 0; l < L_; ++l) {
+      const bool last = l == L_ - 1;
+      const __nv_bfloat16* dy = last ? r->dlog : r->dx[(l + 1) & 1];
+      EDL_TRY(gemm_plan_init_sgd(&w->wgrad_x[l], dy, out_[l], 1, r->act[l], in_[l], 1,
+                                 r->master + off_[l], r->W + off_[l], in_[l], out_[l], in_[l],
+                                 static_cast<int>(rows)));
+      const int prow = out_[l] / n;
+      void* dst[kMaxPeerMaps] = {};
+      __nv_bfloat16* wd[kMaxPeerMaps] = {};
+      uint32_t* ctr[kMaxPeerMaps] = {};
+      const __nv_bfloat16* src[kMaxPeerMaps] = {};
+      for (int o = 0; o < n; ++o) {
+        wd[o] = peers_[o].W + off_[l];
+        ctr[o] = peers_[o].flags + kXchgOffset + static_cast<size_t>(l) * kXchgMaxTiles;
+        if (o == me) continue;
+        const size_t slot = static_cast<size_t>(me < o ? me : me - 1);  // mine in o's recv
+        dst[o] = peers_[o].recv + (slot * shard_total8(o) + seg_off8(o, l)) * 8;
+        const size_t from = static_cast<size_t>(o < me ? o : o - 1);  // o's in my recv
+        src[o] = r->recv + (from * shard_total8(me) + seg_off8(me, l)) * 8;
+      }
+      EDL_TRY(gemm_plan_exchange(&w->wgrad_x[l], prow, me, n, dst, wd, ctr, src, in_[l], order));
+    }
+    w->x_plan_rows = rows;
+    w->x_plan_version = version_;
+  }
   if (fused_update_ && w->sgd_plan_rows != rows) {
     w->wgrad_sgd.assign(static_cast<size_t>(L_), GemmPlan{});
     for (int l = 0; l < L_; ++l) {
@@ -745,6 +776,10 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
       // dW + sgd_step in one kernel (layer 0 ends the backward: nothing left to overlap)
       EDL_TRY(gemm_plan_run(w->wgrad_sgd[l], r->stream, step_scale_));
       if (mw) mark(slot, 5, mw, r->stream);
+    } else if (overlap_mode_ == 4) {
+      // dW + reduce-scatter + sharded SGD + weight all-gather in one kernel per layer
+      EDL_TRY(gemm_plan_run_exchange(w->wgrad_x[l], r->stream, step_scale_, x_expected_));
+      if (mw) mark(slot, 5, mw, r->stream);
     } else if (overlap_mode_ == 3) {
       // dW with the reduce-scatter in its epilogue: rows owned elsewhere are stored into the
       // owner's recv over NVLink while the backward continues; the shard update + all-gather
@@ -766,7 +801,7 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
     launches_ += 1;
   }
   EDL_CUDA_TRY(cudaEventRecord(w->ev_w1[slot], r->stream));
-  if (overlap_ && last && overlap_mode_ != 3) EDL_TRY(finish_layer_colls(r));
+  if (overlap_ && last && overlap_mode_ != 3 && overlap_mode_ != 4) EDL_TRY(finish_layer_colls(r));
   m = mark(slot, 3, m, r->stream);
   (void)m;
   launches_ += 1 + static_cast<uint64_t>(L_) + 1 + static_cast<uint64_t>(2 * L_ - 1);
@@ -874,6 +909,20 @@ bool Job::rs_eligible() const {
 }
 
 // Push collective: one ring member per replica, every replica's recv mapped here.
+// Mode 4 keeps whole 256-row tiles inside one owner block, plain SGD (the epilogue applies
+// the update), and a topology that has not changed since the job started (the per-tile
+// arrival counters are cumulative and a newcomer's would start at zero).
+bool Job::xchg_eligible() const {
+  if (!rs_eligible() || cfg_.momentum != 0.0 || version_ != 1) return false;
+  const int n = static_cast<int>(peers_.size());
+  for (int l = 0; l < L_; ++l) {
+    if (out_[l] % (256 * n) != 0 || in_[l] % 128 != 0) return false;
+    if (static_cast<size_t>(out_[l] / 256) * static_cast<size_t>(in_[l] / 128) > kXchgMaxTiles)
+      return false;
+  }
+  return true;
+}
+
 bool Job::push_eligible() const {
   static int env = -1;
   if (env < 0) {
@@ -1784,6 +1833,8 @@ int Job::step(EdlStepReport* out) {
   // samples/s at N=2, 1.89M vs 1.77M at N=4 over the single push collective.
   if (mlp_ && count > 0 && overlap_env < 0 && peers_.size() > 1 && rs_eligible())
     overlap_mode_ = 3;
+  if (overlap_mode_ == 4 && !xchg_eligible()) overlap_mode_ = rs_eligible() ? 3 : 0;
+  if (overlap_mode_ == 4) x_expected_ += 16u * static_cast<uint32_t>(peers_.size() - 1);
   overlap_ = overlap_mode_ != 0;
   // deferred all-gather (mode 3, EDL_AG_DEFER=1): the push collective of this mini-batch
   // overlaps the next mini-batch's forward.  Opt-in: measured on B200 the push kernel on a

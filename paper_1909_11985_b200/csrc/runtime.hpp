@@ -113,6 +113,9 @@ struct Worker {
   std::vector<GemmPlan> wgrad;
   std::vector<GemmPlan> wgrad_sgd;  // fused weight-gradient + SGD (single-member ring)
   std::vector<GemmPlan> wgrad_rs;   // weight gradient + reduce-scatter into the owners' recv
+  std::vector<GemmPlan> wgrad_x;    // fused exchange: RS + sharded SGD + weight all-gather
+  int64_t x_plan_rows = -1;
+  uint64_t x_plan_version = 0;
   int64_t rs_plan_rows = -1;
   uint64_t rs_plan_version = 0;
   int64_t plan_rows = -1;
@@ -243,6 +246,8 @@ class Job {
                           // 3: reduce-scatter fused into the wgrad GEMM epilogues
   bool ag_defer_ = false;  // mode 3 + the push collective overlapped with the next forward
   bool rs_eligible() const;
+  bool xchg_eligible() const;  // exchange mode 4 (fused into the weight-gradient GEMMs)
+  uint32_t x_expected_ = 0;    // arrival count every owned tile reaches this mini-batch
   bool push_eligible() const;
   uint32_t ce_epoch_ = 0;
   int host_index(const std::string& id) const;  // peers_ index of the replica hosting id

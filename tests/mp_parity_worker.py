@@ -89,7 +89,8 @@ def main():
     # 3. an MLP whose layers split into per-GPU row blocks: with the default EDL_OVERLAP the
     #    reduce-scatter rides in the weight-gradient GEMM epilogues (TMA stores into the
     #    owner's receive buffer over NVLink), then per-layer shard update + all-gather
-    dim, hidden, classes, layers, steps = 256, 512, 512, 3, 6
+    # (1024-wide layers: whole 256-row tiles per owner at 4 GPUs, so EDL_OVERLAP=4 applies)
+    dim, hidden, classes, layers, steps = 256, 1024, 1024, 3, 6
     B = 64 * world
     mspec = {"size": 4000, "dim": dim, "seed": 9}
     cfg = rt.JobConfig(model=rt.MLP, size=4000, dim=dim, seed=9, noise=0.0, num_classes=classes,

@@ -16,9 +16,11 @@ pytestmark = pytest.mark.gpu
 # stream, 2 = per-layer copy-engine transfers + shard updates, 3 = reduce-scatter in the
 # wgrad GEMM epilogues + per-layer shard update / all-gather.  "3/defer" runs mode 3's push
 # collective on a side stream overlapping the next forward (EDL_AG_DEFER=1, per-layer flags).
+# 4 = the whole exchange (reduce-scatter, sharded SGD, weight all-gather) inside the
+# weight-gradient GEMMs, per-tile arrival counters across GPUs.
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("overlap", ["", "0", "1", "2", "3", "3/defer"])
+@pytest.mark.parametrize("overlap", ["", "0", "1", "2", "3", "3/defer", "4"])
 def test_two_or_more_gpus_match_oracle(overlap):
     n = min(torch.cuda.device_count(), 4)
     here = os.path.dirname(os.path.abspath(__file__))
