@@ -21,12 +21,8 @@ constexpr size_t kCeFlagWords = 2ull * kCollMaxSegs * kCollMaxReplicas;
 // kCollMaxReplicas], then this replica's per-layer CTA completion counters [kCollMaxSegs].
 constexpr size_t kAgFlagWords = static_cast<size_t>(kCollMaxSegs) * kCollMaxReplicas + kCollMaxSegs;
 constexpr size_t kAgFlagOffset = kCollBarrierWords + kCeFlagWords;  // in words
-// Fused exchange (exchange mode 4): this replica's per-tile arrival counters of every layer,
-// [kCollMaxSegs layers][kXchgMaxTiles tiles] (incremented by the peers' weight-gradient GEMMs)
-constexpr size_t kXchgMaxTiles = 4096;
-constexpr size_t kXchgOffset = kCollBarrierWords + kCeFlagWords + kAgFlagWords;  // in words
 constexpr size_t kCollFlagBytes =
-    (kXchgOffset + static_cast<size_t>(kCollMaxSegs) * kXchgMaxTiles) * sizeof(uint32_t);
+    (kCollBarrierWords + kCeFlagWords + kAgFlagWords) * sizeof(uint32_t);
 // this replica's flags for layer l: one word per source replica
 #ifdef __CUDACC__
 __host__ __device__

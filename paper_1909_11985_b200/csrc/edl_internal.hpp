@@ -53,15 +53,13 @@ struct EpiParams {
   uint32_t wait_epoch;
   // fused exchange (fused-SGD plan, N > 1, one ring member per GPU; gemm_plan_exchange):
   // tiles whose rows replica o != route_me owns are stored as bf16 into o's receive slot
-  // (PeerMaps::m[o]) and counted on o's arrival counter for the tile; tiles this replica owns
-  // wait until the counter reaches x_target, sum the members' gradients in ring order
-  // (x_order: replica of ring member k), update the fp32 master and store the bf16 weights
-  // into every replica (PeerMaps::w[o]).  The reduce-scatter, the update and the all-gather
-  // of the weights all happen inside the weight-gradient GEMM.
+  // (PeerMaps::m[o]); tiles this replica owns wait until every peer's chunk has replaced the
+  // sentinel in its slot, sum the members' gradients in ring order (x_order: replica of ring
+  // member k), update the fp32 master and store the bf16 weights into every replica
+  // (PeerMaps::w[o]).  The reduce-scatter, the update and the all-gather of the weights all
+  // happen inside the weight-gradient GEMM.
   int xchg;
   int x_n;
-  uint32_t x_target;
-  uint32_t* x_ctr[kMaxPeerMaps];                // replica o's counters for this layer's tiles
   const __nv_bfloat16* x_recv[kMaxPeerMaps];    // my receive slot of source replica r ([prow][ldr])
   int x_ldr;
   int x_order[kMaxPeerMaps];
@@ -99,14 +97,11 @@ int gemm_pick_bn(int M, int N, bool b_mn);
 int gemm_plan_route(GemmPlan* p, int rows_per_owner, int me, void* const* dst, int n_owner);
 // Turns a fused-SGD plan into the fused exchange (EpiParams::xchg): recv_dst[o] = replica o's
 // receive slot for this replica (layer-relative rows), w_dst[o] = replica o's weights of the
-// layer, ctr[o] = replica o's per-tile arrival counters, recv_src[r] = this replica's
-// receive slot of source r (ld_recv), order[k] = replica of ring member k.
+// layer, recv_src[r] = this replica's receive slot of source r (ld_recv; filled with 0xFF
+// bytes before the first mini-batch), order[k] = replica of ring member k.
 int gemm_plan_exchange(GemmPlan* p, int rows_per_owner, int me, int n, void* const* recv_dst,
-                       __nv_bfloat16* const* w_dst, uint32_t* const* ctr,
-                       const __nv_bfloat16* const* recv_src, int ld_recv, const int* order);
-// every owned tile's arrival counter must reach `target` (cumulative over mini-batches)
-int gemm_plan_run_exchange(const GemmPlan& p, cudaStream_t stream, float sgd_scale,
-                           uint32_t target);
+                       __nv_bfloat16* const* w_dst, const __nv_bfloat16* const* recv_src,
+                       int ld_recv, const int* order);
 int gemm_bf16(const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
               int ldc, int M, int N, int K, int relu, int out_f32, const void* mask, int ldm,
               int bn, cudaStream_t stream);

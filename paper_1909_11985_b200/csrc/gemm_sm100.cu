@@ -380,7 +380,7 @@ struct Cfg2 {
 // mainloop each CTA owns one column half of the tile: it sends the other half of its fp32
 // partial to the matching CTA of the other pair through DSMEM (into that CTA's idle stage
 // buffers), receives that CTA's partial of its own half, adds, and runs the epilogue.
-template <int BN, bool A_MN, bool B_MN, bool kSgd, int kMc, int kSk = 1>
+template <int BN, bool A_MN, bool B_MN, bool kSgd, int kMc, int kSk = 1, bool kX = false>
 __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                          const __grid_constant__ CUtensorMap tmap_b,
@@ -390,6 +390,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
   using C = Cfg2<BN, kSgd>;
   static_assert(kSk == 1 || (kSk == 2 && kMc == 1 && !kSgd && BN == 256),
                 "split-K: 256-wide plain tiles, no multicast");
+  static_assert(!kX || (kSgd && kMc == 1 && kSk == 1), "fused exchange: fused-SGD plans");
   // kMc = 4 (8-CTA clusters, K-major A) compiles and was measured: slower than 2 on B200
   static_assert(kMc == 1 || kMc == 2 || (kMc == 4 && !A_MN), "A multicast: 2 pairs, or 4 (K-major A)");
   extern __shared__ uint8_t smem_raw[];
@@ -418,6 +419,23 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
   auto tile_m = [&](int w) { return w % m_tiles; };
   auto tile_n = [&](int w) {
     return (w / m_tiles) * kMc + (kMc >= 2 ? static_cast<int>(pidx) : 0);
+  };
+  // the unit's work sequence: tiles unit, unit + n_units, ...; with the fused exchange (kX)
+  // the tiles other replicas own come first, so every peer's share of my tiles is sent
+  // before anyone waits for it (in lock-step order the replicas would take turns waiting)
+  auto seq_tile = [&](int i) -> int {
+    if (!kX) {
+      const int t = unit + i * n_units;
+      return t < num_work ? t : num_work;
+    }
+    int k = 0;
+    for (int ph = 0; ph < 2; ++ph)
+      for (int t = unit; t < num_work; t += n_units) {
+        const bool own = (tile_m(t) * 256) / ep.route_rows == ep.route_me;
+        if (own != (ph == 1)) continue;
+        if (k++ == i) return t;
+      }
+    return num_work;
   };
   // split-K: this pair's k-blocks (the host guarantees one tile per cluster)
   const int kb_begin = kSk == 2 ? static_cast<int>(pidx) * (num_kb / 2) : 0;
@@ -471,7 +489,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
       if (lane == 0) wait_flags_acquire(ep.wait_flags, ep.wait_n, ep.wait_epoch);
       __syncwarp();
     }
-    for (int w = unit; w < num_work; w += n_units) {
+    for (int wi = 0, w = seq_tile(0); w < num_work; w = seq_tile(++wi)) {
       const int m0 = tile_m(w) * 256 + static_cast<int>(pr) * 128;
       const int n0 = tile_n(w) * BN + static_cast<int>(pr) * C::kHalfN;
       for (int kb = kb_begin; kb < kb_end; ++kb) {
@@ -548,7 +566,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
       // one fixed issuing lane: tcgen05.commit only tracks the MMAs of the executing thread
       const bool issuer = elect_one();
       TRACE_T0(t_mma);
-      for (int w = unit; w < num_work; w += n_units, ++local) {
+      for (int wi = 0, w = seq_tile(0); w < num_work; w = seq_tile(++wi), ++local) {
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         TRACE_T0(t_te);
@@ -601,7 +619,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
     uint8_t* wbase = epi + ew * NB * C::kSgdBufBytes;
     uint64_t* mb = sgd_bar + ew * NB;
     auto coords = [&](int j, int* r0, int* c0) -> bool {
-      const int t = unit + (j / kCPW) * n_units;
+      const int t = seq_tile(j / kCPW);
       if (t >= num_work) return false;
       *r0 = tile_m(t) * 256 + static_cast<int>(pr) * 128 + q * 32;
       *c0 = tile_n(t) * BN + (half * kCPW + j % kCPW) * 64;
@@ -610,13 +628,13 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
     // fused exchange: does this replica own the rows of chunk j's tile?  (the host keeps
     // whole 256-row tiles inside one owner block and NB == 1)
     auto owner_of = [&](int j) -> int {
-      const int t = unit + (j / kCPW) * n_units;
-      return ep.xchg ? (tile_m(t) * 256) / ep.route_rows : ep.route_me;
+      const int t = seq_tile(j / kCPW);
+      return kX ? (tile_m(t) * 256) / ep.route_rows : ep.route_me;
     };
     auto next_own = [&](int j) -> int {  // first chunk >= j whose master this warp loads
-      if (!ep.xchg) return j;
+      if (!kX) return j;
       for (;; ++j) {
-        if (unit + (j / kCPW) * n_units >= num_work) return j;  // past the end: no load
+        if (seq_tile(j / kCPW) >= num_work) return j;  // past the end: no load
         if (owner_of(j) == ep.route_me) return j;
       }
     };
@@ -639,7 +657,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
       for (int c = 0; c < BN / kHalves; c += 32) tma_prefetch_2d(&tmap_m, c0 + c, r0);
     };
     if (lane == 0) {
-      for (int i = 0; i < ep.pf_tiles; ++i) l2_prefetch_tile(unit + i * n_units);
+      for (int i = 0; i < ep.pf_tiles && !kX; ++i) l2_prefetch_tile(unit + i * n_units);
       if (NB == 1) {
         if (!skip_epi) prefetch(next_own(0));
       } else {
@@ -650,10 +668,10 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
     int n_used = 0;  // master chunks consumed (NB == 1: barrier phase n_used & 1)
     int local = 0;
     TRACE_T0(t_epi);
-    for (int w = unit; w < num_work; w += n_units, ++local) {
+    for (int wi = 0, w = seq_tile(0); w < num_work; w = seq_tile(++wi), ++local) {
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      if (lane == 0 && ep.pf_tiles > 0) l2_prefetch_tile(w + ep.pf_tiles * n_units);
+      if (lane == 0 && ep.pf_tiles > 0 && !kX) l2_prefetch_tile(w + ep.pf_tiles * n_units);
       TRACE_T0(t_tf);
       mbar_wait(&tfull_bar[acc], acc_phase);
       if (warp == 2) TRACE_ADD(5, t_tf);
@@ -692,11 +710,15 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
         if (warp == 2) TRACE_ADD(9, t_ld);
         uint8_t* buf = wbase + b * C::kSgdBufBytes;
         uint8_t* wrow = buf + 2 * kEpiChunkBytes + lane * 128;
-        if (ep.xchg) {
+        if constexpr (kX) {
           int r0, c0;
           coords(j, &r0, &c0);
           const int owner = owner_of(j);
-          const int tile = unit + (j / kCPW) * n_units;
+          const int tile = seq_tile(j / kCPW);
+          // the previous chunk's bulk store (a routed one is not waited on) must have read the
+          // staging area before it is written again
+          if (lane == 0) tma_store_wait_read<0>();
+          __syncwarp();
           if (owner != ep.route_me) {
             // reduce-scatter: my bf16 gradient chunk -> the owner's receive slot, then count it
             // on the owner's arrival counter once the bulk store has completed
@@ -714,47 +736,69 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
             if (lane == 0) {
               tma_store_2d(&pm.m[owner], buf + 2 * kEpiChunkBytes, c0, r0 - owner * ep.route_rows);
               tma_store_commit();
-              tma_store_wait<0>();  // written (not just read): the owner may consume it now
-              asm volatile("fence.proxy.async.global;" ::: "memory");
-              __threadfence_system();
-              asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(ep.x_ctr[owner] + tile)
-                           : "memory");
             }
             __syncwarp();
             continue;
           }
-          // my rows: wait for every peer's share of this tile, then the ring-order sum of the
-          // members' bf16 gradients (the push collective's order, collective.cu)
-          if (lane == 0) wait_flags_acquire(ep.x_ctr[ep.route_me] + tile, 1, ep.x_target);
-          __syncwarp();
+          // my rows: the receive slots hold the sentinel 0xFFFF (a NaN no bf16 rounding
+          // produces) until a peer's bf16 chunk lands, so the data is its own arrival signal
+          // (no per-chunk completion wait or flag round trip on the sender).  Per 32-column
+          // half: walk the ring order, taking my own values from g and each peer's from its
+          // slot (4 independent 16-byte loads, re-issued until no sentinel is left), then put
+          // the sentinel back for the next mini-batch.
           const size_t rrow = static_cast<size_t>(r0 - ep.route_me * ep.route_rows + lane);
 #pragma unroll
-          for (int j8 = 0; j8 < 8; ++j8) {
-            float s8[8];
+          for (int h = 0; h < 2; ++h) {
+            float s[32];
 #pragma unroll 1
             for (int k = 0; k < ep.x_n; ++k) {
               const int r = ep.x_order[k];
-              float v[8];
+              float v[32];
               if (r == ep.route_me) {
 #pragma unroll
-                for (int e = 0; e < 8; ++e) v[e] = g[8 * j8 + e];
+                for (int e = 0; e < 32; ++e) v[e] = g[32 * h + e];
               } else {
-                const uint4 u = *reinterpret_cast<const uint4*>(ep.x_recv[r] + rrow * ep.x_ldr +
-                                                                c0 + 8 * j8);
-                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+                const uint4* src =
+                    reinterpret_cast<const uint4*>(ep.x_recv[r] + rrow * ep.x_ldr + c0 + 32 * h);
+                uint4 u[4];
+                for (;;) {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const float2 f2 = __bfloat1622float2(h2[e]);
-                  v[2 * e] = f2.x;
-                  v[2 * e + 1] = f2.y;
+                  for (int q4 = 0; q4 < 4; ++q4)
+                    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(u[q4].x), "=r"(u[q4].y), "=r"(u[q4].z), "=r"(u[q4].w)
+                                 : "l"(src + q4));
+                  bool ready = true;
+#pragma unroll
+                  for (int q4 = 0; q4 < 4; ++q4) {
+                    const uint32_t wv[4] = {u[q4].x, u[q4].y, u[q4].z, u[q4].w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                      ready = ready && (wv[e] & 0xFFFFu) != 0xFFFFu && (wv[e] >> 16) != 0xFFFFu;
+                  }
+                  if (ready) break;
+                  __nanosleep(32);
                 }
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                  const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u[q4]);
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const float2 f2 = __bfloat1622float2(h2[e]);
+                    v[8 * q4 + 2 * e] = f2.x;
+                    v[8 * q4 + 2 * e + 1] = f2.y;
+                  }
+                }
+                uint4* dst = const_cast<uint4*>(src);  // consumed: sentinel back
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) dst[q4] = make_uint4(~0u, ~0u, ~0u, ~0u);
               }
 #pragma unroll
-              for (int e = 0; e < 8; ++e) s8[e] = k == 0 ? v[e] : __fadd_rn(s8[e], v[e]);
+              for (int e = 0; e < 32; ++e) s[e] = k == 0 ? v[e] : __fadd_rn(s[e], v[e]);
             }
 #pragma unroll
-            for (int e = 0; e < 8; ++e) g[8 * j8 + e] = s8[e];
+            for (int e = 0; e < 32; ++e) g[32 * h + e] = s[e];
           }
+          (void)tile;
         }
         TRACE_T0(t_ml);
         mbar_wait(&mb[b], NB == 1 ? (n_used & 1) : ((j / NB) & 1));
@@ -818,7 +862,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
           tma_store_2d(&tmap_m, buf, c0, r0);
           tma_store_2d(&tmap_m, buf + kEpiChunkBytes, c0 + 32, r0);
           if (!C::kWDirect) tma_store_2d(&tmap_c, buf + 2 * kEpiChunkBytes, c0, r0);
-          if (ep.xchg) {  // all-gather: the updated weights into every other replica
+          if (kX) {  // all-gather: the updated weights into every other replica
             for (int o = 0; o < ep.x_n; ++o)
               if (o != ep.route_me) tma_store_2d(&pm.w[o], buf + 2 * kEpiChunkBytes, c0, r0);
           }
@@ -1103,11 +1147,12 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
 
 // prepare_only: set the kernel's attributes on the current device and query its cluster
 // occupancy (this also loads the function), without launching -- gemm_prepare_device()
-template <int BN, bool A_MN, bool B_MN, bool kSgd = false, int kMc = 1, int kSk = 1>
+template <int BN, bool A_MN, bool B_MN, bool kSgd = false, int kMc = 1, int kSk = 1,
+          bool kX = false>
 int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream, float scale = 0.f,
                     bool prepare_only = false) {
   using Cf = Cfg2<BN, kSgd>;
-  auto kern = gemm_bf16_2sm_kernel<BN, A_MN, B_MN, kSgd, kMc, kSk>;
+  auto kern = gemm_bf16_2sm_kernel<BN, A_MN, B_MN, kSgd, kMc, kSk, kX>;
   constexpr int kCl = 2 * kMc * kSk;  // CTAs per cluster
   // per device: the attribute lives in each context.  Atomic: a newcomer's replica is
   // prepared on a side thread while the step thread launches on the other devices.
@@ -1333,8 +1378,8 @@ int gemm_plan_route(GemmPlan* p, int rows_per_owner, int me, void* const* dst, i
 }
 
 int gemm_plan_exchange(GemmPlan* p, int rows_per_owner, int me, int n, void* const* recv_dst,
-                       __nv_bfloat16* const* w_dst, uint32_t* const* ctr,
-                       const __nv_bfloat16* const* recv_src, int ld_recv, const int* order) {
+                       __nv_bfloat16* const* w_dst, const __nv_bfloat16* const* recv_src,
+                       int ld_recv, const int* order) {
   if (!p->ep.sgd || p->cg != 2 || p->bn != 128 || p->mc != 1)
     return fail(EDL_EINVAL, "gemm exchange: needs a fused-SGD CTA-pair plan (N tile 128)");
   if (Cfg2<128, true>::kSgdBufs != 1)
@@ -1343,7 +1388,6 @@ int gemm_plan_exchange(GemmPlan* p, int rows_per_owner, int me, int n, void* con
       rows_per_owner % 256 || rows_per_owner * n != p->M || p->N % 128)
     return fail(EDL_EINVAL, "gemm exchange: owner blocks must tile M in 256-row multiples");
   for (int o = 0; o < n; ++o) {
-    p->ep.x_ctr[o] = ctr[o];
     p->ep.x_recv[o] = recv_src[o];
     p->ep.x_order[o] = order[o];
     if (o == me) {
@@ -1362,13 +1406,6 @@ int gemm_plan_exchange(GemmPlan* p, int rows_per_owner, int me, int n, void* con
   p->ep.x_n = n;
   p->ep.x_ldr = ld_recv;
   return EDL_OK;
-}
-
-int gemm_plan_run_exchange(const GemmPlan& p, cudaStream_t stream, float sgd_scale,
-                           uint32_t target) {
-  GemmPlan q = p;
-  q.ep.x_target = target;
-  return gemm_plan_run(q, stream, sgd_scale);
 }
 
 // Loads and configures, on the current device, the GEMM variants a training step launches
@@ -1429,6 +1466,10 @@ int gemm_plan_run(const GemmPlan& p, cudaStream_t stream, float sgd_scale) {
   if (p.ep.sgd) {
     if (p.cg != 2 || (p.bn != 128 && p.bn != 256) || !a_mn || !b_mn)
       return fail(EDL_EINVAL, "gemm: fused SGD plans are CTA-pair, N tile 128/256, MN-major A/B");
+    if (p.ep.xchg) {
+      if (p.bn != 128 || p.mc != 1) return fail(EDL_EINVAL, "gemm: fused-exchange plan shape");
+      return launch_gemm_2sm<128, true, true, true, 1, 1, true>(p, stream, sgd_scale);
+    }
     if (p.mc == 2 && p.bn == 128) return launch_gemm_2sm<128, true, true, true, 2>(p, stream, sgd_scale);
     if (p.bn == 256) return launch_gemm_2sm<256, true, true, true, 1>(p, stream, sgd_scale);
     return launch_gemm_2sm<128, true, true, true, 1>(p, stream, sgd_scale);

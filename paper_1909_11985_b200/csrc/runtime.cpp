@@ -276,6 +276,8 @@ int Job::build_replica(Replica* r) {
     EDL_TRY(dalloc(&r->master, P_));
     EDL_TRY(dalloc(&r->W, P_));
     EDL_TRY(dalloc(&r->recv, P_));
+    // exchange mode 4 reads "0xFFFF = not arrived yet" from the receive slots
+    EDL_CUDA_TRY(cudaMemset(r->recv, 0xFF, sizeof(__nv_bfloat16) * P_));
     if (cfg_.momentum != 0.0) {
       EDL_TRY(dalloc(&r->mom, P_));
       EDL_CUDA_TRY(cudaMemset(r->mom, 0, sizeof(float) * P_));
@@ -671,18 +673,16 @@ int Job::ensure_plans(Worker* w, int64_t rows) {
       const int prow = out_[l] / n;
       void* dst[kMaxPeerMaps] = {};
       __nv_bfloat16* wd[kMaxPeerMaps] = {};
-      uint32_t* ctr[kMaxPeerMaps] = {};
       const __nv_bfloat16* src[kMaxPeerMaps] = {};
       for (int o = 0; o < n; ++o) {
         wd[o] = peers_[o].W + off_[l];
-        ctr[o] = peers_[o].flags + kXchgOffset + static_cast<size_t>(l) * kXchgMaxTiles;
         if (o == me) continue;
         const size_t slot = static_cast<size_t>(me < o ? me : me - 1);  // mine in o's recv
         dst[o] = peers_[o].recv + (slot * shard_total8(o) + seg_off8(o, l)) * 8;
         const size_t from = static_cast<size_t>(o < me ? o : o - 1);  // o's in my recv
         src[o] = r->recv + (from * shard_total8(me) + seg_off8(me, l)) * 8;
       }
-      EDL_TRY(gemm_plan_exchange(&w->wgrad_x[l], prow, me, n, dst, wd, ctr, src, in_[l], order));
+      EDL_TRY(gemm_plan_exchange(&w->wgrad_x[l], prow, me, n, dst, wd, src, in_[l], order));
     }
     w->x_plan_rows = rows;
     w->x_plan_version = version_;
@@ -778,7 +778,7 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
       if (mw) mark(slot, 5, mw, r->stream);
     } else if (overlap_mode_ == 4) {
       // dW + reduce-scatter + sharded SGD + weight all-gather in one kernel per layer
-      EDL_TRY(gemm_plan_run_exchange(w->wgrad_x[l], r->stream, step_scale_, x_expected_));
+      EDL_TRY(gemm_plan_run(w->wgrad_x[l], r->stream, step_scale_));
       if (mw) mark(slot, 5, mw, r->stream);
     } else if (overlap_mode_ == 3) {
       // dW with the reduce-scatter in its epilogue: rows owned elsewhere are stored into the
@@ -910,16 +910,14 @@ bool Job::rs_eligible() const {
 
 // Push collective: one ring member per replica, every replica's recv mapped here.
 // Mode 4 keeps whole 256-row tiles inside one owner block, plain SGD (the epilogue applies
-// the update), and a topology that has not changed since the job started (the per-tile
-// arrival counters are cumulative and a newcomer's would start at zero).
+// the update), and a topology that has not changed since the job started (every receive slot
+// must hold the "not arrived" sentinel at the start of a mini-batch, which mode 4 restores
+// after consuming; other modes leave gradients there).
 bool Job::xchg_eligible() const {
   if (!rs_eligible() || cfg_.momentum != 0.0 || version_ != 1) return false;
   const int n = static_cast<int>(peers_.size());
-  for (int l = 0; l < L_; ++l) {
+  for (int l = 0; l < L_; ++l)
     if (out_[l] % (256 * n) != 0 || in_[l] % 128 != 0) return false;
-    if (static_cast<size_t>(out_[l] / 256) * static_cast<size_t>(in_[l] / 128) > kXchgMaxTiles)
-      return false;
-  }
   return true;
 }
 
@@ -1834,7 +1832,6 @@ int Job::step(EdlStepReport* out) {
   if (mlp_ && count > 0 && overlap_env < 0 && peers_.size() > 1 && rs_eligible())
     overlap_mode_ = 3;
   if (overlap_mode_ == 4 && !xchg_eligible()) overlap_mode_ = rs_eligible() ? 3 : 0;
-  if (overlap_mode_ == 4) x_expected_ += 16u * static_cast<uint32_t>(peers_.size() - 1);
   overlap_ = overlap_mode_ != 0;
   // deferred all-gather (mode 3, EDL_AG_DEFER=1): the push collective of this mini-batch
   // overlaps the next mini-batch's forward.  Opt-in: measured on B200 the push kernel on a

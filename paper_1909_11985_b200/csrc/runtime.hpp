@@ -247,7 +247,6 @@ class Job {
   bool ag_defer_ = false;  // mode 3 + the push collective overlapped with the next forward
   bool rs_eligible() const;
   bool xchg_eligible() const;  // exchange mode 4 (fused into the weight-gradient GEMMs)
-  uint32_t x_expected_ = 0;    // arrival count every owned tile reaches this mini-batch
   bool push_eligible() const;
   uint32_t ce_epoch_ = 0;
   int host_index(const std::string& id) const;  // peers_ index of the replica hosting id
