@@ -117,6 +117,7 @@ class Job:
         dev = (C.c_int32 * len(devices))(*devices)
         _lib.check(self._L.edl_job_create(C.byref(c), _lib.cstrs(ring), dev, len(ring), C.byref(h)))
         self._h = h
+        self._devices = dict(zip(ring, devices))  # worker -> GPU (replace_straggler's default)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -145,6 +146,7 @@ class Job:
         st = C.c_int64()
         dev = (C.c_int32 * len(devices))(*devices)
         _lib.check(self._L.edl_job_scale_out(self._h, _lib.cstrs(ids), dev, len(ids), C.byref(st)))
+        self._devices.update(zip(ids, devices))
         return st.value
 
     def scale_in(self, ids, allowance_ms: float = 30000.0) -> int:
@@ -157,6 +159,7 @@ class Job:
     def schedule(self, switch_t: int, out: bool, ids, devices=None) -> None:
         ids = list(ids)
         devices = list(devices) if devices is not None else [0] * len(ids)
+        self._devices.update(zip(ids, devices))
         dev = (C.c_int32 * max(1, len(devices)))(*devices)
         _lib.check(self._L.edl_job_schedule(self._h, switch_t, 1 if out else 0, _lib.cstrs(ids),
                                             dev, len(ids)))
@@ -279,6 +282,22 @@ class Job:
         if w is None or len(self.ring()) < 2:
             return None
         return w, self.scale_in([w], allowance_ms)
+
+    def replace_straggler(self, new_id: str, device: int = None, window: int = 10,
+                          factor: float = 1.2, allowance_ms: float = 30000.0):
+        """Straggler replacement (BASELINE configs[3]): scale_in the detected straggler, keep
+        stepping to its switch, then scale_out `new_id` (on `device`, default the straggler's
+        GPU) -- two serialised scaling operations (Retry while one is
+        pending).  Returns (straggler, scale_in switch_t, scale_out switch_t or -1 = pending
+        until the newcomer is Ready) or None when there is no straggler."""
+        got = self.mitigate_straggler(window, factor, allowance_ms)
+        if got is None:
+            return None
+        w, st = got
+        dev = self._devices.get(w, 0) if device is None else device
+        while self.t <= st:
+            self.step()
+        return w, st, self.scale_out([new_id], [dev])
 
     def profile(self, min_p: int, max_p: int = None, steps: int = 20) -> list:
         """from the current parallelism (max_p) scale in one worker at a time

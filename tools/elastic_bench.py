@@ -110,13 +110,38 @@ def main():
                       "steps_call_to_switch": r.t - t0, "call_to_switch_wall_ms": prep_wall})
         out["events"].append(stats)
     if ngpu >= 4:
-        st = job.scale_in(["w02", "w03"])
+        # straggler replacement (BASELINE configs[3]) at 4 GPUs: w03 slowed by 1/3 of a
+        # mini-batch, detected after 10 slow mini-batches (1.2x the median of
+        # the four), scaled in, and replaced stop-free by w04 on its GPU
+        base = sorted(job.worker_ms("w03")[-10:])[5]
+        job.set_worker_delay("w03", 1e3 * base / 3)
+        n_slow = 0
+        while job.straggler() is None and n_slow < 40:
+            run_steps(job, 1)
+            n_slow += 1
+        t_det = job.t
+        w, st, _ = job.replace_straggler("w04", 3)
+        pre = []
+        while True:
+            r = run_steps(job, 1)[0]
+            if r.switched:
+                break
+            pre.append(r)
+        post = [r] + run_steps(job, args.settle + 1)
+        stats = switch_stats(pre[-args.settle:] + post, settle=args.settle)
+        stats.update({"kind": "straggler_replacement", "straggler": w, "replacement": "w04",
+                      "slow_minibatches_to_detection": n_slow, "scale_in_switch_t": st,
+                      "detected_t": t_det, "ring": job.ring()})
+        out["events"].append(stats)
+    if ngpu >= 4:
+        leave = ["w02", "w04"] if "w04" in job.ring() else ["w02", "w03"]
+        st = job.scale_in(leave)
         pre = []
         while job.t < st:
             pre.append(run_steps(job, 1)[0])
         post = run_steps(job, args.settle + 2)
         stats = switch_stats(pre[-args.settle:] + post, settle=args.settle)
-        stats.update({"kind": "scale_in", "ids": ["w02", "w03"]})
+        stats.update({"kind": "scale_in", "ids": leave})
         out["events"].append(stats)
     from oracle import api, restated
     ok, fe, detail = api.check_coverage(restated(), job.log_text(), args.size)
