@@ -420,22 +420,12 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
   auto tile_n = [&](int w) {
     return (w / m_tiles) * kMc + (kMc >= 2 ? static_cast<int>(pidx) : 0);
   };
-  // the unit's work sequence: tiles unit, unit + n_units, ...; with the fused exchange (kX)
-  // the tiles other replicas own come first, so every peer's share of my tiles is sent
-  // before anyone waits for it (in lock-step order the replicas would take turns waiting)
+  // the unit's work sequence: tiles unit, unit + n_units, ...  (Running the fused
+  // exchange's routed tiles first was measured slower: it separates the epilogue-heavy own
+  // tiles from the mainloop-heavy routed ones instead of overlapping them.)
   auto seq_tile = [&](int i) -> int {
-    if (!kX) {
-      const int t = unit + i * n_units;
-      return t < num_work ? t : num_work;
-    }
-    int k = 0;
-    for (int ph = 0; ph < 2; ++ph)
-      for (int t = unit; t < num_work; t += n_units) {
-        const bool own = (tile_m(t) * 256) / ep.route_rows == ep.route_me;
-        if (own != (ph == 1)) continue;
-        if (k++ == i) return t;
-      }
-    return num_work;
+    const int t = unit + i * n_units;
+    return t < num_work ? t : num_work;
   };
   // split-K: this pair's k-blocks (the host guarantees one tile per cluster)
   const int kb_begin = kSk == 2 ? static_cast<int>(pidx) * (num_kb / 2) : 0;
@@ -733,7 +723,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
             }
             fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) {
+            if (lane == 0 && !(ep.dbg & 32)) {  // EDL_GEMM_DBG=32: diagnostics only
               tma_store_2d(&pm.m[owner], buf + 2 * kEpiChunkBytes, c0, r0 - owner * ep.route_rows);
               tma_store_commit();
             }
@@ -748,7 +738,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
           // the sentinel back for the next mini-batch.
           const size_t rrow = static_cast<size_t>(r0 - ep.route_me * ep.route_rows + lane);
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < (ep.dbg & 16 ? 0 : 2); ++h) {  // EDL_GEMM_DBG=16: diagnostics
             float s[32];
 #pragma unroll 1
             for (int k = 0; k < ep.x_n; ++k) {
@@ -761,6 +751,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
                 const uint4* src =
                     reinterpret_cast<const uint4*>(ep.x_recv[r] + rrow * ep.x_ldr + c0 + 32 * h);
                 uint4 u[4];
+                const bool no_wait = (ep.dbg & 4) != 0;  // diagnostics only: EDL_GEMM_DBG=4
                 for (;;) {
 #pragma unroll
                   for (int q4 = 0; q4 < 4; ++q4)
@@ -775,7 +766,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
                     for (int e = 0; e < 4; ++e)
                       ready = ready && (wv[e] & 0xFFFFu) != 0xFFFFu && (wv[e] >> 16) != 0xFFFFu;
                   }
-                  if (ready) break;
+                  if (ready || no_wait) break;
                   __nanosleep(32);
                 }
 #pragma unroll
@@ -864,7 +855,8 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
           if (!C::kWDirect) tma_store_2d(&tmap_c, buf + 2 * kEpiChunkBytes, c0, r0);
           if (kX) {  // all-gather: the updated weights into every other replica
             for (int o = 0; o < ep.x_n; ++o)
-              if (o != ep.route_me) tma_store_2d(&pm.w[o], buf + 2 * kEpiChunkBytes, c0, r0);
+              if (o != ep.route_me && !(ep.dbg & 8))  // EDL_GEMM_DBG=8: diagnostics only
+                tma_store_2d(&pm.w[o], buf + 2 * kEpiChunkBytes, c0, r0);
           }
           tma_store_commit();
           if (NB == 1) {  // single buffer: refill it for this warp's next chunk (next tile)
