@@ -360,6 +360,11 @@ __global__ void ce_signal_kernel(CeSignal a) {
     if (r != a.me) st_release_sys(ce_flag(a.flags[r], a.kind, a.layer, a.me), a.epoch);
 }
 
+__global__ void ag_signal_kernel(AgSignal a) {
+  __threadfence_system();  // the copies before this kernel (stream order) are performed
+  for (int d = 0; d < a.n_dst; ++d) st_release_sys(ag_layer_flags(a.flags[d], a.layer) + a.me, a.epoch);
+}
+
 __global__ void ce_wait_kernel(CeWait a) {
   uint32_t* base = const_cast<uint32_t*>(a.flags);
   for (int l = a.l_lo; l < a.l_hi; ++l)
@@ -447,6 +452,45 @@ int stamp(unsigned long long* dst, cudaStream_t s) {
 int ce_signal(const CeSignal& a, cudaStream_t s) {
   if (a.n_rep <= 1) return EDL_OK;
   ce_signal_kernel<<<1, 1, 0, s>>>(a);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
+
+namespace {
+// cuStreamWriteValue32: the flag store is a stream memory operation (front end, preceded by a
+// system-wide fence after the copies), so it needs no SM.  A signal kernel would have to find
+// a free slot next to the next mini-batch's forward GEMM CTAs (PDL-resident, spinning on
+// these very flags); measured, it could starve behind them.
+using WriteValue32Fn = int (*)(void*, unsigned long long, unsigned int, unsigned int);
+WriteValue32Fn write_value32_fn() {
+  static WriteValue32Fn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    const char* e = getenv("EDL_AG_SIGNAL_KERNEL");
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (!(e && *e == '1') &&
+        cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WriteValue32Fn>(p);
+  }
+  return fn;
+}
+}  // namespace
+
+int ag_signal(const AgSignal& a, cudaStream_t s) {
+  if (a.n_dst <= 0) return EDL_OK;
+  if (WriteValue32Fn fn = write_value32_fn()) {
+    for (int d = 0; d < a.n_dst; ++d) {
+      const int rc = fn(s, reinterpret_cast<unsigned long long>(
+                              ag_layer_flags(a.flags[d], a.layer) + a.me), a.epoch, 0);
+      if (rc != 0) return fail(EDL_ECUDA, "cuStreamWriteValue32 failed (" + std::to_string(rc) + ")");
+    }
+    return EDL_OK;
+  }
+  ag_signal_kernel<<<1, 1, 0, s>>>(a);
   EDL_CUDA_TRY(cudaGetLastError());
   return EDL_OK;
 }

@@ -116,6 +116,15 @@ struct ShardUpdateArgs {
   int blocks = 0;
 };
 int ce_signal(const CeSignal& a, cudaStream_t s);
+// Copy-engine all-gather (EDL_AG_DEFER=2): after the copies of layer l of replica `me`'s
+// shard into the replicas listed here (stream order), store `epoch` into their
+// ag_layer_flags(flags[d], layer)[me] -- the word the next forward GEMM of layer l waits on.
+struct AgSignal {
+  uint32_t* flags[kCollMaxReplicas];  // the target replicas' flag buffers (peer-mapped)
+  int n_dst = 0, me = 0, layer = 0;
+  uint32_t epoch = 0;
+};
+int ag_signal(const AgSignal& a, cudaStream_t s);
 int ce_wait(const CeWait& a, cudaStream_t s);
 int shard_update(const ShardUpdateArgs& a, cudaStream_t s);
 

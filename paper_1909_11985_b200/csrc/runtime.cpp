@@ -1507,7 +1507,7 @@ int Job::reduce_and_update(uint64_t count, uint64_t t, int slot, const double** 
   if (ring_.size() > static_cast<size_t>(kCollMaxSources))
     return fail(EDL_EINVAL, "job: ring larger than the collective supports");
   Replica* prim = primary();
-  cudaEvent_t m = ag_defer_ ? nullptr : mark_begin(prim->stream);
+  cudaEvent_t m = ag_defer_ && !ag_ce_ ? nullptr : mark_begin(prim->stream);
   const uint32_t epoch = ++coll_epoch_;  // one collective per mini-batch, same on every GPU
   for (int me = 0; me < n_rep; ++me) {
     if (!peers_[me].local) continue;  // launched by its own process
@@ -1552,7 +1552,18 @@ int Job::reduce_and_update(uint64_t count, uint64_t t, int slot, const double** 
         for (const auto& id : ring_)
           if (host_index(id) == me) a.own_grad = workers_[id]->grad;
       }
-      if (ag_defer_ && a.push && a.skip_push) {
+      if (ag_ce_ && a.push && a.skip_push) {
+        // copy-engine all-gather: the push collective (full grid, after the backward) sums
+        // and updates this GPU's shard and writes its bf16 weights locally only; the copy
+        // engines then store the shard into every peer layer by layer (forward order, one
+        // stream per peer offset so several copy engines run), each layer followed by a flag
+        // store that releases the peer's next forward GEMM of that layer.  The copies use
+        // no SMs, so they run under the next mini-batch's gather and forward.
+        a.w_dst[0] = r->W;
+        a.n_dst = 1;
+        EDL_TRY(allreduce_sgd(a, r->stream));
+        EDL_TRY(launch_ag_ce(r, me, epoch));
+      } else if (ag_defer_ && a.push && a.skip_push) {
         // deferred all-gather: the push collective runs on the side stream after this
         // mini-batch's backward, concurrently with the next mini-batch's gather / forward;
         // per-layer flags release the forward GEMMs layer by layer.  A small grid (one CTA
@@ -1595,8 +1606,57 @@ int Job::reduce_and_update(uint64_t count, uint64_t t, int slot, const double** 
     }
     launches_ += 1;
   }
-  if (!ag_defer_) m = mark(slot, 4, m, prim->stream);
+  if (!ag_defer_ || ag_ce_) m = mark(slot, 4, m, prim->stream);
   (void)m;
+  return EDL_OK;
+}
+
+int Job::launch_ag_ce(Replica* r, int me, uint32_t epoch) {
+  const int n_rep = static_cast<int>(peers_.size());
+  // each peer copy in `split` chunks (EDL_AG_CE_SPLIT, default 1), chunks and peers spread
+  // over up to three streams so several copy engines run at once
+  static int split = -1;
+  if (split < 0) {
+    const char* e = getenv("EDL_AG_CE_SPLIT");
+    split = e && *e ? atoi(e) : 1;
+    split = split < 1 ? 1 : (split > 3 ? 3 : split);
+  }
+  EDL_CUDA_TRY(cudaEventRecord(r->ev_bwd, r->stream));  // the shard update is done
+  cudaStream_t ss[3] = {r->side, r->side2, r->side3};
+  const int n_s = (n_rep - 1) * split < 3 ? (n_rep - 1) * split : 3;
+  for (int s = 0; s < n_s; ++s) EDL_CUDA_TRY(cudaStreamWaitEvent(ss[s], r->ev_bwd, 0));
+  for (int l = 0; l < L_; ++l) {
+    size_t lo;
+    const size_t n8 = shard8(l, me, &lo);
+    const size_t at = off_[l] + lo * 8;
+    AgSignal sg;
+    sg.me = me;
+    sg.layer = l;
+    sg.epoch = epoch;
+    sg.flags[sg.n_dst++] = r->flags;  // my own shard is final in my W
+    int k = 0;
+    for (int j = 1; j < n_rep; ++j) {
+      const int p = (me + j) % n_rep;  // rotated: every GPU feeds a different peer at once
+      for (int c = 0; c < split; ++c, ++k) {
+        const size_t c0 = n8 * c / split, c1 = n8 * (c + 1) / split;
+        if (c1 > c0)
+          EDL_CUDA_TRY(cudaMemcpyAsync(peers_[p].W + at + c0 * 8, r->W + at + c0 * 8,
+                                       (c1 - c0) * 16, cudaMemcpyDeviceToDevice, ss[k % 3]));
+      }
+      sg.flags[sg.n_dst++] = peers_[p].flags;
+    }
+    // the flag stores follow every copy of the layer (stream memory ops, no SM)
+    cudaEvent_t evl[2] = {r->ev_rs[l], r->ev_upd[l]};
+    for (int s = 1; s < n_s; ++s) {
+      EDL_CUDA_TRY(cudaEventRecord(evl[s - 1], ss[s]));
+      EDL_CUDA_TRY(cudaStreamWaitEvent(r->side, evl[s - 1], 0));
+    }
+    EDL_TRY(ag_signal(sg, r->side));
+  }
+  // `side` ends after every copy (join_side / the next routed wgrad wait on ev_push)
+  EDL_CUDA_TRY(cudaEventRecord(r->ev_push, r->side));
+  r->ag_wait_epoch = epoch;
+  r->side_pending = true;
   return EDL_OK;
 }
 
@@ -1844,6 +1904,11 @@ int Job::step(EdlStepReport* out) {
     defer_env = e && *e ? atoi(e) : 0;
   }
   ag_defer_ = overlap_mode_ == 3 && defer_env != 0 && !cfg_.appx_recovery;
+  // EDL_AG_DEFER=2: the all-gather half on the copy engines (launch_ag_ce).  Opt-in: measured
+  // on B200 at N=2 the copies slow the forward GEMMs they overlap (GEMM time per mini-batch
+  // 0.61 -> 0.74 ms) more than they save on the push kernel (0.26 -> 0.20 ms): 1.10M vs
+  // 1.23M samples/s; splitting each copy over 2-3 copy engines was slower still
+  ag_ce_ = ag_defer_ && defer_env == 2;
   if (!ag_defer_) EDL_TRY(join_side());
   step_count_ = count;
   if (overlap_mode_ == 1) {  // same epochs on every process

@@ -244,6 +244,7 @@ class Job {
   bool overlap_ = false;
   int overlap_mode_ = 0;  // 1: side-stream collective kernels, 2: copy-engine transfers,
                           // 3: reduce-scatter fused into the wgrad GEMM epilogues
+  bool ag_ce_ = false;     // EDL_AG_DEFER=2: the deferred all-gather on the copy engines
   bool ag_defer_ = false;  // mode 3 + the push collective overlapped with the next forward
   bool rs_eligible() const;
   bool xchg_eligible() const;  // exchange mode 4 (fused into the weight-gradient GEMMs)
@@ -316,6 +317,7 @@ class Job {
   // orders every local replica's stream after its deferred push collective (no host sync):
   // before anything that reads the master / weights / loss outside the step pipeline
   int join_side();
+  int launch_ag_ce(Replica* r, int me, uint32_t epoch);  // EDL_AG_DEFER=2 copies + flags
  private:
   int broadcast_model(Replica* src, Replica* dst);
   cudaEvent_t slot_end_[kSlots] = {};

@@ -1,2 +1,4 @@
-for v in scratch/st2 scratch/st3 scratch/st4 paper_1909_11985_b200; do EDL_LIB_PATH=$PWD/$v/libedl_b200.so timeout 200 python scratch/gemm_exp.py; done > gpurun_out/gemm_exp.log 2>&1
-cat gpurun_out/gemm_exp.log
+python -m pytest tests -m gpu -x -q > gpurun_out/pt4.log 2>&1; echo rc=$? >> gpurun_out/pt4.log
+T="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29555 bench.py --gpus 4 --steps 30 --warmup 5 --no-cpu"
+$T > gpurun_out/b4.log 2>&1
+EDL_AG_DEFER=2 $T --no-nccl > gpurun_out/b4ce.log 2>&1

@@ -15,12 +15,14 @@ pytestmark = pytest.mark.gpu
 # fused collective kernel after the backward, 1 = per-layer collective kernels on a side
 # stream, 2 = per-layer copy-engine transfers + shard updates, 3 = reduce-scatter in the
 # wgrad GEMM epilogues + per-layer shard update / all-gather.  "3/defer" runs mode 3's push
-# collective on a side stream overlapping the next forward (EDL_AG_DEFER=1, per-layer flags).
+# collective on a side stream overlapping the next forward (EDL_AG_DEFER=1, per-layer flags);
+# "3/defer-ce" does the all-gather half on the copy engines under the next forward
+# (EDL_AG_DEFER=2: local shard update after the backward, per-layer peer copies + flags).
 # 4 = the whole exchange (reduce-scatter, sharded SGD, weight all-gather) inside the
 # weight-gradient GEMMs, per-tile arrival counters across GPUs.
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("overlap", ["", "0", "1", "2", "3", "3/defer", "4"])
+@pytest.mark.parametrize("overlap", ["", "0", "1", "2", "3", "3/defer", "3/defer-ce", "4"])
 def test_two_or_more_gpus_match_oracle(overlap):
     n = min(torch.cuda.device_count(), 4)
     here = os.path.dirname(os.path.abspath(__file__))
@@ -30,8 +32,8 @@ def test_two_or_more_gpus_match_oracle(overlap):
     env = dict(os.environ)
     env.pop("EDL_OVERLAP", None)
     env.pop("EDL_AG_DEFER", None)
-    if overlap.endswith("/defer"):
-        env["EDL_AG_DEFER"] = "1"
+    if "/defer" in overlap:
+        env["EDL_AG_DEFER"] = "2" if overlap.endswith("-ce") else "1"
         overlap = overlap.split("/")[0]
     if overlap:
         env["EDL_OVERLAP"] = overlap
