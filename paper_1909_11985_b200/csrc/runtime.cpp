@@ -208,8 +208,24 @@ Replica* Job::primary() const {
 // members (all their workers left) drop out of the collective.  Multi-process jobs keep the
 // static order fixed at import time.
 void Job::rebuild_peers() {
-  for (const auto& p : peers_)
-    if (!p.local) return;
+  bool multi = false;
+  for (const auto& p : peers_) multi = multi || !p.local;
+  if (multi) {
+    // one process per GPU: keep the replicas (local or imported) that still host a ring
+    // member, in their original order; their indices (shards, recv slots) follow from it
+    std::vector<PeerRep> v;
+    for (const auto& p : peers_) {
+      bool hosts = false;
+      for (const auto& id : ring_) {
+        const Worker* w = workers_.at(id).get();
+        hosts = hosts || (p.local ? !w->remote && w->rep == p.rep
+                                  : w->remote && w->host_rank == p.rank);
+      }
+      if (hosts) v.push_back(p);
+    }
+    peers_ = v;
+    return;
+  }
   std::vector<PeerRep> v;
   for (auto& [dev, r] : reps_) {
     int first = -1;
@@ -1839,8 +1855,24 @@ int Job::step(EdlStepReport* out) {
   if (slot_end_[slot]) EDL_CUDA_TRY(cudaEventSynchronize(slot_end_[slot]));
   collect_completed();
 
+  if (exited_) return fail(EDL_EINVAL, "job: this process's workers have left the ring");
   bool switched = false;
   EDL_TRY(install_due(&switched));
+  if (peers_.empty() || !peers_[rep_index()].local) {
+    // one process per GPU, scale-in: this process's members left at this switch (their
+    // leases were reclaimed above, the model was consolidated into the survivors):
+    // notify_batch_end answers Exit; no device work from here on
+    exited_ = true;
+    if (out) {
+      *out = EdlStepReport{};
+      out->t = t_;
+      out->version = version_;
+      out->ring_size = static_cast<int32_t>(ring_.size());
+      out->switched = 1;
+      out->loss = NAN;
+    }
+    return EDL_OK;
+  }
   Replica* prim = primary();
   DeviceGuard g(prim->device);
   if (cfg_.appx_recovery) EDL_TRY(take_pre_snapshot());
@@ -2021,10 +2053,12 @@ int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<
   if (ids.empty()) return fail(EDL_EINVAL, "scale: empty worker set");
   if (explicit_switch < 0 && !events_.empty())
     return fail(EDL_RETRY, "a scaling operation is in progress");
-  if (!dry_)
+  // one process per GPU: scale-in is supported (every process schedules the same event, the
+  // leavers' processes exit the job at the switch); a newcomer process is not (yet)
+  if (!dry_ && out)
     for (const auto& p : peers_)
       if (!p.local)
-        return fail(EDL_EINVAL, "scale events need a single-process job in this build");
+        return fail(EDL_EINVAL, "scale_out needs a single-process job in this build");
   auto ev = std::make_unique<Event>();
   ev->out = out;
   ev->ids = ids;

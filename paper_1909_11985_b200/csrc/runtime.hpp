@@ -244,6 +244,7 @@ class Job {
   bool overlap_ = false;
   int overlap_mode_ = 0;  // 1: side-stream collective kernels, 2: copy-engine transfers,
                           // 3: reduce-scatter fused into the wgrad GEMM epilogues
+  bool exited_ = false;    // one process per GPU: this process's members left the ring
   bool ag_ce_ = false;     // EDL_AG_DEFER=2: the deferred all-gather on the copy engines
   bool ag_defer_ = false;  // mode 3 + the push collective overlapped with the next forward
   bool rs_eligible() const;

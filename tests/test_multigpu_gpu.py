@@ -40,3 +40,22 @@ def test_two_or_more_gpus_match_oracle(overlap):
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     assert "MP-PARITY OK" in p.stdout
+
+
+# Scale-in across processes: the upper half of the ring leaves at t=4 (every process
+# schedules the event; the leavers' processes get Exit at the switch), checked against the
+# oracle driving the same event (linear job bit-exact, MLP within the static tolerances).
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+def test_multi_process_scale_in():
+    n = min(torch.cuda.device_count(), 4)
+    here = os.path.dirname(os.path.abspath(__file__))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29537",
+           os.path.join(here, "mp_scale_in_worker.py")]
+    env = dict(os.environ)
+    env.pop("EDL_OVERLAP", None)
+    env.pop("EDL_AG_DEFER", None)
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert "MP-SCALE-IN OK" in p.stdout
