@@ -243,6 +243,17 @@ void edl_job_config_default(EdlJobConfig* cfg);
 /* ring: worker ids in rank order; devices: CUDA device hosting each worker */
 int edl_job_create(const EdlJobConfig* cfg, const char* const* ring, const int32_t* devices,
                    int32_t n, EdlJob** out);
+/* One process per GPU, scale-out: a newcomer process's job.  ring: the
+ * job's current ring (all hosted by other processes); newcomers: every worker joining at
+ * switch_t (one process each); self_id (one of them) is built now on `device` while the ring
+ * keeps stepping.  The ring's processes schedule the same event with device -1
+ * (edl_job_schedule) and copy the model into the newcomers over NVLink at the switch.  rank
+ * orders this replica after the existing ones.  Handles are exchanged (edl_job_export /
+ * edl_job_import) before the switch; until then edl_job_step replays the lease protocol
+ * without device work.                                                                   */
+int edl_job_create_joining(const EdlJobConfig* cfg, const char* const* ring, int32_t n,
+                           const char* const* newcomers, int32_t n_new, const char* self_id,
+                           int32_t device, int32_t rank, int64_t switch_t, EdlJob** out);
 void edl_job_destroy(EdlJob* job);
 /* One mini-batch on every ring member with notify_batch_end folded in:
  * due topology switches are installed first.  Asynchronous: fills t/version/ring/count

@@ -145,6 +145,8 @@ def _declare(L: C.CDLL) -> None:
         "edl_ring_allreduce_f64": ([P(vp), i32, sz, i32, vp, vp], ci),
         "edl_job_config_default": ([P(EdlJobConfig)], None),
         "edl_job_create": ([P(EdlJobConfig), cpp, P(i32), i32, P(vp)], ci),
+        "edl_job_create_joining": ([P(EdlJobConfig), cpp, i32, cpp, i32, cp, i32, i32, i64, P(vp)],
+                                   ci),
         "edl_job_destroy": ([vp], None),
         "edl_job_step": ([vp, P(EdlStepReport)], ci),
         "edl_job_sync": ([vp, P(EdlStepReport)], ci),

@@ -291,6 +291,21 @@ int edl_job_create(const EdlJobConfig* cfg, const char* const* ring, const int32
     return EDL_OK;
   });
 }
+int edl_job_create_joining(const EdlJobConfig* cfg, const char* const* ring, int32_t n,
+                           const char* const* newcomers, int32_t n_new, const char* self_id,
+                           int32_t device, int32_t rank, int64_t switch_t, EdlJob** out) {
+  return guarded([&]() -> int {
+    if (!self_id) return edl::fail(EDL_EINVAL, "create_joining: no worker id");
+    std::vector<std::string> r, nc;
+    for (int32_t i = 0; i < n; ++i) r.emplace_back(ring[i]);
+    for (int32_t i = 0; i < n_new; ++i) nc.emplace_back(newcomers[i]);
+    edl::Job* j = nullptr;
+    const int rc = edl::Job::create_joining(*cfg, r, nc, self_id, device, rank, switch_t, &j);
+    if (rc != EDL_OK) return rc;
+    *out = new EdlJob{j};
+    return EDL_OK;
+  });
+}
 void edl_job_destroy(EdlJob* job) {
   if (!job) return;
   delete job->job;

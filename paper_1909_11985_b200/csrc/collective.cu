@@ -480,6 +480,22 @@ WriteValue32Fn write_value32_fn() {
 }
 }  // namespace
 
+int stream_write_u32(uint32_t* addr, uint32_t value, cudaStream_t s) {
+  static WriteValue32Fn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(EDL_ECUDA, "cuStreamWriteValue32 unavailable");
+    fn = reinterpret_cast<WriteValue32Fn>(p);
+  }
+  const int rc = fn(s, reinterpret_cast<unsigned long long>(addr), value, 0);
+  if (rc != 0) return fail(EDL_ECUDA, "cuStreamWriteValue32 failed (" + std::to_string(rc) + ")");
+  return EDL_OK;
+}
+
 int ag_signal(const AgSignal& a, cudaStream_t s) {
   if (a.n_dst <= 0) return EDL_OK;
   if (WriteValue32Fn fn = write_value32_fn()) {

@@ -21,8 +21,13 @@ constexpr size_t kCeFlagWords = 2ull * kCollMaxSegs * kCollMaxReplicas;
 // kCollMaxReplicas], then this replica's per-layer CTA completion counters [kCollMaxSegs].
 constexpr size_t kAgFlagWords = static_cast<size_t>(kCollMaxSegs) * kCollMaxReplicas + kCollMaxSegs;
 constexpr size_t kAgFlagOffset = kCollBarrierWords + kCeFlagWords;  // in words
+// scale-out across processes: source replica j of the old ring stores [2j] = its collective
+// epoch, then [2j+1] = the new topology version, into a joining replica's flags once the
+// joiner's model slice is copied (join_words)
+constexpr size_t kJoinFlagWords = 2ull * kCollMaxReplicas;
+constexpr size_t kJoinFlagOffset = kCollBarrierWords + kCeFlagWords + kAgFlagWords;
 constexpr size_t kCollFlagBytes =
-    (kCollBarrierWords + kCeFlagWords + kAgFlagWords) * sizeof(uint32_t);
+    (kCollBarrierWords + kCeFlagWords + kAgFlagWords + kJoinFlagWords) * sizeof(uint32_t);
 // this replica's flags for layer l: one word per source replica
 #ifdef __CUDACC__
 __host__ __device__
@@ -125,6 +130,9 @@ struct AgSignal {
   uint32_t epoch = 0;
 };
 int ag_signal(const AgSignal& a, cudaStream_t s);
+// Stream-ordered 32-bit store to device memory (local or peer-mapped), preceded by a
+// system-wide fence (cuStreamWriteValue32): no SM involved.
+int stream_write_u32(uint32_t* addr, uint32_t value, cudaStream_t s);
 int ce_wait(const CeWait& a, cudaStream_t s);
 int shard_update(const ShardUpdateArgs& a, cudaStream_t s);
 

@@ -22,6 +22,8 @@
 #include "runtime.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cstdio>
 #include <cmath>
 #include <cstring>
@@ -77,6 +79,66 @@ int Job::create(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
   return EDL_OK;
 }
 
+int Job::create_joining(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
+                        const std::vector<std::string>& newcomers, const std::string& self_id,
+                        int device, int rank, int64_t switch_t, Job** out) {
+  if (std::find(newcomers.begin(), newcomers.end(), self_id) == newcomers.end())
+    return fail(EDL_EINVAL, "create_joining: self_id is not one of the newcomers");
+  if (cfg.dry_run) return fail(EDL_EINVAL, "create_joining: not for dry-run jobs");
+  if (device < 0) return fail(EDL_EINVAL, "create_joining: the newcomer needs a local GPU");
+  for (const auto& id : ring)
+    if (id == self_id) return fail(EDL_EINVAL, "create_joining: already a ring member");
+  auto* j = new Job;
+  j->joining_ = true;
+  int rc = j->init(cfg, ring, std::vector<int>(ring.size(), -1));
+  Replica* r = nullptr;
+  if (rc == EDL_OK) r = j->replica_for(device, &rc);
+  auto ev = std::make_unique<Event>();
+  for (const auto& id : newcomers) {  // the other newcomers are hosted by their own processes
+    if (rc != EDL_OK) break;
+    auto w = std::make_unique<Worker>();
+    w->id = id;
+    if (id == self_id)
+      rc = j->build_worker(w.get(), r);
+    else
+      w->remote = true;
+    ev->prepared.push_back(std::move(w));
+  }
+  if (rc != EDL_OK) {
+    delete j;
+    return rc;
+  }
+  j->my_rank_ = rank;
+  PeerRep me;
+  me.rank = rank;
+  me.device = device;
+  me.local = true;
+  me.W = r->W;
+  me.master = r->master;
+  me.flags = r->flags;
+  me.recv = r->recv;
+  me.rep = r;
+  j->known_peers_.push_back(me);
+  j->peers_.clear();
+  ev->out = true;
+  ev->ids = newcomers;
+  for (const auto& id : newcomers) ev->devices.push_back(id == self_id ? device : -1);
+  ev->switch_t = switch_t;
+  j->events_.push_back(std::move(ev));
+  *out = j;
+  return EDL_OK;
+}
+
+Worker* Job::find_worker(const std::string& id) const {
+  auto it = workers_.find(id);
+  if (it != workers_.end()) return it->second.get();
+  for (const auto& ev : events_)
+    if (ev->out)
+      for (const auto& w : ev->prepared)
+        if (w && w->id == id) return w.get();
+  return nullptr;
+}
+
 int Job::init(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
               const std::vector<int>& devices) {
   cfg_ = cfg;
@@ -129,6 +191,20 @@ int Job::init(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
     lm_->enroll(ring[i]);
     workers_[ring[i]] = std::move(w);
   }
+  if (joining_) {  // create_joining adds the newcomer's replica and worker
+    ring_ = ring;
+    version_ = 1;
+    resplit();
+    if (cfg_.keep_log) {
+      LogRec r;
+      r.kind = LogRec::Topo;
+      r.t = 0;
+      r.version = version_;
+      r.ring = ring_;
+      log_.push_back(r);
+    }
+    return EDL_OK;
+  }
   if (first_local < 0) return fail(EDL_EINVAL, "job: no local worker (device >= 0) in the ring");
   my_rank_ = first_local;
   {
@@ -143,6 +219,7 @@ int Job::init(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
     me.recv = r->recv;
     me.rep = r;
     peers_.push_back(me);
+    known_peers_.push_back(me);
   }
   ring_ = ring;
   version_ = 1;
@@ -174,14 +251,18 @@ Replica* Job::replica_for(int device, int* rc) {
 
 // NVLink peer access between a new replica's GPU and every other replica's, both ways.
 int Job::enable_peers(Replica* a, const std::vector<Replica*>& also) {
-  if (dry_) return EDL_OK;
   std::vector<int> devs;
   for (auto& [dev, r] : reps_) devs.push_back(dev);
   for (Replica* o : also) devs.push_back(o->device);
+  return enable_peer_devices(a->device, devs);
+}
+
+int Job::enable_peer_devices(int a_dev, const std::vector<int>& devs) {
+  if (dry_) return EDL_OK;
   for (int dev : devs) {
-    if (dev == a->device) continue;
+    if (dev == a_dev) continue;
     for (int pass = 0; pass < 2; ++pass) {
-      const int from = pass ? dev : a->device, to = pass ? a->device : dev;
+      const int from = pass ? dev : a_dev, to = pass ? a_dev : dev;
       int can = 0;
       cudaDeviceCanAccessPeer(&can, from, to);
       if (!can) return fail(EDL_ECUDA, "GPUs " + std::to_string(from) + " and " +
@@ -209,12 +290,12 @@ Replica* Job::primary() const {
 // static order fixed at import time.
 void Job::rebuild_peers() {
   bool multi = false;
-  for (const auto& p : peers_) multi = multi || !p.local;
+  for (const auto& p : known_peers_) multi = multi || !p.local;
   if (multi) {
-    // one process per GPU: keep the replicas (local or imported) that still host a ring
-    // member, in their original order; their indices (shards, recv slots) follow from it
+    // one process per GPU: the replicas (local or imported) that host a ring member, in
+    // rank order; their indices (shards, recv slots) follow from it
     std::vector<PeerRep> v;
-    for (const auto& p : peers_) {
+    for (const auto& p : known_peers_) {
       bool hosts = false;
       for (const auto& id : ring_) {
         const Worker* w = workers_.at(id).get();
@@ -521,7 +602,12 @@ int Job::install_due(bool* switched) {
     // the fp32 master is sharded across GPUs; make every replica whole before the
     // membership (and with it the sharding) changes
     EDL_TRY(consolidate_master());
-    if (ev->out) {
+    // newcomers hosted by their own processes (scale-out across processes)
+    bool multi = !dry_ && ev->out && joining_;
+    for (const auto& w : ev->prepared) multi = multi || (!dry_ && w && w->remote);
+    if (ev->out && multi) {
+      EDL_TRY(install_out_mp(ev.get()));
+    } else if (ev->out) {
       if (ev->prep && ev->prep->joinable()) ev->prep->join();  // stall only if prep is late
       if (ev->prep_rc != EDL_OK) return ev->prep_rc;
       Replica* src = primary();  // lowest existing ring member's replica
@@ -539,6 +625,10 @@ int Job::install_due(bool* switched) {
           continue;
         }
         reps_[dst->device] = std::move(nr);
+        // GPUs that joined since this event was prepared (its preparation ran concurrently)
+        std::vector<int> all;
+        for (auto& [d, r] : reps_) all.push_back(d);
+        EDL_TRY(enable_peer_devices(dst->device, all));
       }
       // model broadcast to every replica that is not in the collective yet (new GPUs, or
       // GPUs whose members all left earlier and whose model is stale)
@@ -1818,7 +1908,14 @@ double Job::median_step_ms() const {
 int Job::step_dry(EdlStepReport* out) {
   bool switched = false;
   EDL_TRY(install_due(&switched));
-  if (cfg_.appx_recovery) EDL_TRY(take_pre_snapshot());
+  return step_host_only(switched, out);
+}
+
+// The lease protocol of one mini-batch without device work: dry-run jobs, and a newcomer
+// process replaying the ring's draws until its switch (every process holds the leader's
+// decisions, so the newcomer's lease state is the ring's when it joins).
+int Job::step_host_only(bool switched, EdlStepReport* out) {
+  if (cfg_.appx_recovery && dry_) EDL_TRY(take_pre_snapshot());
   uint64_t count = 0;
   for (size_t k = 0; k < ring_.size(); ++k) {
     Worker* w = workers_[ring_[k]].get();
@@ -1858,6 +1955,7 @@ int Job::step(EdlStepReport* out) {
   if (exited_) return fail(EDL_EINVAL, "job: this process's workers have left the ring");
   bool switched = false;
   EDL_TRY(install_due(&switched));
+  if (joining_) return step_host_only(switched, out);  // newcomer before its switch
   if (peers_.empty() || !peers_[rep_index()].local) {
     // one process per GPU, scale-in: this process's members left at this switch (their
     // leases were reclaimed above, the model was consolidated into the survivors):
@@ -2048,17 +2146,122 @@ int Job::sync(EdlStepReport* out) {
 
 // scale_out / scale_in / scripted event.  explicit_switch < 0: scheduler-facing call,
 // switch at t + max(1, ceil(T_a / T_b)) and Retry while another scaling op is pending.
+// Scale-out across processes, at the switch (after consolidate_master: every live replica
+// holds the whole model).  Sources (processes hosting a current member): copy slice j/n of
+// the fp32 master and bf16 weights into every newcomer's replica over NVLink (peer copies
+// on the job stream, so they precede this replica's next update), then store the collective
+// epoch and the new topology version into the newcomer's join words.  Newcomer: wait on the
+// host until every source's version word has arrived, adopt the epoch.  Everyone: the
+// newcomers join the ring (ascending id) and the replica list.
+int Job::install_out_mp(Event* ev) {
+  const uint64_t new_version = version_ + 1;
+  std::vector<PeerRep> joiners;  // newcomer replicas (imported, or this process's own)
+  for (const auto& w : ev->prepared)
+    for (const auto& p : known_peers_) {
+      const bool hosts = w->remote ? p.rank == w->host_rank && !p.local
+                                   : p.local && p.rep == w->rep;
+      if (!hosts) continue;
+      bool dup = false;
+      for (const auto& q : joiners) dup = dup || q.rank == p.rank;
+      if (!dup) joiners.push_back(p);
+    }
+  for (const auto& w : ev->prepared)
+    if (w->remote && !w->imported)
+      return fail(EDL_EINVAL, "scale_out: newcomer " + w->id + " has not exported its handles");
+  const int n_src = static_cast<int>(peers_.size());  // the current replicas, rank order
+  if (joining_) {
+    // this process's newcomer: its buffers are filled by the sources
+    Replica* r = reps_.begin()->second.get();
+    DeviceGuard g(r->device);
+    std::vector<uint32_t> words(kJoinFlagWords);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      EDL_CUDA_TRY(cudaMemcpy(words.data(), r->flags + kJoinFlagOffset,
+                              sizeof(uint32_t) * kJoinFlagWords, cudaMemcpyDeviceToHost));
+      bool all = true;
+      for (int j = 0; j < n_src; ++j) all = all && words[2 * j + 1] == new_version;
+      if (all) break;
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60))
+        return fail(EDL_TIMEOUT, "scale_out: the model did not arrive from the ring");
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+    coll_epoch_ = words[0];
+    for (int j = 1; j < n_src; ++j)
+      if (words[2 * j] != coll_epoch_)
+        return fail(EDL_VERSION_MISMATCH, "scale_out: sources disagree on the collective epoch");
+    joining_ = false;
+  } else {
+    const int me = rep_index();
+    Replica* r = peers_[me].rep;
+    DeviceGuard g(r->device);
+    if (mlp_) {
+      size_t lo, hi;
+      shard_range(P_ / 8, n_src, me, &lo, &hi);
+      lo *= 8;
+      hi = hi == P_ / 8 ? P_ : hi * 8;
+      for (const auto& q : joiners) {
+        if (hi > lo) {
+          EDL_CUDA_TRY(cudaMemcpyAsync(q.master + lo, r->master + lo, sizeof(float) * (hi - lo),
+                                       cudaMemcpyDeviceToDevice, r->stream));
+          EDL_CUDA_TRY(cudaMemcpyAsync(q.W + lo, r->W + lo, sizeof(__nv_bfloat16) * (hi - lo),
+                                       cudaMemcpyDeviceToDevice, r->stream));
+        }
+      }
+    }
+    for (const auto& q : joiners) {
+      EDL_TRY(stream_write_u32(q.flags + kJoinFlagOffset + 2 * me, coll_epoch_, r->stream));
+      EDL_TRY(stream_write_u32(q.flags + kJoinFlagOffset + 2 * me + 1,
+                               static_cast<uint32_t>(new_version), r->stream));
+    }
+  }
+  std::vector<size_t> order(ev->ids.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](size_t a, size_t b) { return ev->ids[a] < ev->ids[b]; });
+  for (size_t i : order) {
+    const std::string& id = ev->ids[i];
+    ring_.push_back(id);
+    lm_->enroll(id);
+    workers_[id] = std::move(ev->prepared[i]);
+  }
+  return EDL_OK;
+}
+
 int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<int>& devices,
                int64_t explicit_switch, int64_t* switch_t) {
   if (ids.empty()) return fail(EDL_EINVAL, "scale: empty worker set");
   if (explicit_switch < 0 && !events_.empty())
     return fail(EDL_RETRY, "a scaling operation is in progress");
-  // one process per GPU: scale-in is supported (every process schedules the same event, the
-  // leavers' processes exit the job at the switch); a newcomer process is not (yet)
-  if (!dry_ && out)
-    for (const auto& p : peers_)
-      if (!p.local)
-        return fail(EDL_EINVAL, "scale_out needs a single-process job in this build");
+  // one process per GPU (every process schedules the same event at an explicit switch
+  // step): scale-in -- the leavers' processes exit the job at the switch; scale-out -- the
+  // newcomers are hosted by their own processes (Job::create_joining, device -1 here)
+  bool remote_new = false;
+  for (int d : devices) remote_new = remote_new || d < 0;
+  if (!dry_ && out && remote_new) {
+    if (!mlp_) return fail(EDL_EINVAL, "scale_out across processes: MLP jobs only in this build");
+    if (explicit_switch < 0)
+      return fail(EDL_EINVAL, "scale_out across processes needs an explicit switch step");
+    if (cfg_.momentum != 0.0)
+      return fail(EDL_EINVAL, "scale_out across processes: momentum buffers are not moved");
+    for (int d : devices)
+      if (d >= 0) return fail(EDL_EINVAL, "scale_out across processes: newcomers are remote (-1)");
+    auto ev = std::make_unique<Event>();
+    ev->out = true;
+    ev->ids = ids;
+    ev->devices = devices;
+    ev->switch_t = explicit_switch;
+    for (const auto& id : ids) {
+      if (find_worker(id)) return fail(EDL_EINVAL, "scale_out: worker already in the job");
+      auto w = std::make_unique<Worker>();
+      w->id = id;
+      w->remote = true;  // its process exports the handles (import_handles before the switch)
+      ev->prepared.push_back(std::move(w));
+    }
+    if (switch_t) *switch_t = ev->switch_t;
+    auto pos = std::upper_bound(events_.begin(), events_.end(), ev->switch_t,
+                                [](int64_t s, const std::unique_ptr<Event>& e) { return s < e->switch_t; });
+    events_.insert(pos, std::move(ev));
+    return EDL_OK;
+  }
   auto ev = std::make_unique<Event>();
   ev->out = out;
   ev->ids = ids;
@@ -2083,7 +2286,12 @@ int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<
     // here while the job keeps stepping; the switch only copies the model.
     ev->prepared.resize(ids.size());
     Event* raw = ev.get();
-    ev->prep = std::make_unique<std::thread>([this, raw]() {
+    // the job's replicas now (reps_ is only read here: install_due inserts into it on the
+    // training thread while this preparation runs; GPUs that join through an earlier
+    // pending event get their peer access at that install)
+    std::map<int, Replica*> have;
+    for (auto& [d, r] : reps_) have[d] = r.get();
+    ev->prep = std::make_unique<std::thread>([this, raw, have]() {
       struct ReadyOnExit {
         std::atomic<bool>& f;
         ~ReadyOnExit() { f.store(true, std::memory_order_release); }
@@ -2092,7 +2300,7 @@ int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<
       std::map<int, Replica*> made;
       std::vector<std::unique_ptr<Replica>> fresh;
       for (int d : raw->devices) {
-        if (reps_.count(d) || made.count(d)) continue;  // reps_ changes only at install
+        if (have.count(d) || made.count(d)) continue;
         fresh.push_back(std::make_unique<Replica>());
         fresh.back()->device = d;
         made[d] = fresh.back().get();
@@ -2109,17 +2317,18 @@ int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<
           return;
         }
         // peer mappings with the job's GPUs and with this event's other newcomers
-        std::vector<Replica*> others;
-        for (size_t o = 0; o < k; ++o) others.push_back(fresh[o].get());
-        const int rc = enable_peers(fresh[k].get(), others);
+        std::vector<int> others;
+        for (const auto& [d, r] : have) others.push_back(d);
+        for (size_t o = 0; o < k; ++o) others.push_back(fresh[o]->device);
+        const int rc = enable_peer_devices(fresh[k]->device, others);
         if (rc != EDL_OK) raw->prep_rc = rc;
       }
       for (auto& f : fresh) raw->new_reps.push_back(std::move(f));
       if (raw->prep_rc != EDL_OK) return;
       for (size_t i = 0; i < raw->ids.size(); ++i) {
         const int d = raw->devices[i];
-        auto it = reps_.find(d);
-        Replica* r = it != reps_.end() ? it->second.get() : made[d];
+        auto it = have.find(d);
+        Replica* r = it != have.end() ? it->second : made[d];
         auto w = std::make_unique<Worker>();
         w->id = raw->ids[i];
         const int rc = build_worker(w.get(), r);
@@ -2301,11 +2510,16 @@ int Job::export_handles(std::vector<uint8_t>* out) const {
   EDL_TRY(w.handle(r->master));
   EDL_TRY(w.handle(r->flags));
   EDL_TRY(w.handle(r->recv));
-  uint32_t n = 0;
-  for (const auto& [id, wk] : workers_) n += wk->remote ? 0 : 1;
-  w.pod(n);
-  for (const auto& [id, wk] : workers_) {
-    if (wk->remote) continue;
+  std::vector<const Worker*> mine;  // local members + this process's scheduled newcomers
+  for (const auto& [id, wk] : workers_)
+    if (!wk->remote) mine.push_back(wk.get());
+  for (const auto& ev : events_)
+    if (ev->out)
+      for (const auto& wk : ev->prepared)
+        if (wk && !wk->remote) mine.push_back(wk.get());
+  w.pod(static_cast<uint32_t>(mine.size()));
+  for (const Worker* wk : mine) {
+    const std::string& id = wk->id;
     w.text(id);
     EDL_TRY(w.handle(wk->grad));
     EDL_TRY(w.handle(wk->g));
@@ -2345,10 +2559,9 @@ int Job::import_handles(const uint8_t* blob, size_t len) {
   const uint32_t n = rd.pod<uint32_t>();
   for (uint32_t i = 0; i < n && rd.ok; ++i) {
     const std::string id = rd.text();
-    auto it = workers_.find(id);
-    if (it == workers_.end() || !it->second->remote)
+    Worker* w = find_worker(id);  // a ring member or a scheduled newcomer
+    if (!w || !w->remote)
       return fail(EDL_UNKNOWN_WORKER, "import: " + id + " is not a remote member of this ring");
-    Worker* w = it->second.get();
     w->imported = true;
     w->host_rank = peer.rank;
     EDL_TRY(open(&p));
@@ -2359,11 +2572,12 @@ int Job::import_handles(const uint8_t* blob, size_t len) {
     w->loss = static_cast<double*>(p);
   }
   if (!rd.ok) return fail(EDL_ETRUNCATED, "import: truncated handle blob");
-  if (peers_.size() >= static_cast<size_t>(kCollMaxReplicas))
+  if (known_peers_.size() >= static_cast<size_t>(kCollMaxReplicas))
     return fail(EDL_EINVAL, "import: too many replicas");
-  peers_.push_back(peer);
-  std::sort(peers_.begin(), peers_.end(),
+  known_peers_.push_back(peer);
+  std::sort(known_peers_.begin(), known_peers_.end(),
             [](const PeerRep& a, const PeerRep& b) { return a.rank < b.rank; });
+  rebuild_peers();
   return EDL_OK;
 }
 

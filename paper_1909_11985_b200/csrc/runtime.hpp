@@ -163,6 +163,14 @@ class Job {
  public:
   static int create(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
                     const std::vector<int>& devices, Job** out);
+  // One process per GPU, scale-out: a newcomer process's job.  `ring` is the job's current
+  // ring (every member hosted by another process); worker `self_id` on `device` is built now
+  // (context, dataset, buffers -- while the ring keeps stepping) and joins at `switch_t`;
+  // `rank` orders its replica after the existing ones.  Until the switch step() replays the
+  // lease protocol only (no device work).
+  static int create_joining(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
+                            const std::vector<std::string>& newcomers, const std::string& self_id,
+                            int device, int rank, int64_t switch_t, Job** out);
   ~Job();
 
   int step(EdlStepReport* rep);
@@ -306,12 +314,21 @@ class Job {
   size_t P_ = 0;
   std::unique_ptr<LeaseManager> lm_;
   std::vector<PeerRep> peers_;  // sorted by rank; includes the local replica
+  // multi-process: every replica known (local + imported), members or not; peers_ is the
+  // subset hosting ring members
+  std::vector<PeerRep> known_peers_;
+  bool joining_ = false;  // newcomer process whose worker has not switched in yet
+  int step_host_only(bool switched, EdlStepReport* out);
+  int install_out_mp(Event* ev);
+  Worker* find_worker(const std::string& id) const;
   int my_rank_ = 0;
   std::vector<void*> ipc_mapped_;
   int rep_index() const;
   int rep_index(const Replica* r) const;
   Replica* primary() const;  // replica of the lowest-ranked local ring member
   int enable_peers(Replica* a, const std::vector<Replica*>& also = {});
+  // peer access between GPU `dev` and every GPU in `devs`, both ways (idempotent)
+  int enable_peer_devices(int dev, const std::vector<int>& devs);
   void rebuild_peers();
   int consolidate_master();  // async all-gather of the sharded fp32 master (local replicas)
  public:

@@ -119,6 +119,30 @@ class Job:
         self._h = h
         self._devices = dict(zip(ring, devices))  # worker -> GPU (replace_straggler's default)
 
+    @classmethod
+    def joining(cls, cfg: JobConfig, ring, newcomers, self_id: str, device: int, rank: int,
+                switch_t: int) -> "Job":
+        """Scale-out across processes (one process per GPU): this process's newcomer
+        `self_id` (one of `newcomers`, each hosted by its own process) on `device` joins the
+        job whose current ring is `ring` at `switch_t`.  The ring's processes schedule the
+        same event with device -1 (`schedule(switch_t, True, newcomers, [-1] * k)`); handles
+        are exchanged before the switch; until then step() replays the lease protocol
+        without device work."""
+        self = cls.__new__(cls)
+        self._L = _lib.lib()
+        self.cfg = cfg
+        ring = list(ring)
+        h = C.c_void_p()
+        c = cfg.to_c()
+        newcomers = list(newcomers)
+        _lib.check(self._L.edl_job_create_joining(C.byref(c), _lib.cstrs(ring), len(ring),
+                                                  _lib.cstrs(newcomers), len(newcomers),
+                                                  self_id.encode(), device, rank, switch_t,
+                                                  C.byref(h)))
+        self._h = h
+        self._devices = {self_id: device}
+        return self
+
     def close(self):
         if getattr(self, "_h", None):
             self._L.edl_job_destroy(self._h)

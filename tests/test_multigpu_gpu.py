@@ -59,3 +59,22 @@ def test_multi_process_scale_in():
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     assert "MP-SCALE-IN OK" in p.stdout
+
+
+# Stop-free scale-out across processes: the upper half of the ranks join at t=4 through
+# Job.joining (built while the ring trains, model copied in over NVLink at the switch),
+# checked against the oracle driving the same event.
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+def test_multi_process_scale_out():
+    n = min(torch.cuda.device_count(), 4)
+    here = os.path.dirname(os.path.abspath(__file__))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29539",
+           os.path.join(here, "mp_scale_out_worker.py")]
+    env = dict(os.environ)
+    env.pop("EDL_OVERLAP", None)
+    env.pop("EDL_AG_DEFER", None)
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert "MP-SCALE-OUT OK" in p.stdout
