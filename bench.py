@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -41,6 +42,17 @@ def flops_per_sample(w=WORKLOAD) -> float:
     kept in the algorithmic count like SURVEY.md §8(d))."""
     p = w["dim"] * w["hidden"] + (w["layers"] - 2) * w["hidden"] ** 2 + w["hidden"] * w["classes"]
     return 6.0 * p, p
+
+
+def _finite(x):
+    """JSON has no NaN/inf: an unmeasured figure is emitted as null."""
+    if isinstance(x, float) and not math.isfinite(x):
+        return None
+    if isinstance(x, dict):
+        return {k: _finite(v) for k, v in x.items()}
+    if isinstance(x, list):
+        return [_finite(v) for v in x]
+    return x
 
 
 def measured_peaks() -> dict:
@@ -304,14 +316,26 @@ def run_b200(args, rank: int, world: int) -> None:
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)"}
     else:
         tf = 2 * w["batch"] * (P // n_wgrad) / (per_launch_ms / 1e3) / 1e12
+        rs = upd.get("exchange_mode") == 3
         dominant = {"bound": "tensor", "kernel": "gemm_bf16_2sm_kernel<128,MN,MN> "
-                    "(weight gradient, bf16 out, one launch per layer)",
+                    + ("(weight gradient, reduce-scatter stored to the shard owners over NVLink "
+                       "from the epilogue, one launch per layer)" if rs else
+                       "(weight gradient, bf16 out, one launch per layer)"),
                     "achieved": tf, "peak": peak_t, "unit": "TFLOP/s", "frac": tf / peak_t,
                     "traffic": _ncu_traffic("wgrad]") if w is WORKLOAD else None,
                     "traffic_source": NCU_FULL,
                     "algorithmic_flop_per_launch": 2 * w["batch"] * (P // n_wgrad),
                     "launch_ms": per_launch_ms,
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"}
+        if rs:
+            # the epilogue stores the (N-1)/N of each layer's bf16 gradient owned by the other
+            # replicas over NVLink: that store stream, not the tensor pipe, bounds the launch
+            remote = (world - 1) / world * 2 * (P // n_wgrad)
+            dominant["nvlink_store"] = {
+                "bytes_per_launch": remote, "achieved": remote / (per_launch_ms / 1e3) / 1e9,
+                "peak": 770.0, "unit": "GB/s",
+                "frac": remote / (per_launch_ms / 1e3) / 1e9 / 770.0,
+                "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction"}
 
     # ---- e2e: every step through the public API with a D2H read of its loss
     job.reset_counters()
@@ -398,7 +422,7 @@ def run_b200(args, rank: int, world: int) -> None:
         "cpu_baseline": cpu,
     }
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(_finite(line)), flush=True)
     if dist is not None:
         dist.barrier()
     job.close()

@@ -877,8 +877,15 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
   m = mark(slot, 2, m, r->stream);
   for (int l = L_ - 1; l >= 0; --l) {
     if (l > 0) EDL_TRY(gemm_plan_run(r->dgrad[l], r->stream));
+    const bool fused_here = fused_update_ && (!overlap_ || l == 0);
+    if (!fused_here && overlap_mode_ == 3 && r->side_pending) {
+      // the previous push collective reads every replica's recv until its final barrier
+      // (waited on before the wgrad sub-phase mark so the wait is not timed as GEMM work)
+      EDL_CUDA_TRY(cudaStreamWaitEvent(r->stream, r->ev_push, 0));
+      r->side_pending = false;
+    }
     cudaEvent_t mw = prof ? mark_begin(r->stream) : nullptr;  // wgrad sub-phase
-    if (fused_update_ && (!overlap_ || l == 0)) {
+    if (fused_here) {
       // dW + sgd_step in one kernel (layer 0 ends the backward: nothing left to overlap)
       EDL_TRY(gemm_plan_run(w->wgrad_sgd[l], r->stream, step_scale_));
       if (mw) mark(slot, 5, mw, r->stream);
@@ -890,12 +897,8 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
       // dW with the reduce-scatter in its epilogue: rows owned elsewhere are stored into the
       // owner's recv over NVLink while the backward continues; the shard update + all-gather
       // run once, after the backward (the push collective with its phase A skipped)
-      if (r->side_pending) {
-        // the previous push collective reads every replica's recv until its final barrier
-        EDL_CUDA_TRY(cudaStreamWaitEvent(r->stream, r->ev_push, 0));
-        r->side_pending = false;
-      }
       EDL_TRY(gemm_plan_run(w->wgrad_rs[l], r->stream));
+      if (mw) mark(slot, 5, mw, r->stream);
     } else {
       EDL_TRY(gemm_plan_run(w->wgrad[l], r->stream));
       if (mw) mark(slot, 5, mw, r->stream);
