@@ -37,11 +37,20 @@ WIDE = dict(dim=11264, hidden=11264, classes=11264, layers=8, batch=512, size=1 
 WORKLOADS = {"mlp4096x8": WORKLOAD, "wide11264x8": WIDE}
 
 
-def flops_per_sample(w=WORKLOAD) -> float:
-    """6 * params per sample (fwd 2P + dgrad 2P + wgrad 2P; layer-0 dgrad is skipped but
-    kept in the algorithmic count like SURVEY.md §8(d))."""
-    p = w["dim"] * w["hidden"] + (w["layers"] - 2) * w["hidden"] ** 2 + w["hidden"] * w["classes"]
-    return 6.0 * p, p
+def flops_per_sample(w=WORKLOAD):
+    """GEMM FLOPs per sample of the GEMMs the step runs, and the parameter count P.
+    fwd 2P + wgrad 2P + dgrad 2(P - P_0): the layer-0 dgrad (the gradient w.r.t. the input
+    features) is never computed, so it is not counted (SURVEY.md §8(d)'s 6P counts it)."""
+    p0 = w["dim"] * w["hidden"]
+    p = p0 + (w["layers"] - 2) * w["hidden"] ** 2 + w["hidden"] * w["classes"]
+    return 6.0 * p - 2.0 * p0, p
+
+
+def fwd_dgrad_flops_per_sample(w=WORKLOAD) -> float:
+    """The tensor-bound GEMMs: 8 forward + 7 dgrad (the wgrad GEMMs carry the fused update
+    at N=1 and are timed as the dominant, HBM-bound kernel)."""
+    fl, p = flops_per_sample(w)
+    return fl - 2.0 * p
 
 
 def _finite(x):
@@ -118,11 +127,14 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_step(batch: int, steps: int, w=WORKLOAD):
-    """The CPU port of the same MLP step (oracle/mlp.py, numpy/BLAS on every host core):
-    the reference has no MLP, so its SGD semantics are restated there."""
+def cpu_mlp_port_steps(batch: int, steps: int, w=WORKLOAD):
+    """The CPU port of the same MLP step (oracle/mlp.py: torch CPU fp32 BLAS on every host
+    core, the GPU's bf16 rounding points): the reference has no MLP, so its
+    SGD semantics are restated there.  Returns per-step seconds."""
     import numpy as np
+    import torch
     from oracle.mlp import MLPOracle
+    torch.set_num_threads(os.cpu_count() or 1)
     orc = MLPOracle(w["dim"], w["hidden"], w["classes"], w["layers"], 1, 0, 0.05, 0.0)
     rng = np.random.default_rng(0)
     times = []
@@ -134,33 +146,59 @@ def cpu_reference_step(batch: int, steps: int, w=WORKLOAD):
     return times
 
 
+LINEAR = dict(size=8192, dim=4096, batch=512, eta=0.05, name="linear_ls_dim4096_b512")
+
+
+def reference_linear(budget_s: float = 6.0):
+    """The reference's own CPU path, compiled from /root/reference (oracle/_ref/libedlref.so),
+    on the linear least-squares job at dim 4096 / batch 512: per step
+    SyntheticDataset::get x 512 (dataset.cpp:36-54) + local_gradient (trainer.cpp:30-39) +
+    sgd_step (trainer.cpp:56-61) behind the reference ShardManager (datapipeline.cpp), one
+    thread (the reference runs one thread per worker; one worker here)."""
+    from oracle import api, reference
+    R = reference()
+    if R is None:
+        return {"unavailable": "oracle/_ref/libedlref.so not built (needs /root/reference)"}
+    spec = {"size": LINEAR["size"], "dim": LINEAR["dim"], "seed": 1, "noise": 0.01,
+            "sign_labels": False}
+    job = api.Job(R, spec, 0, LINEAR["eta"], 0.0, LINEAR["batch"], 7, 64, ["w00"])
+    job.step()  # warm-up
+    n, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < budget_s or n < 3:
+        job.step()
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": LINEAR["batch"] * n / dt, "unit": UNIT, "cores": 1, "kind": "reference",
+            "ms_per_step": 1e3 * dt / n, "workload": LINEAR["name"],
+            "sample": f"{n} mini-batches of the reference's linear job (SyntheticDataset dim "
+                      f"4096, batch 512, ShardManager leases, local_gradient + sgd_step), "
+                      f"compiled from /root/reference by oracle/Makefile"}
+
+
 def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
-    import numpy as np  # noqa: F401
-    # size each step's sample so the whole --warmup + --steps run stays near 2 minutes
-    probe = cpu_reference_step(16, 1)[0]
-    per_sample = probe / 16
-    budget = float(os.environ.get("EDL_REF_BUDGET_S", "120"))
-    batch = int(max(8, min(512, budget / (args.warmup + args.steps) / per_sample)))
-    batch = int(os.environ.get("EDL_REF_BATCH", batch))
-    times = cpu_reference_step(batch, args.warmup + args.steps)
+    w = WORKLOADS[args.workload]
+    times = cpu_mlp_port_steps(w["batch"], args.warmup + args.steps, w)
     timed = times[args.warmup:]
     total = sum(timed)
-    value = batch * len(timed) / total
+    value = w["batch"] * len(timed) / total
     cores = os.cpu_count()
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(timed),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic", "config": {"workload": "mlp4096x8_bf16_b512_sgd",
-                                        "parallelism": f"dp{args.gpus}"},
+        "data": "synthetic", "config": {"workload": w["name"], "global_batch": w["batch"],
+                                        "per_gpu_batch": w["batch"], "parallelism": "cpu",
+                                        "same_config": True},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{batch}-sample mini-batches of the full 4096x8 MLP step "
-                                   f"(numpy/BLAS port oracle/mlp.py; the reference has no MLP)"},
+                         "sample": f"{len(timed)} full {w['batch']}-sample mini-batches of the "
+                                   f"{w['name']} step (torch CPU fp32 BLAS port oracle/mlp.py "
+                                   f"on {cores} threads; the reference has no MLP)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_linear": reference_linear(),
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(_finite(line)), flush=True)
 
 
 def run_b200(args, rank: int, world: int) -> None:
@@ -254,11 +292,17 @@ def run_b200(args, rank: int, world: int) -> None:
 
     ph = counters["phase_ms"]
     n = max(1, counters["steps"])
+    # the phase breakdown comes from the profiled pass (events at phase boundaries break the
+    # PDL launch overlap, so its phases sum to more than the unprofiled step); every per-step
+    # figure below is that phase's SHARE of the profiled step times the unprofiled ms/step
+    prof_ms = sum(v for k, v in ph.items() if k != "wgrad") / n
+    share = (ms / args.steps) / prof_ms if prof_ms > 0 else float("nan")
     wgrad_ms = ph.get("wgrad", 0.0) / n  # the 8 weight-gradient GEMMs (sub-phase of backward)
     ph_main = {k: v for k, v in ph.items() if k != "wgrad"}
-    gemm_ms = (ph["forward"] + ph["backward"]) / n
+    fd_ms = (ph["forward"] + ph["backward"]) / n - wgrad_ms  # 8 fwd + 7 dgrad GEMMs
     upd_ms = ph["update"] / n
-    gemm_tflops = flops * w["batch"] / (gemm_ms / 1e3) / 1e12
+    fd_flops = fwd_dgrad_flops_per_sample(w) * w["batch"]
+    gemm_tflops = fd_flops / (fd_ms * share / 1e3) / 1e12
     peaks = measured_peaks()
     peak_t = peaks.get("bf16_tflops_sustained", 1354.1)
     peak_h = peaks.get("hbm_gbs", 6555.5)
@@ -277,9 +321,12 @@ def run_b200(args, rank: int, world: int) -> None:
             # the all-gather half (push collective: shard sum + SGD + weight stores) is exposed
             upd = {"bound": "nvlink", "achieved": half / (upd_ms / 1e3) / 1e9, "peak": 770.0,
                    "unit": "GB/s", "frac": half / (upd_ms / 1e3) / 1e9 / 770.0,
-                   "bytes_per_step": half, "per_step_ms": upd_ms,
+                   "bytes_per_step": half, "per_step_ms": upd_ms * share,
                    "allreduce_bus_bytes_per_step": 2 * half,
-                   "exposed_allreduce_bus_gbs": 2 * half / (upd_ms / 1e3) / 1e9,
+                   # bus bandwidth: RS + AG bytes over the time the transfers occupy (the
+                   # reduce-scatter rides in the wgrad GEMMs, the all-gather is the push)
+                   "busbw_gbs": 2 * half / ((wgrad_ms + upd_ms) / 1e3) / 1e9,
+                   "busbw_peak_gbs": 900.0,
                    "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction "
                                   "(900 GB/s NVLink 5 nominal)",
                    "kernel": "push all-gather + sharded SGD (reduce-scatter routed from the "
@@ -288,9 +335,9 @@ def run_b200(args, rank: int, world: int) -> None:
             nv = 2 * half
             upd = {"bound": "nvlink", "achieved": nv / (upd_ms / 1e3) / 1e9, "peak": 770.0,
                    "unit": "GB/s", "frac": nv / (upd_ms / 1e3) / 1e9 / 770.0,
-                   "bytes_per_step": nv, "per_step_ms": upd_ms,
+                   "bytes_per_step": nv, "per_step_ms": upd_ms * share,
                    "allreduce_bus_bytes_per_step": nv,
-                   "exposed_allreduce_bus_gbs": nv / (upd_ms / 1e3) / 1e9,
+                   "busbw_gbs": nv / (upd_ms / 1e3) / 1e9, "busbw_peak_gbs": 900.0,
                    "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction "
                                   "(900 GB/s NVLink 5 nominal)",
                    "kernel": "fused reduce-scatter + sharded SGD + all-gather over NVLink P2P"}
@@ -383,13 +430,25 @@ def run_b200(args, rank: int, world: int) -> None:
             upd["nccl_allreduce_same_bytes"] = {"unavailable": str(e)[:200]}
 
     # ---- CPU baseline (oracle port), bounded sample on this host, rank 0 at N=1 only
-    cpu = None
+    cpu = ref_lin = None
     if rank == 0 and world == 1 and not args.no_cpu and w is WORKLOAD:
-        batch = int(os.environ.get("EDL_CPU_BATCH", "64"))
-        t = cpu_reference_step(batch, 2)
-        cpu = {"value": batch / min(t), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-               "sample": f"best of 2 {batch}-sample steps of the full 4096x8 MLP "
-                         f"(numpy/BLAS, oracle/mlp.py); the reference has no MLP"}
+        steps_cpu = int(os.environ.get("EDL_CPU_STEPS", "3"))
+        t = cpu_mlp_port_steps(w["batch"], steps_cpu + 1, w)[1:]
+        cpu = {"value": w["batch"] * len(t) / sum(t), "unit": UNIT, "cores": os.cpu_count(),
+               "kind": "port",
+               "sample": f"{len(t)} full {w['batch']}-sample mini-batches of the 4096x8 MLP "
+                         f"step after one warm-up (torch CPU fp32 BLAS port oracle/mlp.py, "
+                         f"{os.cpu_count()} threads); the reference has no MLP"}
+        ref_lin = reference_linear()
+
+    # ---- the reference's own path on the GPU: the linear least-squares job at dim 4096 /
+    # batch 512 through the same job API, f64, bit-exact with the reference
+    lin = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        lin = gpu_linear_job(args.steps)
+        if ref_lin and ref_lin.get("value"):
+            lin["reference_cpu"] = ref_lin
+            lin["speedup_vs_reference"] = lin["value"] / ref_lin["value"]
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -408,26 +467,218 @@ def run_b200(args, rank: int, world: int) -> None:
                         "H2D as gather-kernel launch parameters, D2H loss"},
         "gpu_launches": launches,
         "roofline": dominant,
-        "gemm_roofline": {"bound": "tensor", "kernel": "tcgen05 GEMMs (8 fwd + 7 dgrad + 8 wgrad)",
+        "gemm_roofline": {"bound": "tensor", "kernel": "tcgen05 GEMMs (8 fwd + 7 dgrad)",
                           "achieved": gemm_tflops, "peak": peak_t, "unit": "TFLOP/s",
                           "frac": gemm_tflops / peak_t,
                           "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
-                          "per_step_ms": gemm_ms,
-                          "algorithmic_gflop_per_step": flops * w["batch"] / 1e9},
+                          "per_step_ms": fd_ms * share,
+                          "algorithmic_gflop_per_step": fd_flops / 1e9,
+                          "note": "per_step_ms = the fwd+dgrad share of the profiled pass x the "
+                                  "unprofiled ms_per_step"},
+        "step_tflops": {"achieved": flops * w["batch"] / (ms / args.steps / 1e3) / 1e12,
+                        "gflop_per_step": flops * w["batch"] / 1e9, "gemms": 23,
+                        "frac": flops * w["batch"] / (ms / args.steps / 1e3) / 1e12 / peak_t,
+                        "note": "all GEMM FLOPs of the step over the whole step time"},
         "update_roofline": upd,
-        "phase_ms_per_step": {k: v / n for k, v in ph_main.items()},
-        "wgrad_ms_per_step": wgrad_ms,
+        "phase_ms_per_step_profiled": {k: v / n for k, v in ph_main.items()},
+        "wgrad_ms_per_step_profiled": wgrad_ms,
+        "profiled_over_unprofiled": 1.0 / share,
         "loss_first_last": [losses[0], losses[-1]] if losses else None,
         "clocks": clocks,
         "cpu_baseline": cpu,
+        "linear_job": lin,
     }
+    if dist is not None:
+        dist.barrier()
+    job.close()
+    # ---- stop-free scaling stall vs stop-resume (the metric's second half, configs[2]/[3])
+    if not args.no_elastic and w is WORKLOAD:
+        line["elastic"] = (elastic_leg_single(args) if world == 1 else
+                           elastic_leg_mp(args, rank, world, local, dist))
     if rank == 0:
         print(json.dumps(_finite(line)), flush=True)
     if dist is not None:
         dist.barrier()
-    job.close()
-    if dist is not None:
         dist.destroy_process_group()
+
+
+def gpu_linear_job(steps: int) -> dict:
+    """LeastSquares job at dim 4096 / batch 512 on cuda:0 through the public job API (the f64
+    kernels that reproduce trainer.cpp bit for bit), timed with CUDA events."""
+    import torch
+    from paper_1909_11985_b200 import runtime as rt
+    cfg = rt.JobConfig(model=rt.LEAST_SQUARES, size=LINEAR["size"], dim=LINEAR["dim"], seed=1,
+                       noise=0.01, eta=LINEAR["eta"], batch=LINEAR["batch"], lease_seed=7,
+                       partitions=64, keep_log=False)
+    job = rt.Job(cfg, ["w00"], [0])
+    for _ in range(5):
+        job.step()
+    job.sync()
+    stream = torch.cuda.ExternalStream(job.stream_handle())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        job.step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    job.close()
+    return {"workload": LINEAR["name"], "value": LINEAR["batch"] * steps / (ms / 1e3),
+            "unit": UNIT, "ms_per_step": ms / steps, "dtype": "f64",
+            "note": "GPU f64 path bit-exact with the reference trainer (tests/test_job_gpu.py); "
+                    "latency-bound sequential sums, not a throughput kernel"}
+
+
+def _elastic_cfg(batch: int, world: int):
+    from paper_1909_11985_b200 import runtime as rt
+    w = WORKLOAD
+    return rt.JobConfig(model=rt.MLP, size=w["size"], dim=w["dim"], seed=1, noise=0.0,
+                        num_classes=w["classes"], layers=w["layers"], hidden=w["hidden"],
+                        eta=0.05, batch=batch, lease_seed=7, partitions=0,
+                        max_workers=max(2, world), init_seed=0, t_a_ms=500.0, keep_log=True)
+
+
+def _switch_stall(reps, settle: int = 10) -> dict:
+    """reps: per-mini-batch reports (synced each step) around one switch."""
+    k = next(i for i, r in enumerate(reps) if r.switched)
+    before = statistics.median(r.step_ms for r in reps[max(0, k - settle):k])
+    after = statistics.median(r.step_ms for r in reps[k + 2:k + 2 + settle])
+    sw = reps[k]
+    return {"switch_t": sw.t, "ring_size": sw.ring_size, "version": sw.version,
+            "step_ms_before": before, "step_ms_after": after, "switch_step_ms": sw.step_ms,
+            "stall_ms": max(0.0, sw.step_ms - after) + sw.stall_ms,
+            "stall_over_step": (max(0.0, sw.step_ms - after) + sw.stall_ms) / after}
+
+
+def elastic_leg_single(args) -> dict:
+    """N=1: stop-free scale-out 1 -> 2 workers and scale-in 2 -> 1 on cuda:0 through the
+    scheduler-facing API (newcomer prepared on a side thread, switch at Ready + k), aggregate
+    batch 512 constant; then stop-resume of the same 1 -> 2 change: checkpoint -> the job is
+    torn down -> a FRESH process (new CUDA context, library load, HBM dataset, buffers) loads
+    the checkpoint with the new ring and runs its first mini-batch."""
+    from paper_1909_11985_b200 import runtime as rt
+    settle = 12
+    job = rt.Job(_elastic_cfg(512, 1), ["w00"], [0])
+
+    def run(n):
+        out = []
+        for _ in range(n):
+            job.step()
+            out.append(job.sync())
+        return out
+
+    pre = run(settle + 3)
+    t_call = time.perf_counter()
+    job.scale_out(["w01"], [0])
+    while True:
+        r = run(1)[0]
+        if r.switched:
+            break
+        pre.append(r)
+    call_to_switch = 1e3 * (time.perf_counter() - t_call)
+    reps = pre[-settle:] + [r] + run(settle + 2)
+    out = _switch_stall(reps, settle)
+    out["call_to_switch_wall_ms"] = call_to_switch
+    st = job.scale_in(["w01"])
+    pre = run(max(0, st - job.t))
+    reps = pre[-settle:] + run(settle + 3)
+    sin = _switch_stall(reps, settle)
+    from oracle import api, restated  # checker only: the lease log's exactly-once coverage
+    ok, _, _ = api.check_coverage(restated(), job.log_text(), WORKLOAD["size"])
+    steady = sin["step_ms_after"]
+    # stop-resume: checkpoint, teardown, fresh process, restore, first mini-batch
+    import tempfile
+    fd, path = tempfile.mkstemp(suffix=".ckpt")
+    os.close(fd)
+    t0 = time.time()
+    job.save_checkpoint(path)
+    job.close()
+    r = subprocess.run([sys.executable, os.path.abspath(__file__), "--_restore", path,
+                        "--_ring", "w00,w01"], capture_output=True, text=True, timeout=600)
+    child = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    os.unlink(path)
+    sr_ms = 1e3 * (child["t_done"] - t0) - steady
+    return {"what": "stop-free scale-out 1->2 workers and scale-in 2->1 on one GPU (configs[1] "
+                    "MLP, aggregate batch 512, T_a 500 ms) vs stop-resume through a fresh "
+                    "process", "scale_out": out, "scale_in": sin,
+            "coverage_exactly_once": ok, "stop_resume_ms": sr_ms,
+            "stop_resume_parts_ms": child.get("parts_ms"),
+            "stall_ms": out["stall_ms"], "stop_resume_over_stall":
+                sr_ms / max(out["stall_ms"], 1e-3)}
+
+
+def restore_child(path: str, ring: str) -> None:
+    """--_restore: the resumed job of a stop-resume (fresh process, no torch import)."""
+    from paper_1909_11985_b200 import runtime as rt
+    t_start = time.time()
+    ids = ring.split(",")
+    job = rt.Job(_elastic_cfg(512, len(ids)), ids, [0] * len(ids))
+    t_built = time.time()
+    job.load_checkpoint(path)
+    t_loaded = time.time()
+    job.step()
+    job.sync()
+    t_done = time.time()
+    print(json.dumps({"t_done": t_done, "parts_ms": {
+        "process_start_to_job_built": 1e3 * (t_built - t_start),
+        "load_checkpoint": 1e3 * (t_loaded - t_built),
+        "first_minibatch": 1e3 * (t_done - t_loaded)}}), flush=True)
+    job.close()
+
+
+def elastic_leg_mp(args, rank: int, world: int, local: int, dist) -> dict:
+    """N>1 (one process per GPU): the lower half of the ranks train; the upper half build
+    their newcomers with Job.joining while the ring trains and switch in at S1 (the ring copies
+    the consolidated model into them over NVLink); at S2 they leave again (scale-in).  Stall =
+    switch mini-batch minus the steady mini-batch after it, max over the ring's ranks."""
+    from paper_1909_11985_b200 import runtime as rt
+    s1, s2, steps = 20, 40, 60
+    full = [f"w{r:02d}" for r in range(world)]
+    half = world // 2
+    ring0, newcomers = full[:half], full[half:]
+    cfg = _elastic_cfg(256 * world, world)
+    cfg.keep_log = False
+    if rank >= half:
+        job = rt.Job.joining(cfg, ring0, newcomers, full[rank], local, rank, s1)
+    else:
+        job = rt.Job(cfg, ring0, [local if r == rank else -1 for r in range(half)])
+        job.schedule(s1, True, newcomers, [-1] * len(newcomers))
+    job.schedule(s2, False, newcomers)
+    blobs = [None] * world
+    dist.all_gather_object(blobs, job.export_handles())
+    for r, b in enumerate(blobs):
+        if r != rank:
+            job.import_handles(b)
+    dist.barrier()
+    ms = {}
+    for _ in range(steps):
+        rep = job.step()
+        if full[rank] not in job.ring():
+            if rep.t >= s2:
+                break
+            continue
+        ms[rep.t] = job.sync().step_ms
+    allms = [None] * world
+    dist.all_gather_object(allms, ms)
+    dist.barrier()
+    job.close()
+    per_t = {}
+    for m in allms:
+        for t, v in m.items():
+            per_t[t] = max(per_t.get(t, 0.0), v)
+
+    def stall(s, lo, hi):
+        steady = statistics.median(per_t[t] for t in range(lo, hi))
+        return {"switch_t": s, "switch_step_ms": per_t[s], "step_ms_after": steady,
+                "stall_ms": max(0.0, per_t[s] - steady),
+                "stall_over_step": max(0.0, per_t[s] - steady) / steady}
+
+    out = stall(s1, s1 + 3, s2)
+    sin = stall(s2, s2 + 3, steps)
+    return {"what": f"stop-free scale-out {half}->{world} GPUs and scale-in {world}->{half} "
+                    f"across processes (configs[1] MLP, aggregate batch {256 * world})",
+            f"scale_out_{half}to{world}": out, f"scale_in_{world}to{half}": sin,
+            "stall_ms": out["stall_ms"]}
 
 
 NCU_FULL = "profiles/r01_ncu_full.md"
@@ -460,10 +711,30 @@ def main() -> None:
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="mlp4096x8",
                     help="mlp4096x8 = BASELINE configs[1] (the headline); wide11264x8 = "
                          "configs[4], the ~1B-param allreduce-bound MLP")
+    ap.add_argument("--no-elastic", action="store_true",
+                    help="skip the stop-free scaling vs stop-resume leg")
+    ap.add_argument("--_restore", help=argparse.SUPPRESS)
+    ap.add_argument("--_ring", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args._restore:
+        restore_child(args._restore, args._ring)
+        return
     args.warmup = max(args.warmup, 3)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: launch N ranks of this script (rank 0 prints the line)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

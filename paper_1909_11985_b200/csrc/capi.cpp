@@ -227,20 +227,13 @@ int edl_gather(const EdlDataset* ds, const EdlRun* runs_dev, int32_t n_runs, int
 int edl_local_gradient(int32_t kind, const double* w, const double* x, const double* y, int64_t n,
                        int32_t dim, double* grad_out, void* stream) {
   if (dim <= 0 || n < 0) return edl::fail(EDL_EINVAL, "gradient dimension mismatch");
-  double* ws = nullptr;
-  if (n > 0) EDL_CUDA_TRY(cudaMallocAsync(&ws, sizeof(double) * n, S(stream)));
-  int rc = edl::linear_local_gradient(kind, w, x, y, n, dim, grad_out, ws, S(stream));
-  if (ws) cudaFreeAsync(ws, S(stream));
-  return rc;
+  // no workspace: one fused launch, nothing allocated on the call path
+  return edl::linear_local_gradient(kind, w, x, y, n, dim, grad_out, nullptr, S(stream));
 }
 int edl_batch_loss(int32_t kind, const double* w, const double* x, const double* y, int64_t n,
                    int32_t dim, double* loss_out, void* stream) {
   if (dim <= 0 || n < 0) return edl::fail(EDL_EINVAL, "loss dimension mismatch");
-  double* ws = nullptr;
-  if (n > 0) EDL_CUDA_TRY(cudaMallocAsync(&ws, sizeof(double) * n, S(stream)));
-  int rc = edl::linear_batch_loss(kind, w, x, y, n, dim, loss_out, ws, S(stream));
-  if (ws) cudaFreeAsync(ws, S(stream));
-  return rc;
+  return edl::linear_batch_loss(kind, w, x, y, n, dim, loss_out, nullptr, S(stream));
 }
 int edl_sgd_step(double* w, const double* g, int64_t count, double eta, int32_t dim,
                  void* stream) {

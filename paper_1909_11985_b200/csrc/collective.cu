@@ -344,6 +344,11 @@ __global__ void __launch_bounds__(256) master_allgather_kernel(CollArgs a) {
       const float4 v = src[i];
       for (int d = 0; d < a.n_dst; ++d)
         if (d != a.me) reinterpret_cast<float4*>(a.m_dst[d])[i] = v;
+      if (a.mom) {  // the momentum shard is as current as the master shard, and only there
+        const float4 u = reinterpret_cast<const float4*>(a.mom)[i];
+        for (int d = 0; d < a.n_dst; ++d)
+          if (d != a.me) reinterpret_cast<float4*>(a.v_dst[d])[i] = u;
+      }
     }
   }
   cross_replica_barrier(a, 1);

@@ -41,6 +41,7 @@ struct CollArgs {
   int n_src = 0;
   __nv_bfloat16* w_dst[kCollMaxReplicas];  // bf16 working weights of every replica
   float* m_dst[kCollMaxReplicas];          // fp32 masters of every replica (all-gather)
+  float* v_dst[kCollMaxReplicas];          // momentum buffers of every replica (all-gather)
   int n_dst = 0;
   uint32_t* flags[kCollMaxReplicas];  // flag buffers of every replica (peer-mapped)
   int me = 0, n_rep = 1;
@@ -145,7 +146,8 @@ int spin(uint64_t ns, cudaStream_t s);
 int allreduce_sgd(const CollArgs& a, cudaStream_t s);
 int replica_barrier(const CollArgs& a, cudaStream_t s);
 int linear_allreduce_sgd(const LinearCollArgs& a, cudaStream_t s);
-// Every replica copies its master shard into every peer's master (checkpoint / scale events).
+// Every replica copies its master shard (and, with a.mom set, its momentum shard) into every
+// peer's master / momentum (checkpoint / scale events).
 int master_allgather(const CollArgs& a, cudaStream_t s);
 void shard_range(size_t n8, int n_rep, int r, size_t* lo, size_t* hi);
 

@@ -752,6 +752,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
                     reinterpret_cast<const uint4*>(ep.x_recv[r] + rrow * ep.x_ldr + c0 + 32 * h);
                 uint4 u[4];
                 const bool no_wait = (ep.dbg & 4) != 0;  // diagnostics only: EDL_GEMM_DBG=4
+                const uint64_t t_wait = globaltimer_ns();
                 for (;;) {
 #pragma unroll
                   for (int q4 = 0; q4 < 4; ++q4)
@@ -767,6 +768,8 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
                       ready = ready && (wv[e] & 0xFFFFu) != 0xFFFFu && (wv[e] >> 16) != 0xFFFFu;
                   }
                   if (ready || no_wait) break;
+                  // a peer died before storing its chunk: fail the launch, don't hang the GPU
+                  if (globaltimer_ns() - t_wait > 5000000000ull) __trap();
                   __nanosleep(32);
                 }
 #pragma unroll

@@ -90,6 +90,70 @@ __global__ void sgd_kernel(double* __restrict__ w, const double* __restrict__ g,
   w[i] = __dsub_rn(w[i], __dmul_rn(sc, g[i]));
 }
 
+// Workspace-free variants for the C-ABI entry points (edl_local_gradient / edl_batch_loss:
+// no allocation on the call path).  Same operation order: per chunk of blockDim samples the
+// threads compute s_j (or the loss term) into shared memory, then the features (gradient) or
+// thread 0 (loss) fold the chunk in draw order before the next chunk.  Each block of the
+// gradient kernel owns blockDim features and recomputes the chunk's s_j.
+constexpr int kFusedThreads = 128;
+
+__device__ __forceinline__ double sample_scale(int kind, const double* __restrict__ w,
+                                               const double* __restrict__ a, double b, int dim) {
+  double z = 0.0;
+  for (int i = 0; i < dim; ++i) z = __dadd_rn(z, __dmul_rn(w[i], a[i]));
+  if (kind == EDL_MODEL_LEAST_SQUARES) return __dsub_rn(z, b);
+  const double m = __dmul_rn(-b, z);
+  return __ddiv_rn(-b, __dadd_rn(1.0, exp(-m)));
+}
+
+__global__ void __launch_bounds__(kFusedThreads)
+local_gradient_fused_kernel(int kind, const double* __restrict__ w, const double* __restrict__ x,
+                            const double* __restrict__ y, int64_t n, int dim,
+                            double* __restrict__ g) {
+  __shared__ double sc[kFusedThreads];
+  const int i = blockIdx.x * kFusedThreads + threadIdx.x;
+  double acc = 0.0;
+  for (int64_t j0 = 0; j0 < n; j0 += kFusedThreads) {
+    const int64_t j = j0 + threadIdx.x;
+    if (j < n) sc[threadIdx.x] = sample_scale(kind, w, x + j * dim, y[j], dim);
+    __syncthreads();
+    const int m = n - j0 < kFusedThreads ? static_cast<int>(n - j0) : kFusedThreads;
+    if (i < dim)
+      for (int k = 0; k < m; ++k) acc = __dadd_rn(acc, __dmul_rn(sc[k], x[(j0 + k) * dim + i]));
+    __syncthreads();
+  }
+  if (i < dim) g[i] = acc;
+  if (i == 0) g[dim] = static_cast<double>(n);
+}
+
+__global__ void __launch_bounds__(kFusedThreads)
+batch_loss_fused_kernel(int kind, const double* __restrict__ w, const double* __restrict__ x,
+                        const double* __restrict__ y, int64_t n, int dim,
+                        double* __restrict__ out) {
+  __shared__ double lv[kFusedThreads];
+  double acc = 0.0;
+  for (int64_t j0 = 0; j0 < n; j0 += kFusedThreads) {
+    const int64_t j = j0 + threadIdx.x;
+    if (j < n) {
+      const double* a = x + j * dim;
+      double z = 0.0;
+      for (int i = 0; i < dim; ++i) z = __dadd_rn(z, __dmul_rn(w[i], a[i]));
+      if (kind == EDL_MODEL_LEAST_SQUARES) {
+        const double e = __dsub_rn(z, y[j]);
+        lv[threadIdx.x] = __dmul_rn(__dmul_rn(0.5, e), e);
+      } else {
+        lv[threadIdx.x] = log1p(exp(__dmul_rn(-y[j], z)));
+      }
+    }
+    __syncthreads();
+    const int m = n - j0 < kFusedThreads ? static_cast<int>(n - j0) : kFusedThreads;
+    if (threadIdx.x == 0)
+      for (int k = 0; k < m; ++k) acc = __dadd_rn(acc, lv[k]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = acc;
+}
+
 struct PtrArray {
   const double* p[64];
 };
@@ -117,6 +181,12 @@ __global__ void ordered_sum_kernel(PtrArray in, int n, double* __restrict__ out)
 
 int linear_local_gradient(int kind, const double* w, const double* x, const double* y, int64_t n,
                           int dim, double* grad_out, double* scale_ws, cudaStream_t s) {
+  if (!scale_ws) {  // C-ABI call: no workspace, one fused launch
+    local_gradient_fused_kernel<<<(dim + kFusedThreads - 1) / kFusedThreads, kFusedThreads, 0,
+                                  s>>>(kind, w, x, y, n, dim, grad_out);
+    EDL_CUDA_TRY(cudaGetLastError());
+    return EDL_OK;
+  }
   if (n > 0) {
     sample_scale_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(kind, w, x, y, n,
                                                                                dim, scale_ws);
@@ -128,6 +198,11 @@ int linear_local_gradient(int kind, const double* w, const double* x, const doub
 
 int linear_batch_loss(int kind, const double* w, const double* x, const double* y, int64_t n,
                       int dim, double* loss_out, double* ws, cudaStream_t s) {
+  if (!ws) {  // C-ABI call: no workspace, one launch
+    batch_loss_fused_kernel<<<1, kFusedThreads, 0, s>>>(kind, w, x, y, n, dim, loss_out);
+    EDL_CUDA_TRY(cudaGetLastError());
+    return EDL_OK;
+  }
   if (n > 0)
     sample_loss_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(kind, w, x, y, n,
                                                                               dim, ws);

@@ -117,6 +117,7 @@ int Job::create_joining(const EdlJobConfig& cfg, const std::vector<std::string>&
   me.master = r->master;
   me.flags = r->flags;
   me.recv = r->recv;
+  me.mom = r->mom;
   me.rep = r;
   j->known_peers_.push_back(me);
   j->peers_.clear();
@@ -217,6 +218,7 @@ int Job::init(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
     me.master = r->master;
     me.flags = r->flags;
     me.recv = r->recv;
+    me.mom = r->mom;
     me.rep = r;
     peers_.push_back(me);
     known_peers_.push_back(me);
@@ -323,6 +325,7 @@ void Job::rebuild_peers() {
     p.master = r->master;
     p.flags = r->flags;
     p.recv = r->recv;
+    p.mom = r->mom;
     p.rep = r.get();
     v.push_back(p);
   }
@@ -1228,8 +1231,28 @@ int Job::load_checkpoint(const std::string& path) {
     return fail(EDL_SHAPE_MISMATCH, "checkpoint: model / size / batch differ from the job");
   const size_t esz = mlp_ ? sizeof(float) : sizeof(double);
   if (!dry_ && plen != esz * P_) return fail(EDL_SHAPE_MISMATCH, "checkpoint: parameter bytes");
+  if (mlen != 0 && mlen != sizeof(float) * P_)
+    return fail(EDL_SHAPE_MISMATCH, "checkpoint: momentum bytes");
+  // pipeline: lease state as checkpointed, parsed into a copy first so a rejected or
+  // truncated payload leaves the job untouched; the checkpointed members' in-flight shards go
+  // back to the reclaimed queue at their offsets (their cursors are gone), leavers retire
+  auto lm = std::make_unique<LeaseManager>(*lm_);
+  LeaseStatus ls;
+  try {
+    ls = lm->restore(reinterpret_cast<const uint8_t*>(b.data()) + lease_at, llen);
+  } catch (const std::exception&) {
+    return fail(EDL_ETRUNCATED, "checkpoint: truncated lease state");
+  }
+  if (ls != LeaseStatus::Ok) return fail(EDL_SHAPE_MISMATCH, "checkpoint: lease state rejected");
+  for (const auto& id : ring) {
+    lm->reclaim(id);
+    if (std::find(ring_.begin(), ring_.end(), id) == ring_.end()) lm->retire(id);
+  }
+  for (const auto& id : ring_)
+    if (std::find(ring.begin(), ring.end(), id) == ring.end()) lm->enroll(id);
+  // everything validated: parameters (every replica; MLP bf16 weights re-derived from the
+  // master), momentum, lease state and t_cur change together
   EDL_TRY(sync(nullptr));
-  // parameters (every replica; MLP bf16 weights re-derived from the master)
   if (!dry_) {
     EDL_TRY(set_params(b.data() + params_at, plen));
     for (auto& [dev, r] : reps_) {
@@ -1241,16 +1264,7 @@ int Job::load_checkpoint(const std::string& path) {
         EDL_CUDA_TRY(cudaMemset(r->mom, 0, sizeof(float) * P_));
     }
   }
-  // pipeline: lease state as checkpointed; the checkpointed members' in-flight shards go
-  // back to the reclaimed queue at their offsets (their cursors are gone), leavers retire
-  const LeaseStatus ls = lm_->restore(reinterpret_cast<const uint8_t*>(b.data()) + lease_at, llen);
-  if (ls != LeaseStatus::Ok) return fail(EDL_SHAPE_MISMATCH, "checkpoint: lease state rejected");
-  for (const auto& id : ring) {
-    lm_->reclaim(id);
-    if (std::find(ring_.begin(), ring_.end(), id) == ring_.end()) lm_->retire(id);
-  }
-  for (const auto& id : ring_)
-    if (std::find(ring.begin(), ring.end(), id) == ring.end()) lm_->enroll(id);
+  lm_ = std::move(lm);
   for (auto& [id, w] : workers_) w->cur = Cursor{};
   t_ = t;
   version_ = std::max(version_, version) + 1;
@@ -1794,6 +1808,7 @@ int Job::consolidate_master() {
     CollArgs a;
     for (const auto& p : peers_) {
       a.m_dst[a.n_dst] = p.master;
+      a.v_dst[a.n_dst] = p.mom;
       a.flags[a.n_dst] = p.flags;
       ++a.n_dst;
     }
@@ -1802,6 +1817,7 @@ int Job::consolidate_master() {
     a.epoch = epoch;
     own_segments(me, n_rep, &a);
     a.master = r->master;
+    a.mom = r->mom;  // each replica's momentum is current only on its own shard, too
     EDL_TRY(master_allgather(a, r->stream));
   }
   return EDL_OK;
@@ -2208,6 +2224,11 @@ int Job::install_out_mp(Event* ev) {
                                        cudaMemcpyDeviceToDevice, r->stream));
           EDL_CUDA_TRY(cudaMemcpyAsync(q.W + lo, r->W + lo, sizeof(__nv_bfloat16) * (hi - lo),
                                        cudaMemcpyDeviceToDevice, r->stream));
+          if (r->mom) {
+            if (!q.mom) return fail(EDL_EINVAL, "scale_out: newcomer has no momentum buffer");
+            EDL_CUDA_TRY(cudaMemcpyAsync(q.mom + lo, r->mom + lo, sizeof(float) * (hi - lo),
+                                         cudaMemcpyDeviceToDevice, r->stream));
+          }
         }
       }
     }
@@ -2243,8 +2264,6 @@ int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<
     if (!mlp_) return fail(EDL_EINVAL, "scale_out across processes: MLP jobs only in this build");
     if (explicit_switch < 0)
       return fail(EDL_EINVAL, "scale_out across processes needs an explicit switch step");
-    if (cfg_.momentum != 0.0)
-      return fail(EDL_EINVAL, "scale_out across processes: momentum buffers are not moved");
     for (int d : devices)
       if (d >= 0) return fail(EDL_EINVAL, "scale_out across processes: newcomers are remote (-1)");
     auto ev = std::make_unique<Event>();
@@ -2513,6 +2532,7 @@ int Job::export_handles(std::vector<uint8_t>* out) const {
   EDL_TRY(w.handle(r->master));
   EDL_TRY(w.handle(r->flags));
   EDL_TRY(w.handle(r->recv));
+  EDL_TRY(w.handle(r->mom));
   std::vector<const Worker*> mine;  // local members + this process's scheduled newcomers
   for (const auto& [id, wk] : workers_)
     if (!wk->remote) mine.push_back(wk.get());
@@ -2539,6 +2559,14 @@ int Job::import_handles(const uint8_t* blob, size_t len) {
   if (rd.pod<uint32_t>() != kBlobMagic) return fail(EDL_EINVAL, "import: not an edl handle blob");
   PeerRep peer;
   peer.rank = rd.pod<int32_t>();
+  // a second copy of a known replica (or of this process's own) would raise the replica
+  // count the collective barriers wait for
+  if (rd.ok && peer.rank == my_rank_)
+    return fail(EDL_EINVAL, "import: blob of this process's own replica");
+  for (const auto& q : known_peers_)
+    if (rd.ok && q.rank == peer.rank)
+      return fail(EDL_EINVAL, "import: replica rank " + std::to_string(peer.rank) +
+                                  " already imported");
   peer.device = rd.pod<int32_t>();
   if (rd.pod<uint64_t>() != P_) return fail(EDL_SHAPE_MISMATCH, "import: model shape differs");
   auto open = [&](void** dst) -> int {
@@ -2559,6 +2587,8 @@ int Job::import_handles(const uint8_t* blob, size_t len) {
   peer.flags = static_cast<uint32_t*>(p);
   EDL_TRY(open(&p));
   peer.recv = static_cast<__nv_bfloat16*>(p);
+  EDL_TRY(open(&p));
+  peer.mom = static_cast<float*>(p);
   const uint32_t n = rd.pod<uint32_t>();
   for (uint32_t i = 0; i < n && rd.ok; ++i) {
     const std::string id = rd.text();
@@ -2597,6 +2627,7 @@ int Job::gather_master() {
     CollArgs a;
     for (const auto& p : peers_) {
       a.m_dst[a.n_dst] = p.master;
+      a.v_dst[a.n_dst] = p.mom;
       a.flags[a.n_dst] = p.flags;
       ++a.n_dst;
     }
@@ -2605,6 +2636,7 @@ int Job::gather_master() {
     a.epoch = ++coll_epoch_;
     own_segments(a.me, a.n_rep, &a);
     a.master = r->master;
+    a.mom = r->mom;
     EDL_TRY(master_allgather(a, r->stream));
   }
   for (auto& [dev, rr] : reps_) {

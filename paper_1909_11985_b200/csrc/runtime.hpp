@@ -156,6 +156,7 @@ struct PeerRep {
   float* master = nullptr;
   uint32_t* flags = nullptr;
   __nv_bfloat16* recv = nullptr;
+  float* mom = nullptr;  // momentum (momentum != 0 only)
   Replica* rep = nullptr;  // local replicas
 };
 

@@ -1,5 +1,5 @@
-"""bench.py's JSON contract on CPU: the reference arm (the numpy port of the MLP step, run on
-the host cores) prints one parseable line with the driver's keys, and unmeasured figures are
+"""bench.py's JSON contract on CPU: the reference arm (the CPU port of the MLP step at the
+bench's batch, run on the host cores, plus the compiled reference's linear job) prints one parseable line with the driver's keys, and unmeasured figures are
 emitted as null rather than NaN (json.dumps would write the non-JSON token NaN)."""
 import json
 import math
@@ -34,3 +34,14 @@ def test_reference_arm_json_line():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
     assert d["config"]["workload"] == "mlp4096x8_bf16_b512_sgd"
+    assert d["config"]["per_gpu_batch"] == 512 and d["config"]["same_config"]
+    # the reference's own compiled C++ on its linear job (kind "reference"), when built here
+    rl = d["reference_linear"]
+    assert "unavailable" in rl or (rl["kind"] == "reference" and rl["value"] > 0)
+
+
+def test_gpus_must_match_world_size():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0")
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--impl", "reference"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=120, env=env)
+    assert r.returncode == 2 and "WORLD_SIZE" in r.stderr
