@@ -2289,6 +2289,31 @@ int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<
   ev->ids = ids;
   ev->devices = devices;
   if (explicit_switch >= 0) {
+    if (explicit_switch < static_cast<int64_t>(t_))
+      return fail(EDL_EINVAL, "schedule: switch step already passed");
+    // scripted event: the membership it meets at its switch is the ring after every event
+    // installed before it (switch order, ties in scheduling order) -- it must not empty the
+    // ring nor remove a non-member / add a member
+    std::set<std::string> m(ring_.begin(), ring_.end());
+    auto apply = [&](bool o, const std::vector<std::string>& v) -> int {
+      for (const auto& id : v) {
+        if (o && m.count(id)) return fail(EDL_EINVAL, "schedule: " + id + " already a member");
+        if (!o && !m.count(id))
+          return fail(EDL_UNKNOWN_WORKER, "schedule: " + id + " not a member at its switch");
+        if (o) m.insert(id); else m.erase(id);
+      }
+      if (m.empty()) return fail(EDL_EINVAL, "schedule: no worker would remain");
+      return EDL_OK;
+    };
+    bool placed = false;
+    for (const auto& e : events_) {
+      if (!placed && e->switch_t > explicit_switch) {
+        EDL_TRY(apply(out, ids));
+        placed = true;
+      }
+      if (e->switch_t != std::numeric_limits<int64_t>::max()) EDL_TRY(apply(e->out, e->ids));
+    }
+    if (!placed) EDL_TRY(apply(out, ids));
     ev->switch_t = explicit_switch;
   } else if (out) {
     ev->await_ready = true;  // switch_t chosen when the newcomers are Ready

@@ -70,7 +70,7 @@ def main():
         pj.step()
         plan = [(wk, [i for _, i in s]) for wk, s in pj.plan()]
         ref_loss = orc.step(plan, t)
-        if t in got and abs(got[t].loss - ref_loss) > 2e-3 * abs(ref_loss):
+        if t in got and abs(got[t].loss - ref_loss) > 1e-3 * abs(ref_loss):
             failures.append(f"rank {rank}: t={t} loss {got[t].loss} vs {ref_loss}")
         if t in got and got[t].switched != (1 if t == SWITCH else 0):
             failures.append(f"rank {rank}: t={t} switched={got[t].switched}")
@@ -78,7 +78,8 @@ def main():
     wm = job.params(full[rank])
     ref = orc.flat_master()
     err = np.abs(wm - ref)
-    if err.max() > 2 ** -8 * np.abs(ref).max() or err.mean() > 1e-4 * np.abs(ref).max():
+    if err.max() > 2 ** -8 * np.abs(ref).max() or err.mean() > 1e-4 * np.abs(ref).max() \
+            or np.linalg.norm(err) > 1e-3 * np.linalg.norm(ref):
         failures.append(f"rank {rank}: params max err {err.max()} mean {err.mean()}")
     if job.log_text() != pj.log_text():
         failures.append(f"rank {rank}: assignment log differs")

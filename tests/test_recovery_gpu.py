@@ -76,21 +76,21 @@ def test_mlp_approximate_recovery_matches_oracle():
     for t in range(10):
         job.step()
         pj.step()
-        saved = [m.copy() for m in orc.master]  # boundary state of mini-batch t
+        saved = [m.clone() for m in orc.master]  # boundary state of mini-batch t
         orc.step([(wk, [i for _, i in s]) for wk, s in pj.plan()], t)
     job.sync()
     assert saved is not None
     # mini-batch 9 "failed": roll both back and redo it without w02
     job.fail(["w02"], approximate=True)
     pj.fail_approximate(["w02"])
-    orc.master = [m.copy() for m in saved]
+    orc.master = [m.clone() for m in saved]
     for t in range(9, 16):
         job.step()
         pj.step()
         ref_loss = orc.step([(wk, [i for _, i in s]) for wk, s in pj.plan()], t)
         got = job.sync()
         assert got.t == t
-        assert abs(got.loss - ref_loss) <= 2e-3 * abs(ref_loss), (t, got.loss, ref_loss)
+        assert abs(got.loss - ref_loss) <= 1e-3 * abs(ref_loss), (t, got.loss, ref_loss)
     assert job.log_text() == pj.log_text()
     w = job.params("w00")
     ref = orc.flat_master()
@@ -99,4 +99,5 @@ def test_mlp_approximate_recovery_matches_oracle():
     # element by one bf16 ulp of the largest weight and the bulk much tighter.
     err = np.abs(w - ref)
     assert err.max() <= 2 ** -8 * np.abs(ref).max()
+    assert np.linalg.norm(err) <= 1e-3 * np.linalg.norm(ref)  # north_star: 1e-3 relative
     assert err.mean() <= 1e-4 * np.abs(ref).max()
