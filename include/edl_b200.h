@@ -311,6 +311,9 @@ int edl_job_import(EdlJob* job, const uint8_t* blob, size_t len);
  * (before edl_job_params / checkpoints in multi-process jobs).                          */
 int edl_job_gather_master(EdlJob* job);
 void edl_job_set_profile(EdlJob* job, int32_t on);
+/* phase_ms[7]: device ms per phase accumulated while profiling is on -- gather, forward,
+ * loss, backward, update, and inside the backward: weight-gradient GEMMs, backward pair
+ * launches (dgrad l-1 + wgrad/SGD l) -- plus mini-batches and library kernels launched.  */
 void edl_job_counters(const EdlJob* job, double* phase_ms, uint64_t* steps, uint64_t* launches);
 void edl_job_reset_counters(EdlJob* job);
 

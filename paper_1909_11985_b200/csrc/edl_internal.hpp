@@ -92,6 +92,13 @@ int gemm_plan_run_wait(const GemmPlan& p, cudaStream_t stream, const uint32_t* f
 int gemm_plan_init_sgd(GemmPlan* p, const void* A, int lda, int a_mn, const void* B, int ldb,
                        int b_mn, float* master, __nv_bfloat16* W, int ldw, int M, int N, int K);
 int gemm_pick_bn(int M, int N, bool b_mn);
+// Backward pair (bwd_pair.cu): the dgrad plan of layer l-1 (CTA pair, N tile 128, relu'
+// mask, bf16 out) and the fused wgrad + SGD plan of layer l in one persistent launch.
+bool gemm_pair_enabled();  // EDL_BWD_PAIR (default 0: measured no faster)
+bool gemm_pair_eligible(const GemmPlan& dgrad, const GemmPlan& wgrad_sgd);
+int gemm_pair_run(const GemmPlan& dgrad, const GemmPlan& wgrad_sgd, cudaStream_t stream,
+                  float scale);
+int gemm_pair_prepare_device(int* units_out);
 // Turns a bf16-output CTA-pair plan into a reduce-scatter producer: rows owned by replica o
 // (blocks of rows_per_owner) go to dst[o] ([rows_per_owner][N], ld = N), o != me.
 int gemm_plan_route(GemmPlan* p, int rows_per_owner, int me, void* const* dst, int n_owner);

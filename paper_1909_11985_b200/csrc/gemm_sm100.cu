@@ -1415,6 +1415,7 @@ int gemm_prepare_device() {
   if (!rc) rc = launch_gemm_2sm<128, true, true, true, 1>(p, nullptr, 0.f, true);
   if (!rc) rc = launch_gemm_2sm<128, false, false, false, 1>(p, nullptr, 0.f, true);
   if (!rc) rc = launch_gemm_2sm<128, false, true, false, 1>(p, nullptr, 0.f, true);
+  if (!rc) rc = gemm_pair_prepare_device(nullptr);
   return rc;
 }
 

@@ -395,6 +395,7 @@ int Job::build_replica(Replica* r) {
     int widest = cfg_.data.dim > cfg_.hidden ? cfg_.data.dim : cfg_.hidden;
     EDL_TRY(dalloc(&r->dx[0], static_cast<size_t>(rows) * widest));
     EDL_TRY(dalloc(&r->dx[1], static_cast<size_t>(rows) * widest));
+    EDL_TRY(dalloc(&r->dx[2], static_cast<size_t>(rows) * widest));
     EDL_TRY(dalloc(&r->row_loss, static_cast<size_t>(rows)));
     EDL_CUDA_TRY(cudaMalloc(&r->xent_done, sizeof(unsigned)));
     EDL_CUDA_TRY(cudaMemset(r->xent_done, 0, sizeof(unsigned)));
@@ -465,6 +466,7 @@ void Job::free_replica(Replica* r) {
   cudaFree(r->dlog);
   cudaFree(r->dx[0]);
   cudaFree(r->dx[1]);
+  cudaFree(r->dx[2]);
   cudaFree(r->row_loss);
   cudaFree(r->xent_done);
   cudaFree(r->labels);
@@ -726,9 +728,9 @@ int Job::ensure_plans(Worker* w, int64_t rows) {
                              out_[l], static_cast<int>(rows), out_[l], in_[l], last ? 0 : 1,
                              last ? 1 : 0, nullptr, 0, 0));
       if (l > 0) {
-        const __nv_bfloat16* dy = last ? r->dlog : r->dx[(l + 1) & 1];
+        const __nv_bfloat16* dy = last ? r->dlog : r->dx[(l + 1) % 3];
         EDL_TRY(gemm_plan_init(&r->dgrad[l], dy, out_[l], 0, r->W + off_[l], in_[l], 1,
-                               r->dx[l & 1], in_[l], static_cast<int>(rows), in_[l], out_[l], 0,
+                               r->dx[l % 3], in_[l], static_cast<int>(rows), in_[l], out_[l], 0,
                                0, r->act[l], in_[l], 0));
       }
     }
@@ -738,7 +740,7 @@ int Job::ensure_plans(Worker* w, int64_t rows) {
     w->wgrad.assign(static_cast<size_t>(L_), GemmPlan{});
     for (int l = 0; l < L_; ++l) {
       const bool last = l == L_ - 1;
-      const __nv_bfloat16* dy = last ? r->dlog : r->dx[(l + 1) & 1];
+      const __nv_bfloat16* dy = last ? r->dlog : r->dx[(l + 1) % 3];
       EDL_TRY(gemm_plan_init(&w->wgrad[l], dy, out_[l], 1, r->act[l], in_[l], 1,
                              w->grad + off_[l], in_[l], out_[l], in_[l], static_cast<int>(rows),
                              0, 0, nullptr, 0, 0));
@@ -751,7 +753,7 @@ int Job::ensure_plans(Worker* w, int64_t rows) {
     w->wgrad_rs.assign(static_cast<size_t>(L_), GemmPlan{});
     for (int l = 0; l < L_; ++l) {
       const bool last = l == L_ - 1;
-      const __nv_bfloat16* dy = last ? r->dlog : r->dx[(l + 1) & 1];
+      const __nv_bfloat16* dy = last ? r->dlog : r->dx[(l + 1) % 3];
       EDL_TRY(gemm_plan_init(&w->wgrad_rs[l], dy, out_[l], 1, r->act[l], in_[l], 1,
                              w->grad + off_[l], in_[l], out_[l], in_[l], static_cast<int>(rows),
                              0, 0, nullptr, 0, 1000 + 128));
@@ -775,7 +777,7 @@ int Job::ensure_plans(Worker* w, int64_t rows) {
     for (size_t k = 0; k < ring_.size(); ++k) order[k] = host_index(ring_[k]);
     for (int l = 0; l < L_; ++l) {
       const bool last = l == L_ - 1;
-      const __nv_bfloat16* dy = last ? r->dlog : r->dx[(l + 1) & 1];
+      const __nv_bfloat16* dy = last ? r->dlog : r->dx[(l + 1) % 3];
       EDL_TRY(gemm_plan_init_sgd(&w->wgrad_x[l], dy, out_[l], 1, r->act[l], in_[l], 1,
                                  r->master + off_[l], r->W + off_[l], in_[l], out_[l], in_[l],
                                  static_cast<int>(rows)));
@@ -800,7 +802,7 @@ int Job::ensure_plans(Worker* w, int64_t rows) {
     w->wgrad_sgd.assign(static_cast<size_t>(L_), GemmPlan{});
     for (int l = 0; l < L_; ++l) {
       const bool last = l == L_ - 1;
-      const __nv_bfloat16* dy = last ? r->dlog : r->dx[(l + 1) & 1];
+      const __nv_bfloat16* dy = last ? r->dlog : r->dx[(l + 1) % 3];
       EDL_TRY(gemm_plan_init_sgd(&w->wgrad_sgd[l], dy, out_[l], 1, r->act[l], in_[l], 1,
                                  r->master + off_[l], r->W + off_[l], in_[l], out_[l], in_[l],
                                  static_cast<int>(rows)));
@@ -878,7 +880,25 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
   EDL_TRY(softmax_xent(r->logits, r->labels, static_cast<int>(rows), cfg_.num_classes, r->dlog,
                        r->row_loss, wloss, r->xent_done, r->stream));
   m = mark(slot, 2, m, r->stream);
-  for (int l = L_ - 1; l >= 0; --l) {
+  // N = 1 fused update: dgrad of layer l-1 and wgrad + SGD of layer l share one launch
+  // (bwd_pair.cu) -- the tensor-bound and the HBM-bound halves of the backward overlap
+  bool pair = fused_update_ && !overlap_ && L_ >= 3 && gemm_pair_enabled();
+  for (int l = 2; pair && l < L_; ++l)
+    pair = gemm_pair_eligible(r->dgrad[l - 1], w->wgrad_sgd[l]);
+  if (pair) {
+    EDL_TRY(gemm_plan_run(r->dgrad[L_ - 1], r->stream));
+    for (int l = L_ - 1; l >= 2; --l) {
+      cudaEvent_t mp = prof ? mark_begin(r->stream) : nullptr;
+      EDL_TRY(gemm_pair_run(r->dgrad[l - 1], w->wgrad_sgd[l], r->stream, step_scale_));
+      if (mp) mark(slot, 6, mp, r->stream);
+    }
+    for (int l = 1; l >= 0; --l) {
+      cudaEvent_t mw = prof ? mark_begin(r->stream) : nullptr;
+      EDL_TRY(gemm_plan_run(w->wgrad_sgd[l], r->stream, step_scale_));
+      if (mw) mark(slot, 5, mw, r->stream);
+    }
+  }
+  for (int l = pair ? -1 : L_ - 1; l >= 0; --l) {
     if (l > 0) EDL_TRY(gemm_plan_run(r->dgrad[l], r->stream));
     const bool fused_here = fused_update_ && (!overlap_ || l == 0);
     if (!fused_here && overlap_mode_ == 3 && r->side_pending) {
@@ -916,7 +936,9 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
   if (overlap_ && last && overlap_mode_ != 3 && overlap_mode_ != 4) EDL_TRY(finish_layer_colls(r));
   m = mark(slot, 3, m, r->stream);
   (void)m;
-  launches_ += 1 + static_cast<uint64_t>(L_) + 1 + static_cast<uint64_t>(2 * L_ - 1);
+  // gather + L fwd + softmax-CE + backward (2L - 1 GEMMs, or L - 2 of them paired)
+  launches_ += 1 + static_cast<uint64_t>(L_) + 1 +
+               static_cast<uint64_t>(pair ? L_ + 1 : 2 * L_ - 1);
   return EDL_OK;
 }
 

@@ -52,7 +52,9 @@ struct Replica {
   std::vector<__nv_bfloat16*> act;  // act[l]: input of layer l, [rows][in_l]
   float* logits = nullptr;
   __nv_bfloat16* dlog = nullptr;
-  __nv_bfloat16* dx[2] = {nullptr, nullptr};
+  // dgrad outputs, rotated by layer (dgrad l writes dx[l % 3]): the backward pair launch
+  // runs dgrad l-1 (writing dx[(l-1) % 3]) next to wgrad l (reading dx[(l+1) % 3])
+  __nv_bfloat16* dx[3] = {nullptr, nullptr, nullptr};
   float* row_loss = nullptr;
   unsigned* xent_done = nullptr;  // CTA counter of the fused softmax + loss-sum kernel
   int32_t* labels = nullptr;
@@ -215,7 +217,8 @@ class Job {
     phase_steps_ = 0;
     launches_ = 0;
   }
-  static constexpr int kPhases = 6;  // + 5: weight-gradient GEMMs (inside the backward)
+  // + 5: weight-gradient GEMMs, 6: backward pair launches (both inside the backward)
+  static constexpr int kPhases = 7;
   static constexpr int kMaxMarks = 64;
 
  private:

@@ -242,7 +242,7 @@ class Job:
         deferred push collective on the side stream); no host sync (edl_job_join)."""
         _lib.check(self._L.edl_job_join(self._h))
 
-    PHASES = ("gather", "forward", "loss", "backward", "update", "wgrad")
+    PHASES = ("gather", "forward", "loss", "backward", "update", "wgrad", "pair")
 
     def counters(self) -> dict:
         ms = (C.c_double * len(self.PHASES))()
