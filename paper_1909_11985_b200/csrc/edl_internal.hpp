@@ -45,6 +45,12 @@ struct EpiParams {
   int route_rows;
   int route_me;
   int dbg;  // trace builds only: 1 = skip the K loop, 2 = skip the epilogue work
+  // L2 prefetch of an unrelated region while this (tensor-bound) GEMM runs: the producer of
+  // every CTA pulls its 1/grid share of [l2pf, l2pf + l2pf_bytes) into L2 over its first
+  // k-blocks (the dgrad GEMM of layer l prefetches layer l's fp32 master for the fused
+  // wgrad + SGD kernel that follows: HBM is idle during the dgrad mainloop)
+  const void* l2pf;
+  size_t l2pf_bytes;
   // B operand (the layer's weights) all-gathered by the previous mini-batch's deferred push
   // collective: the producer waits until wait_flags[r] >= wait_epoch for r < wait_n (every
   // replica signalled this layer) before its first load.  nullptr: no wait.
@@ -99,6 +105,11 @@ bool gemm_pair_eligible(const GemmPlan& dgrad, const GemmPlan& wgrad_sgd);
 int gemm_pair_run(const GemmPlan& dgrad, const GemmPlan& wgrad_sgd, cudaStream_t stream,
                   float scale);
 int gemm_pair_prepare_device(int* units_out);
+// Fused wgrad + SGD with the B panel resident in shared memory (wgrad_sgd.cu): used by
+// gemm_plan_run for fused-SGD plans with K <= 512 when EDL_SGD_BRES=1 (measured slower).
+bool wgrad_sgd_bres_eligible(const GemmPlan& p);
+int wgrad_sgd_bres_run(const GemmPlan& p, cudaStream_t stream, float scale);
+int wgrad_sgd_bres_prepare_device(int* units_out);
 // Turns a bf16-output CTA-pair plan into a reduce-scatter producer: rows owned by replica o
 // (blocks of rows_per_owner) go to dst[o] ([rows_per_owner][N], ld = N), o != me.
 int gemm_plan_route(GemmPlan* p, int rows_per_owner, int me, void* const* dst, int n_owner);

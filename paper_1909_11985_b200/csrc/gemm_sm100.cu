@@ -479,6 +479,18 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
       if (lane == 0) wait_flags_acquire(ep.wait_flags, ep.wait_n, ep.wait_epoch);
       __syncwarp();
     }
+    // ep.l2pf: this CTA's share of the prefetch region, 64 KB per k-block from the first
+    size_t pf_lo = 0, pf_hi = 0, pf_step = 65536;
+    if (ep.l2pf_bytes) {
+      const size_t share = ((ep.l2pf_bytes / gridDim.x) + 15) & ~static_cast<size_t>(15);
+      pf_lo = share * blockIdx.x;
+      pf_hi = pf_lo + share < ep.l2pf_bytes ? pf_lo + share : ep.l2pf_bytes;
+      // spread evenly over this CTA's k-blocks
+      int my_kb = 0;
+      for (int wi = 0, w = seq_tile(0); w < num_work; w = seq_tile(++wi)) my_kb += kb_end - kb_begin;
+      if (my_kb > 0) pf_step = ((share / my_kb) + 1023) & ~static_cast<size_t>(1023);
+      if (pf_step == 0) pf_step = 1024;
+    }
     for (int wi = 0, w = seq_tile(0); w < num_work; w = seq_tile(++wi)) {
       const int m0 = tile_m(w) * 256 + static_cast<int>(pr) * 128;
       const int n0 = tile_n(w) * BN + static_cast<int>(pr) * C::kHalfN;
@@ -486,6 +498,13 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
         TRACE_T0(t_w);
         mbar_wait(&empty_bar[stage], phase ^ 1);
         TRACE_ADD(3, t_w);
+        if (pf_lo < pf_hi) {  // warp-uniform: every lane advances pf_lo
+          const size_t n = pf_hi - pf_lo < pf_step ? pf_hi - pf_lo : pf_step;
+          if (elect_one())
+            bulk_prefetch_l2(static_cast<const uint8_t*>(ep.l2pf) + pf_lo, static_cast<uint32_t>(n));
+          __syncwarp();
+          pf_lo += n;
+        }
         if (elect_one()) {
           uint8_t* sa = smem + stage * C::kStageBytes;
           uint8_t* sb = sa + C::kABytes;
@@ -1416,6 +1435,7 @@ int gemm_prepare_device() {
   if (!rc) rc = launch_gemm_2sm<128, false, false, false, 1>(p, nullptr, 0.f, true);
   if (!rc) rc = launch_gemm_2sm<128, false, true, false, 1>(p, nullptr, 0.f, true);
   if (!rc) rc = gemm_pair_prepare_device(nullptr);
+  if (!rc) rc = wgrad_sgd_bres_prepare_device(nullptr);
   return rc;
 }
 
@@ -1462,6 +1482,9 @@ int gemm_plan_run(const GemmPlan& p, cudaStream_t stream, float sgd_scale) {
   if (p.ep.sgd) {
     if (p.cg != 2 || (p.bn != 128 && p.bn != 256) || !a_mn || !b_mn)
       return fail(EDL_EINVAL, "gemm: fused SGD plans are CTA-pair, N tile 128/256, MN-major A/B");
+    // opt-in (EDL_SGD_BRES=1): the B-resident kernel (wgrad_sgd.cu) streams ~1/3 fewer
+    // operand bytes per parameter; measured slower, the epilogue bounds this GEMM
+    if (wgrad_sgd_bres_eligible(p)) return wgrad_sgd_bres_run(p, stream, sgd_scale);
     if (p.ep.xchg) {
       if (p.bn != 128 || p.mc != 1) return fail(EDL_EINVAL, "gemm: fused-exchange plan shape");
       return launch_gemm_2sm<128, true, true, true, 1, 1, true>(p, stream, sgd_scale);

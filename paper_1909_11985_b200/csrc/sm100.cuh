@@ -87,6 +87,13 @@ __device__ __forceinline__ void tma_prefetch_2d(const void* tmap, int c0, int c1
                : "memory");
 }
 
+// L2 prefetch of a contiguous global range (bytes: multiple of 16): no smem, no barrier.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)),
+               "r"(bytes)
+               : "memory");
+}
+
 // Spin until flags[r] >= epoch (wrapping compare) for r < n, system-scope acquire, then order
 // the async proxy (TMA loads) after it: the flags release peer / local generic-proxy stores.
 __device__ __forceinline__ void wait_flags_acquire(const uint32_t* flags, int n, uint32_t epoch) {
