@@ -307,6 +307,13 @@ int edl_job_join(EdlJob* job);
  * The per-step allreduce + update then runs as one kernel per GPU over NVLink peer memory. */
 int edl_job_export(const EdlJob* job, uint8_t* buf, size_t cap, size_t* len);
 int edl_job_import(EdlJob* job, const uint8_t* blob, size_t len);
+/* Scheduler-facing scale-out across processes (the newcomer receives the
+ * pending topology): the leader exports its host protocol state (t_cur, version, ring,
+ * ShardManager snapshot, shard cursors) at the boundary where it fixes switch_t
+ * (EDL_RETRY while another scaling operation is pending); a newcomer process created with
+ * edl_job_create_joining adopts it before its first step and replays only from there.   */
+int edl_job_export_state(const EdlJob* job, uint8_t* buf, size_t cap, size_t* len);
+int edl_job_adopt_state(EdlJob* job, const uint8_t* blob, size_t len, int64_t switch_t);
 /* Collective: all-gather the sharded fp32 master so every replica holds all of it
  * (before edl_job_params / checkpoints in multi-process jobs).                          */
 int edl_job_gather_master(EdlJob* job);

@@ -168,6 +168,8 @@ def _declare(L: C.CDLL) -> None:
         "edl_job_reset_counters": ([vp], None),
         "edl_job_export": ([vp, vp, sz, P(sz)], ci),
         "edl_job_import": ([vp, vp, sz], ci),
+        "edl_job_export_state": ([vp, vp, sz, P(sz)], ci),
+        "edl_job_adopt_state": ([vp, vp, sz, i64], ci),
         "edl_job_gather_master": ([vp], ci),
         "edl_job_set_params": ([vp, vp, sz], ci),
         "edl_gemm_wgrad_sgd": ([vp, i32, vp, i32, vp, vp, i32, i32, i32, i32, C.c_float, vp], ci),

@@ -380,6 +380,19 @@ int edl_job_export(const EdlJob* job, uint8_t* buf, size_t cap, size_t* len) {
     return EDL_OK;
   });
 }
+int edl_job_export_state(const EdlJob* job, uint8_t* buf, size_t cap, size_t* len) {
+  return guarded([&]() -> int {
+    std::vector<uint8_t> b;
+    const int rc = job->job->export_host_state(&b);
+    if (rc != EDL_OK) return rc;
+    if (len) *len = b.size();
+    if (buf) std::memcpy(buf, b.data(), b.size() < cap ? b.size() : cap);
+    return EDL_OK;
+  });
+}
+int edl_job_adopt_state(EdlJob* job, const uint8_t* blob, size_t len, int64_t switch_t) {
+  return guarded([&]() -> int { return job->job->adopt_host_state(blob, len, switch_t); });
+}
 int edl_job_import(EdlJob* job, const uint8_t* blob, size_t len) {
   return guarded([&]() -> int { return job->job->import_handles(blob, len); });
 }

@@ -2585,6 +2585,88 @@ struct BlobR {
 };
 }  // namespace
 
+constexpr uint32_t kStateMagic = 0x45444c53;  // "EDLS"
+
+// Host protocol state at this mini-batch boundary (the leader's decisions so far): t_cur,
+// topology version, ring, the lease manager snapshot (datapipeline.cpp:115 layout) and every
+// ring member's current shard cursor.  A newcomer process adopts it instead of replaying the
+// job's whole history (the newcomer receives the pending topology).
+int Job::export_host_state(std::vector<uint8_t>* out) const {
+  if (!events_.empty()) return fail(EDL_RETRY, "state: a scaling operation is pending");
+  BlobW w;
+  w.pod(kStateMagic);
+  w.pod<uint64_t>(t_);
+  w.pod<uint64_t>(version_);
+  w.pod(static_cast<uint32_t>(ring_.size()));
+  for (const auto& id : ring_) {
+    w.text(id);
+    const Cursor& c = workers_.at(id)->cur;
+    w.pod<uint8_t>(c.has ? 1 : 0);
+    w.pod(c.part);
+    w.pod(c.off);
+    w.pod(c.len);
+    w.pod(c.first);
+    w.pod(c.epoch);
+  }
+  const std::vector<uint8_t> lease = lm_->snapshot();
+  w.pod<uint64_t>(lease.size());
+  w.b.insert(w.b.end(), lease.begin(), lease.end());
+  *out = std::move(w.b);
+  return EDL_OK;
+}
+
+int Job::adopt_host_state(const uint8_t* blob, size_t len, int64_t switch_t) {
+  if (!joining_ || t_ != 0 || launched_ != 0 || events_.size() != 1)
+    return fail(EDL_EINVAL, "adopt_state: only a newcomer process before its first step");
+  BlobR rd{blob, len};
+  if (rd.pod<uint32_t>() != kStateMagic) return fail(EDL_EINVAL, "adopt_state: not a state blob");
+  const uint64_t t = rd.pod<uint64_t>();
+  const uint64_t version = rd.pod<uint64_t>();
+  const uint32_t n = rd.pod<uint32_t>();
+  std::vector<std::string> ring;
+  std::vector<Cursor> cur;
+  for (uint32_t i = 0; i < n && rd.ok; ++i) {
+    ring.push_back(rd.text());
+    Cursor c;
+    c.has = rd.pod<uint8_t>() != 0;
+    c.part = rd.pod<uint32_t>();
+    c.off = rd.pod<uint64_t>();
+    c.len = rd.pod<uint64_t>();
+    c.first = rd.pod<uint64_t>();
+    c.epoch = rd.pod<uint64_t>();
+    cur.push_back(c);
+  }
+  const uint64_t llen = rd.pod<uint64_t>();
+  if (!rd.ok || rd.at + llen > len) return fail(EDL_ETRUNCATED, "adopt_state: truncated");
+  if (ring != ring_) return fail(EDL_EINVAL, "adopt_state: the ring changed since the command");
+  if (switch_t <= static_cast<int64_t>(t)) return fail(EDL_EINVAL, "adopt_state: switch passed");
+  // validated: replace the placeholder state (parse the leases into a copy first)
+  auto lm = std::make_unique<LeaseManager>(*lm_);
+  LeaseStatus ls;
+  try {
+    ls = lm->restore(blob + rd.at, llen);
+  } catch (const std::exception&) {
+    return fail(EDL_ETRUNCATED, "adopt_state: truncated lease state");
+  }
+  if (ls != LeaseStatus::Ok) return fail(EDL_SHAPE_MISMATCH, "adopt_state: lease state rejected");
+  lm_ = std::move(lm);
+  for (size_t i = 0; i < ring.size(); ++i) workers_.at(ring[i])->cur = cur[i];
+  t_ = t;
+  version_ = version;
+  events_.front()->switch_t = switch_t;
+  log_.clear();
+  if (cfg_.keep_log) {  // this process's log starts at the adopted boundary
+    LogRec r;
+    r.kind = LogRec::Topo;
+    r.t = t_ == 0 ? 0 : t_ - 1;
+    r.version = version_;
+    r.ring = ring_;
+    log_.push_back(r);
+  }
+  resplit();
+  return EDL_OK;
+}
+
 int Job::export_handles(std::vector<uint8_t>* out) const {
   const Replica* r = reps_.begin()->second.get();
   DeviceGuard g(dry_ ? 0 : r->device);

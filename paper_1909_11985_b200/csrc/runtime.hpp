@@ -198,6 +198,10 @@ class Job {
   // multi-process data parallelism (one process per GPU): CUDA IPC handle exchange
   int export_handles(std::vector<uint8_t>* out) const;
   int import_handles(const uint8_t* blob, size_t len);
+  // scheduler-facing scale-out across processes: the leader's host state at a boundary and
+  // its adoption by a newcomer process (created with create_joining) before its first step
+  int export_host_state(std::vector<uint8_t>* out) const;
+  int adopt_host_state(const uint8_t* blob, size_t len, int64_t switch_t);
   bool peers_ready() const;
   // all-gather of the sharded fp32 master across replicas (collective: every process calls)
   int gather_master();

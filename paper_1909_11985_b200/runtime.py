@@ -266,6 +266,21 @@ class Job:
         buf = (C.c_uint8 * max(1, len(blob))).from_buffer_copy(blob or b"\0")
         _lib.check(self._L.edl_job_import(self._h, buf, len(blob)))
 
+    def export_state(self) -> bytes:
+        """Host protocol state at this boundary (leader side of a scheduler-facing
+        scale-out across processes; EdlError(Retry) while a scaling op is pending)."""
+        n = C.c_size_t()
+        _lib.check(self._L.edl_job_export_state(self._h, None, 0, C.byref(n)))
+        buf = (C.c_uint8 * max(1, n.value))()
+        _lib.check(self._L.edl_job_export_state(self._h, buf, n.value, C.byref(n)))
+        return bytes(buf[:n.value])
+
+    def adopt_state(self, blob: bytes, switch_t: int) -> None:
+        """Newcomer process (Job.joining, before its first step): continue from the leader's
+        boundary state and switch in at switch_t."""
+        buf = (C.c_uint8 * max(1, len(blob))).from_buffer_copy(blob or b"\0")
+        _lib.check(self._L.edl_job_adopt_state(self._h, buf, len(blob), switch_t))
+
     def gather_master(self) -> None:
         _lib.check(self._L.edl_job_gather_master(self._h))
 

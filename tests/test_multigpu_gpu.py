@@ -78,3 +78,24 @@ def test_multi_process_scale_out():
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     assert "MP-SCALE-OUT OK" in p.stdout
+
+
+# Scheduler-facing scaling across processes (paper_1909_11985_b200/control.py): scale_out
+# with Ready -> switch_t = t + max(k, margin) agreed through the rendezvous store, Retry while
+# pending, momentum carried to the newcomers, straggler detection over the processes' published
+# mini-batch times and the leader's scale_in, all checked against the oracle.
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+def test_multi_process_scheduler_facing_scaling():
+    n = min(torch.cuda.device_count(), 4)
+    here = os.path.dirname(os.path.abspath(__file__))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29541",
+           os.path.join(here, "mp_elastic_api_worker.py")]
+    env = dict(os.environ)
+    env.pop("EDL_OVERLAP", None)
+    env.pop("EDL_AG_DEFER", None)
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=400, env=env)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert "MP-ELASTIC-API OK" in p.stdout
+    print([ln for ln in p.stdout.splitlines() if "MP-ELASTIC-API" in ln])
