@@ -1184,8 +1184,11 @@ bool get(const std::string& b, size_t* o, T* v) {
 int Job::save_checkpoint(const std::string& path) {
   EDL_TRY(join_side());  // the deferred push collective updates master / W
   if (path.empty()) return fail(EDL_EINVAL, "checkpoint: empty path");
-  for (const auto& p : peers_)
-    if (!p.local) return fail(EDL_EINVAL, "checkpoint: multi-process jobs gather first (not supported)");
+  // one process per GPU: a collective -- every ring process saves at the same boundary (the
+  // fp32 master / momentum shards are all-gathered, then each process writes the identical
+  // checkpoint from its own replica; the host state is the same everywhere by construction)
+  bool all_local = true;
+  for (const auto& p : peers_) all_local = all_local && p.local;
   EDL_TRY(sync(nullptr));
   std::string b(kCkptMagic, 8);
   put<uint32_t>(&b, 1);  // format version
@@ -1206,7 +1209,10 @@ int Job::save_checkpoint(const std::string& path) {
   std::vector<char> params(dry_ ? 0 : esz * P_), mom;
   if (!dry_) {
     Replica* r = primary();
-    EDL_TRY(consolidate_master());
+    if (all_local)
+      EDL_TRY(consolidate_master());
+    else
+      EDL_TRY(gather_master());
     DeviceGuard g(r->device);
     EDL_CUDA_TRY(cudaStreamSynchronize(r->stream));
     EDL_CUDA_TRY(cudaMemcpy(params.data(), mlp_ ? static_cast<void*>(r->master)
@@ -1231,8 +1237,8 @@ int Job::save_checkpoint(const std::string& path) {
 
 int Job::load_checkpoint(const std::string& path) {
   EDL_TRY(join_side());  // the deferred push collective updates master / W
-  for (const auto& p : peers_)
-    if (!p.local) return fail(EDL_EINVAL, "checkpoint: multi-process restore not supported");
+  // one process per GPU: every ring process loads the same checkpoint (each replica then
+  // holds the whole model, which the sharded update keeps consistent from here)
   if (!events_.empty()) return fail(EDL_RETRY, "checkpoint: a scaling operation is pending");
   std::string b;
   {
@@ -1330,8 +1336,14 @@ int Job::load_checkpoint(const std::string& path) {
 
 int Job::recover(const std::vector<std::string>& failed, bool approximate, EdlRecovery* out) {
   EDL_TRY(join_side());  // the deferred push collective updates master / W
-  for (const auto& p : peers_)
-    if (!p.local) return fail(EDL_EINVAL, "recover: multi-process recovery not supported");
+  bool all_local = true;
+  for (const auto& p : peers_) all_local = all_local && p.local;
+  // one process per GPU: consistent recovery only -- each survivor drops the failed
+  // processes' replicas (never touching their memory again) and reloads its checkpoint.
+  // Approximate recovery would need the failed GPU's fp32 master shard, which died with it.
+  if (!all_local && approximate)
+    return fail(EDL_EINVAL, "recover: approximate recovery needs every master shard "
+                            "(single process); use consistent recovery across processes");
   size_t hit = 0;
   for (const auto& id : failed) hit += std::count(ring_.begin(), ring_.end(), id);
   if (hit == 0 || hit != failed.size()) return fail(EDL_UNKNOWN_WORKER, "recover: not ring members");

@@ -99,3 +99,22 @@ def test_multi_process_scheduler_facing_scaling():
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     assert "MP-ELASTIC-API OK" in p.stdout
     print([ln for ln in p.stdout.splitlines() if "MP-ELASTIC-API" in ln])
+
+
+# Consistent failure recovery across processes: collective checkpoint at t=5, the last rank's
+# process dies after t=8, the survivors drop its replica, reload the checkpoint and go on --
+# least squares bit-exact with the oracle's snapshot / restore, MLP (momentum) within 1e-3.
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+def test_multi_process_consistent_recovery():
+    n = min(torch.cuda.device_count(), 4)
+    here = os.path.dirname(os.path.abspath(__file__))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29543",
+           os.path.join(here, "mp_recovery_worker.py")]
+    env = dict(os.environ)
+    env.pop("EDL_OVERLAP", None)
+    env.pop("EDL_AG_DEFER", None)
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=400, env=env)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert "MP-RECOVERY OK" in p.stdout
