@@ -35,6 +35,142 @@ from .runtime import Job, switch_delay
 K_SLOTS = 4  # csrc/runtime.hpp kSlots: host steps in flight ahead of the device
 
 
+class SystemClock:
+    def now(self) -> float:
+        return time.monotonic()
+
+
+class ManualClock:
+    """Injectable clock for deterministic expiry tests (the reference's ManualClock)."""
+
+    def __init__(self, t: float = 0.0):
+        self.t = t
+
+    def now(self) -> float:
+        return self.t
+
+    def advance(self, dt: float) -> None:
+        self.t += dt
+
+
+class LeaderLease:
+    """Lease-backed leader election with compare-and-swap semantics (the reference's
+    LeaseStore, coordination.hpp / coordination.cpp:26-117) on a
+    torch.distributed Store: the record "address|deadline|generation" of key `job` is
+    claimed by an atomic compare_set when it is absent, erased or expired; refresh extends
+    the holder's deadline, erase removes it (graceful exit), get reads it.  watch()/poll()
+    deliver Elected(address, generation) after each successful claim and Expired within one
+    poll after a record expires or is erased.  TTL default 3 s (refresh ttl/3, poll ttl/10).
+    Times come from `clock` (monotonic; processes on one node share it)."""
+
+    WON, LOST = "Won", "Lost"
+    OK, NOT_LEADER = "Ok", "NotLeader"
+
+    def __init__(self, store, clock=None, ttl: float = 3.0, prefix: str = "edl/leader/"):
+        self.store = store
+        self.clock = clock or SystemClock()
+        self.ttl = ttl
+        self.p = prefix
+        self._watch = {}   # id -> (job, fn)
+        self._seen = {}    # job -> (present, generation) last delivered to watchers
+        self._next = 0
+
+    def _key(self, job: str) -> str:
+        return self.p + job
+
+    def _read(self, job: str) -> str:
+        k = self._key(job)
+        return self.store.get(k).decode() if self.store.check([k]) else ""
+
+    @staticmethod
+    def _parse(rec: str):
+        if not rec or rec.startswith("-"):  # absent, or erased ("-<generation>")
+            return None
+        addr, dl, gen = rec.rsplit("|", 2)
+        return addr, float(dl), int(gen)
+
+    @staticmethod
+    def _last_gen(rec: str) -> int:
+        if not rec:
+            return 0
+        if rec.startswith("-"):
+            return int(rec[1:])
+        return int(rec.rsplit("|", 1)[1])
+
+    def cas_put_if_absent_or_expired(self, job: str, address: str, ttl: float = None):
+        """(Won, generation, address) or (Lost, generation, winner's address)."""
+        t = self.ttl if ttl is None else ttl
+        while True:
+            cur = self._read(job)
+            rec = self._parse(cur)
+            now = self.clock.now()
+            if rec is not None and now <= rec[1]:
+                return (self.LOST, rec[2], rec[0])
+            gen = self._last_gen(cur) + 1
+            new = f"{address}|{now + t!r}|{gen}"
+            got = self.store.compare_set(self._key(job), cur, new).decode()
+            if got == new:
+                self.poll()
+                return (self.WON, gen, address)
+            # somebody changed the record between the read and the swap: look again
+
+    def refresh(self, job: str, address: str, ttl: float = None) -> str:
+        t = self.ttl if ttl is None else ttl
+        cur = self._read(job)
+        rec = self._parse(cur)
+        now = self.clock.now()
+        if rec is None or rec[0] != address or now > rec[1]:
+            return self.NOT_LEADER
+        new = f"{address}|{now + t!r}|{rec[2]}"
+        return self.OK if self.store.compare_set(self._key(job), cur, new).decode() == new \
+            else self.NOT_LEADER
+
+    def erase(self, job: str, address: str) -> str:
+        cur = self._read(job)
+        rec = self._parse(cur)
+        if rec is None or rec[0] != address:
+            return self.NOT_LEADER
+        new = f"-{rec[2]}"  # keeps the generation counter monotonic across erases
+        ok = self.store.compare_set(self._key(job), cur, new).decode() == new
+        if ok:
+            self.poll()
+        return self.OK if ok else self.NOT_LEADER
+
+    def get(self, job: str):
+        """(address, deadline, generation) of the unexpired record, or None."""
+        rec = self._parse(self._read(job))
+        return rec if rec is not None and self.clock.now() <= rec[1] else None
+
+    def watch(self, job: str, fn) -> int:
+        self._next += 1
+        self._watch[self._next] = (job, fn)
+        self._seen.setdefault(job, (False, 0))
+        return self._next
+
+    def unwatch(self, wid_: int) -> None:
+        self._watch.pop(wid_, None)
+
+    def poll(self) -> None:
+        """Deliver Elected / Expired to the watchers of every watched job (call every
+        ttl/10, or after own claims / erases)."""
+        for job in {j for j, _ in self._watch.values()}:
+            rec = self.get(job)
+            was_present, was_gen = self._seen.get(job, (False, 0))
+            evs = []
+            if rec is not None and rec[2] != was_gen:
+                if was_present:
+                    evs.append(("Expired", job, "", 0))
+                evs.append(("Elected", job, rec[0], rec[2]))
+                self._seen[job] = (True, rec[2])
+            elif rec is None and was_present:
+                evs.append(("Expired", job, "", 0))
+                self._seen[job] = (False, was_gen)
+            for ev in evs:
+                for j, fn in list(self._watch.values()):
+                    if j == job:
+                        fn(ev)
+
+
 def wid(rank: int) -> str:
     return f"w{rank:02d}"
 
@@ -44,10 +180,16 @@ class ElasticGroup:
     (worker ids w<rank>); the leader is the lowest rank of the current ring."""
 
     def __init__(self, store, rank: int, ring_ranks, t_a_ms: float = 500.0, poll_every: int = 8,
-                 prefix: str = "edl/"):
+                 prefix: str = "edl/", lease: "LeaderLease" = None, job_key: str = "job"):
         self.store = store
         self.rank = rank
         self.ring_ranks = sorted(ring_ranks)
+        # leader election (SPEC.md:17-90): with a LeaderLease the leader is whoever holds the
+        # job's lease record (address "rank:<r>"); without one, the lowest ring rank
+        self.lease = lease
+        self.job_key = job_key
+        self._leader_rank = None
+        self._refreshed = 0.0
         self.t_a_ms = t_a_ms
         self.poll_every = max(1, poll_every)
         self.margin = self.poll_every + 2 * K_SLOTS + 2
@@ -72,7 +214,28 @@ class ElasticGroup:
 
     @property
     def leader(self) -> int:
-        return self.ring_ranks[0]
+        if self.lease is None:
+            return self.ring_ranks[0]
+        if self._leader_rank is None:
+            rec = self.lease.get(self.job_key)
+            self._leader_rank = int(rec[0].split(":")[1]) if rec else -1
+        return self._leader_rank
+
+    def elect(self) -> bool:
+        """Ring process: try to become the leader (cas_put_if_absent_or_expired)."""
+        st, gen, addr = self.lease.cas_put_if_absent_or_expired(self.job_key, f"rank:{self.rank}")
+        self._leader_rank = int(addr.split(":")[1])
+        self._refreshed = self.lease.clock.now()
+        self.generation = gen
+        return st == LeaderLease.WON
+
+    def leave(self, job: Job) -> None:
+        """A leaving leader's graceful exit: erase the coordination record so the
+        survivors elect a successor at once; the job meta-data (t_cur, B, pipeline cursor) is
+        already identical in every process (each replays the leader's decisions)."""
+        if self.lease is not None and self.leader == self.rank:
+            self.lease.erase(self.job_key, f"rank:{self.rank}")
+            self._leader_rank = None
 
     def busy(self, job: Job) -> bool:
         return self.pending is not None or job.t <= self.pending_until
@@ -102,8 +265,8 @@ class ElasticGroup:
         if self.busy(job):
             raise _lib.EdlError(_lib.EDL_RETRY, "a scaling operation is in progress")
         ranks = sorted(ranks)
-        if self.leader in ranks:
-            raise _lib.EdlError(_lib.EDL_EINVAL, "scale_in of the leader: hand off first")
+        if self.leader in ranks and self.lease is None:
+            raise _lib.EdlError(_lib.EDL_EINVAL, "scale_in of the leader needs leader election")
         switch_t = job.t + self._delay(job)
         ids = [wid(r) for r in ranks]
         self._set(self._k("cmd", self.n_cmd), {"kind": "in", "ranks": ranks, "ids": ids,
@@ -126,6 +289,18 @@ class ElasticGroup:
     def notify_batch_end(self, job: Job):
         """Call after each job.step() on every ring process.  Returns the (kind, ids,
         switch_t) of an event scheduled by this call, else None."""
+        if self.lease is not None:
+            if self.leader == self.rank:  # keep the lease: refresh every ttl / 3
+                now = self.lease.clock.now()
+                if now - self._refreshed > self.lease.ttl / 3:
+                    if self.lease.refresh(self.job_key, f"rank:{self.rank}") != LeaderLease.OK:
+                        self._leader_rank = None  # lost it (expired and re-elected)
+                    self._refreshed = now
+            elif job.t % self.poll_every == 0 and job.t > self.pending_until:
+                # the leader left (erased) or died (expired): elect a successor
+                self._leader_rank = None
+                if self.leader < 0 or self.leader not in self.ring_ranks:
+                    self.elect()
         if self.rank == self.leader and self.pending is not None:
             return self._leader_poll_ready(job)
         if self.rank != self.leader and job.t % self.poll_every == 0:

@@ -2723,10 +2723,18 @@ int Job::import_handles(const uint8_t* blob, size_t len) {
   // count the collective barriers wait for
   if (rd.ok && peer.rank == my_rank_)
     return fail(EDL_EINVAL, "import: blob of this process's own replica");
-  for (const auto& q : known_peers_)
-    if (rd.ok && q.rank == peer.rank)
+  for (auto it = known_peers_.begin(); rd.ok && it != known_peers_.end(); ++it) {
+    if (it->rank != peer.rank) continue;
+    // a replica whose process left the ring and now re-joins: its old entry (mappings of
+    // memory that process has freed) is replaced; a live one is a duplicate
+    bool hosts = false;
+    for (const auto& [id, w] : workers_) hosts = hosts || (w->remote && w->host_rank == peer.rank);
+    if (hosts || it->local)
       return fail(EDL_EINVAL, "import: replica rank " + std::to_string(peer.rank) +
                                   " already imported");
+    known_peers_.erase(it);
+    break;
+  }
   peer.device = rd.pod<int32_t>();
   if (rd.pod<uint64_t>() != P_) return fail(EDL_SHAPE_MISMATCH, "import: model shape differs");
   auto open = [&](void** dst) -> int {

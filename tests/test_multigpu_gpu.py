@@ -118,3 +118,21 @@ def test_multi_process_consistent_recovery():
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=400, env=env)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     assert "MP-RECOVERY OK" in p.stdout
+
+
+# Leader election and handoff across processes (control.LeaderLease over the rendezvous
+# store): the elected leader scales itself in, the survivor wins the next election
+# (generation 2) and scales the old leader's process back out -- checked against the oracle.
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+def test_multi_process_leader_handoff():
+    here = os.path.dirname(os.path.abspath(__file__))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29545",
+           os.path.join(here, "mp_leader_handoff_worker.py")]
+    env = dict(os.environ)
+    env.pop("EDL_OVERLAP", None)
+    env.pop("EDL_AG_DEFER", None)
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=400, env=env)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert "MP-HANDOFF OK" in p.stdout
