@@ -539,15 +539,19 @@ def _elastic_cfg(batch: int, world: int):
 
 
 def _switch_stall(reps, settle: int = 10) -> dict:
-    """reps: per-mini-batch reports (synced each step) around one switch."""
+    """reps: per-mini-batch reports (synced each step) around one switch.  A mini-batch's
+    device cost is its own time plus the device idle gap before it (the model copies and
+    consolidation of a switch are enqueued before the switch mini-batch's first kernel);
+    stall = that cost at the switch minus its median over the steady mini-batches after."""
     k = next(i for i, r in enumerate(reps) if r.switched)
-    before = statistics.median(r.step_ms for r in reps[max(0, k - settle):k])
-    after = statistics.median(r.step_ms for r in reps[k + 2:k + 2 + settle])
+    cost = [r.step_ms + r.stall_ms for r in reps]
+    before = statistics.median(cost[max(0, k - settle):k])
+    after = statistics.median(cost[k + 2:k + 2 + settle])
     sw = reps[k]
     return {"switch_t": sw.t, "ring_size": sw.ring_size, "version": sw.version,
-            "step_ms_before": before, "step_ms_after": after, "switch_step_ms": sw.step_ms,
-            "stall_ms": max(0.0, sw.step_ms - after) + sw.stall_ms,
-            "stall_over_step": (max(0.0, sw.step_ms - after) + sw.stall_ms) / after}
+            "ms_before": before, "ms_after": after, "switch_ms": cost[k],
+            "stall_ms": max(0.0, cost[k] - after),
+            "stall_over_step": max(0.0, cost[k] - after) / after}
 
 
 def elastic_leg_single(args) -> dict:
@@ -585,7 +589,7 @@ def elastic_leg_single(args) -> dict:
     sin = _switch_stall(reps, settle)
     from oracle import api, restated  # checker only: the lease log's exactly-once coverage
     ok, _, _ = api.check_coverage(restated(), job.log_text(), WORKLOAD["size"])
-    steady = sin["step_ms_after"]
+    steady = sin["ms_after"]
     # stop-resume: checkpoint, teardown, fresh process, restore, first mini-batch
     import tempfile
     fd, path = tempfile.mkstemp(suffix=".ckpt")
@@ -657,7 +661,8 @@ def elastic_leg_mp(args, rank: int, world: int, local: int, dist) -> dict:
             if rep.t >= s2:
                 break
             continue
-        ms[rep.t] = job.sync().step_ms
+        r2 = job.sync()
+        ms[rep.t] = r2.step_ms + r2.stall_ms  # incl. the idle gap of the switch's copies
     allms = [None] * world
     dist.all_gather_object(allms, ms)
     dist.barrier()

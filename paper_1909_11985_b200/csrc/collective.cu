@@ -541,6 +541,35 @@ int master_allgather(const CollArgs& a, cudaStream_t s) {
   return EDL_OK;
 }
 
+__global__ void __launch_bounds__(256) multi_copy_kernel(const __grid_constant__ MultiCopyArgs a) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (int k = 0; k < a.n; ++k) {
+    const uint4* src = static_cast<const uint4*>(a.seg[k].src);
+    uint4* dst = static_cast<uint4*>(a.seg[k].dst);
+    const size_t n = a.seg[k].bytes / 16;
+    size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    for (; i + 3 * stride < n; i += 4 * stride) {  // four loads in flight per thread
+      const uint4 v0 = __ldcs(src + i), v1 = __ldcs(src + i + stride);
+      const uint4 v2 = __ldcs(src + i + 2 * stride), v3 = __ldcs(src + i + 3 * stride);
+      dst[i] = v0;
+      dst[i + stride] = v1;
+      dst[i + 2 * stride] = v2;
+      dst[i + 3 * stride] = v3;
+    }
+    for (; i < n; i += stride) dst[i] = __ldcs(src + i);
+  }
+}
+
+int multi_copy(const MultiCopyArgs& a, cudaStream_t s) {
+  if (a.n < 0 || a.n > kMaxCopySegs) return fail(EDL_EINVAL, "multi_copy: segments");
+  for (int k = 0; k < a.n; ++k)
+    if (a.seg[k].bytes % 16) return fail(EDL_EINVAL, "multi_copy: 16-byte multiples");
+  if (a.n == 0) return EDL_OK;
+  multi_copy_kernel<<<coll_blocks(), 256, 0, s>>>(a);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
+
 int coll_blocks() { return 148 * 4; }
 
 // Loads the collective kernels on the current device (cudaFuncGetAttributes forces the lazy
@@ -552,6 +581,7 @@ int coll_prepare_device() {
   EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, allreduce_sgd_kernel<false, 2>));
   EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, allreduce_sgd_kernel<true, 2>));
   EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, master_allgather_kernel));
+  EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, multi_copy_kernel));
   EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, barrier_kernel));
   EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, linear_allreduce_sgd_kernel));
   return EDL_OK;

@@ -137,6 +137,22 @@ int stream_write_u32(uint32_t* addr, uint32_t value, cudaStream_t s);
 int ce_wait(const CeWait& a, cudaStream_t s);
 int shard_update(const ShardUpdateArgs& a, cudaStream_t s);
 
+// SM-driven copy of up to kMaxCopySegs (dst, src, bytes) segments in one launch (every SM,
+// 16-byte vectors, several loads in flight): the model re-sharding of a scale event, where
+// dst is mostly peer memory over NVLink (SM stores reach ~690 GB/s per direction, more than
+// one copy-engine memcpy of an IPC mapping).  bytes must be multiples of 16.
+constexpr int kMaxCopySegs = 64;
+struct CopySeg {
+  void* dst;
+  const void* src;
+  size_t bytes;
+};
+struct MultiCopyArgs {
+  CopySeg seg[kMaxCopySegs];
+  int n = 0;
+};
+int multi_copy(const MultiCopyArgs& a, cudaStream_t s);
+
 int coll_blocks();
 int coll_prepare_device();  // current device: load the collective kernels
 // Debug timeline: one thread writes %globaltimer (ns) to dst (mapped pinned host memory).

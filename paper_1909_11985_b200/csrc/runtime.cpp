@@ -604,12 +604,22 @@ int Job::install_due(bool* switched) {
   while (!events_.empty() && events_.front()->switch_t <= static_cast<int64_t>(t_)) {
     std::unique_ptr<Event> ev = std::move(events_.front());
     events_.pop_front();
-    // the fp32 master is sharded across GPUs; make every replica whole before the
-    // membership (and with it the sharding) changes
-    EDL_TRY(consolidate_master());
     // newcomers hosted by their own processes (scale-out across processes)
     bool multi = !dry_ && ev->out && joining_;
     for (const auto& w : ev->prepared) multi = multi || (!dry_ && w && w->remote);
+    // the fp32 master is sharded across GPUs; make every replica whole before the
+    // membership (and with it the sharding) changes -- except for a scale-out across
+    // processes, which re-shards with targeted copies (install_out_mp)
+    bool all_local = true;
+    for (const auto& p : peers_) all_local = all_local && p.local;
+    if (ev->out && multi) {
+      EDL_TRY(join_side());  // the deferred push collective updates master / W
+    } else if (!ev->out && !all_local && mlp_ && !dry_ && peers_.size() > 1) {
+      EDL_TRY(join_side());
+      EDL_TRY(reshard_in_mp(ev.get()));  // targeted: each survivor gets its new shard only
+    } else {
+      EDL_TRY(consolidate_master());
+    }
     if (ev->out && multi) {
       EDL_TRY(install_out_mp(ev.get()));
     } else if (ev->out) {
@@ -2225,6 +2235,74 @@ int Job::sync(EdlStepReport* out) {
 // epoch and the new topology version into the newcomer's join words.  Newcomer: wait on the
 // host until every source's version word has arrived, adopt the epoch.  Everyone: the
 // newcomers join the ring (ascending id) and the replica list.
+int Job::add_copy(MultiCopyArgs* cp, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (!bytes) return EDL_OK;
+  if (cp->n == kMaxCopySegs) {
+    EDL_TRY(multi_copy(*cp, s));
+    launches_ += 1;
+    cp->n = 0;
+  }
+  cp->seg[cp->n++] = CopySeg{dst, src, bytes};
+  return EDL_OK;
+}
+
+// The fp32 master (and momentum) is current on each replica only for its own shard
+// (own_segments under peers_.size() replicas).  For the replicas `after` a switch, copy from
+// this replica (peers_ index me) every piece of its old shard that lies in another replica's
+// new shard (own_segments under after.size()): after the copies land every replica holds its
+// new shard, with no all-gather of the whole model.
+int Job::add_reshard_pieces(MultiCopyArgs* cp, int me, const std::vector<PeerRep>& after,
+                            Replica* r) {
+  const int n_old = static_cast<int>(peers_.size()), n_new = static_cast<int>(after.size());
+  for (int l = 0; l < L_; ++l) {
+    const size_t len8 = static_cast<size_t>(in_[l]) * out_[l] / 8, base = off_[l];
+    size_t olo, ohi;  // my old shard of layer l
+    shard_range(len8, n_old, me, &olo, &ohi);
+    for (int j = 0; j < n_new; ++j) {
+      if (after[j].rank == peers_[me].rank) continue;  // my new shard: already mine
+      size_t nlo, nhi;
+      shard_range(len8, n_new, j, &nlo, &nhi);
+      const size_t a8 = std::max(olo, nlo), b8 = std::min(ohi, nhi);
+      if (b8 <= a8) continue;
+      const size_t at = base + a8 * 8, n = (b8 - a8) * 8;
+      EDL_TRY(add_copy(cp, after[j].master + at, r->master + at, sizeof(float) * n, r->stream));
+      if (r->mom) {
+        if (!after[j].mom) return fail(EDL_EINVAL, "reshard: a replica has no momentum buffer");
+        EDL_TRY(add_copy(cp, after[j].mom + at, r->mom + at, sizeof(float) * n, r->stream));
+      }
+    }
+  }
+  return EDL_OK;
+}
+
+// Scale-in across processes: the survivors' new shards from the old owners (leavers
+// included, they are still in the ring at this boundary), then a barrier of every old
+// replica so nobody updates before the pieces it needs have landed.
+int Job::reshard_in_mp(const Event* ev) {
+  std::vector<PeerRep> after;
+  for (size_t i = 0; i < peers_.size(); ++i) {
+    bool keeps = false;
+    for (const auto& id : ring_)
+      keeps = keeps || (std::find(ev->ids.begin(), ev->ids.end(), id) == ev->ids.end() &&
+                        host_index(id) == static_cast<int>(i));
+    if (keeps) after.push_back(peers_[i]);
+  }
+  const int me = rep_index();
+  Replica* r = peers_[me].rep;
+  DeviceGuard g(r->device);
+  MultiCopyArgs cp;
+  EDL_TRY(add_reshard_pieces(&cp, me, after, r));
+  EDL_TRY(multi_copy(cp, r->stream));
+  CollArgs a;
+  for (const auto& p : peers_) a.flags[a.n_dst++] = p.flags;
+  a.me = me;
+  a.n_rep = static_cast<int>(peers_.size());
+  a.epoch = ++coll_epoch_;
+  EDL_TRY(replica_barrier(a, r->stream));
+  launches_ += 2;
+  return EDL_OK;
+}
+
 int Job::install_out_mp(Event* ev) {
   const uint64_t new_version = version_ + 1;
   std::vector<PeerRep> joiners;  // newcomer replicas (imported, or this process's own)
@@ -2267,23 +2345,65 @@ int Job::install_out_mp(Event* ev) {
     Replica* r = peers_[me].rep;
     DeviceGuard g(r->device);
     if (mlp_) {
-      size_t lo, hi;
-      shard_range(P_ / 8, n_src, me, &lo, &hi);
-      lo *= 8;
-      hi = hi == P_ / 8 ? P_ : hi * 8;
-      for (const auto& q : joiners) {
-        if (hi > lo) {
-          EDL_CUDA_TRY(cudaMemcpyAsync(q.master + lo, r->master + lo, sizeof(float) * (hi - lo),
-                                       cudaMemcpyDeviceToDevice, r->stream));
-          EDL_CUDA_TRY(cudaMemcpyAsync(q.W + lo, r->W + lo, sizeof(__nv_bfloat16) * (hi - lo),
-                                       cudaMemcpyDeviceToDevice, r->stream));
-          if (r->mom) {
-            if (!q.mom) return fail(EDL_EINVAL, "scale_out: newcomer has no momentum buffer");
-            EDL_CUDA_TRY(cudaMemcpyAsync(q.mom + lo, r->mom + lo, sizeof(float) * (hi - lo),
-                                         cudaMemcpyDeviceToDevice, r->stream));
+      // Targeted re-sharding instead of consolidating the whole model: the bf16 weights are
+      // current and identical on every replica, so each source ships slice me/n of them to
+      // every newcomer; the fp32 master (and momentum) is only current on each replica's
+      // own shard, and after the switch every replica -- old or new -- only needs its NEW
+      // shard (own_segments under n_new), so the old owner of each piece of a new shard
+      // copies exactly that piece to its new owner.  A newcomer receives 2 B/param of
+      // weights plus 4 B (8 with momentum) per parameter of its shard instead of the whole
+      // fp32 model, and no replica all-gathers ("broadcast the model").
+      MultiCopyArgs cp;
+      std::vector<PeerRep> after = peers_;  // the replicas after the switch, rank order
+      for (const auto& q : joiners) after.push_back(q);
+      std::sort(after.begin(), after.end(),
+                [](const PeerRep& a, const PeerRep& b) { return a.rank < b.rank; });
+      // The newcomers' bf16 weights come from every source, in shares that even out each
+      // source's NVLink egress with the master pieces it also sends (every process computes
+      // the same split): source i sends the [wlo_i, whi_i) part, in units of 8 parameters, of
+      // the weights of all newcomers laid end to end.
+      const size_t p8 = P_ / 8, jn = joiners.size();
+      const int n_new = static_cast<int>(after.size());
+      std::vector<double> mb(n_src, 0.0);  // master (+ momentum) bytes source i sends
+      for (int i = 0; i < n_src; ++i)
+        for (int l = 0; l < L_; ++l) {
+          const size_t len8 = static_cast<size_t>(in_[l]) * out_[l] / 8;
+          size_t olo, ohi;
+          shard_range(len8, n_src, i, &olo, &ohi);
+          for (int j = 0; j < n_new; ++j) {
+            if (after[j].rank == peers_[i].rank) continue;
+            size_t nlo, nhi;
+            shard_range(len8, n_new, j, &nlo, &nhi);
+            const size_t a8 = std::max(olo, nlo), b8 = std::min(ohi, nhi);
+            if (b8 > a8) mb[i] += (b8 - a8) * 8.0 * (r->mom ? 8.0 : 4.0);
           }
         }
+      const double wtot = static_cast<double>(jn * p8) * 16.0;  // bytes of weights to ship
+      double sum_m = 0;
+      for (double m : mb) sum_m += m;
+      std::vector<double> quota(n_src);
+      double qsum = 0;
+      for (int i = 0; i < n_src; ++i) {
+        quota[i] = std::max(0.0, (wtot + sum_m) / n_src - mb[i]);
+        qsum += quota[i];
       }
+      size_t wlo = 0, whi = 0, acc = 0;
+      for (int i = 0; i <= me; ++i) {
+        const size_t share = qsum > 0 ? static_cast<size_t>(quota[i] / qsum * (jn * p8))
+                                      : (jn * p8) / n_src;
+        wlo = acc;
+        acc = (i == n_src - 1) ? jn * p8 : std::min(jn * p8, acc + share);
+        whi = acc;
+      }
+      for (size_t pos = wlo; pos < whi;) {  // split the range at newcomer boundaries
+        const size_t q = pos / p8, off = pos % p8, end = std::min(whi, (q + 1) * p8);
+        const size_t lo = off * 8, n = (end - pos) * 8;
+        EDL_TRY(add_copy(&cp, joiners[q].W + lo, r->W + lo, sizeof(__nv_bfloat16) * n, r->stream));
+        pos = end;
+      }
+      EDL_TRY(add_reshard_pieces(&cp, me, after, r));
+      EDL_TRY(multi_copy(cp, r->stream));  // SM stores over NVLink, one launch
+      launches_ += 1;
     }
     for (const auto& q : joiners) {
       EDL_TRY(stream_write_u32(q.flags + kJoinFlagOffset + 2 * me, coll_epoch_, r->stream));

@@ -328,6 +328,10 @@ class Job {
   bool joining_ = false;  // newcomer process whose worker has not switched in yet
   int step_host_only(bool switched, EdlStepReport* out);
   int install_out_mp(Event* ev);
+  int reshard_in_mp(const Event* ev);
+  int add_copy(MultiCopyArgs* cp, void* dst, const void* src, size_t bytes, cudaStream_t s);
+  int add_reshard_pieces(MultiCopyArgs* cp, int me, const std::vector<PeerRep>& after,
+                         Replica* r);
   Worker* find_worker(const std::string& id) const;
   int my_rank_ = 0;
   std::vector<void*> ipc_mapped_;

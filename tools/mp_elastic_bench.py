@@ -9,7 +9,9 @@ the leavers' processes get Exit).  Every process syncs after each mini-batch so 
 the device time of that mini-batch on its GPU; rank 0 prints, as one JSON line, the max over
 the ring's ranks of each mini-batch's time and
 
-  stall_ms = switch mini-batch - median of the following steady mini-batches (same ring)
+  stall_ms = switch mini-batch - median of the following steady mini-batches (same ring),
+             each mini-batch counted with the device idle gap before it (the switch's model
+             copies are enqueued ahead of its first kernel)
 
   python -m torch.distributed.run --nproc-per-node 4 --master-addr 127.0.0.1 \
       tools/mp_elastic_bench.py [--batch 2048]
@@ -64,7 +66,12 @@ def main():
             if rep.t >= args.s2:
                 break
             continue
-        ms[rep.t] = job.sync().step_ms
+        r2 = job.sync()
+        ms[rep.t] = r2.step_ms + r2.stall_ms  # incl. the idle gap of the switch's copies
+        if os.environ.get("EDL_STALL_DEBUG") and rep.t in (args.s1 - 1, args.s1, args.s1 + 1,
+                                                         args.s2, args.s2 + 1):
+            print(f"rank {rank} t={rep.t} step_ms={r2.step_ms:.3f} gap_ms={r2.stall_ms:.3f}",
+                  file=sys.stderr, flush=True)
     allms = [None] * world
     dist.all_gather_object(allms, ms)
     dist.barrier()
