@@ -612,11 +612,24 @@ int Job::install_due(bool* switched) {
     // processes, which re-shards with targeted copies (install_out_mp)
     bool all_local = true;
     for (const auto& p : peers_) all_local = all_local && p.local;
+    // one process driving every replica: re-shard with targeted copies after the switch
+    // (reshard_local); EDL_RESHARD=0 falls back to consolidating the whole model
+    static int reshard_env = -1;
+    if (reshard_env < 0) {
+      const char* e = getenv("EDL_RESHARD");
+      reshard_env = e ? atoi(e) : 1;
+    }
+    const bool local_targeted = reshard_env && !multi && mlp_ && !dry_ && all_local &&
+                                !peers_.empty();
+    const std::vector<PeerRep> old_peers = peers_;
+    std::vector<Replica*> fresh;  // replicas that join the collective at this switch
     if (ev->out && multi) {
       EDL_TRY(join_side());  // the deferred push collective updates master / W
     } else if (!ev->out && !all_local && mlp_ && !dry_ && peers_.size() > 1) {
       EDL_TRY(join_side());
       EDL_TRY(reshard_in_mp(ev.get()));  // targeted: each survivor gets its new shard only
+    } else if (local_targeted) {
+      EDL_TRY(join_side());
     } else {
       EDL_TRY(consolidate_master());
     }
@@ -667,7 +680,10 @@ int Job::install_due(bool* switched) {
       std::set<Replica*> sent;
       for (auto& w : ev->prepared) {
         if (!w || live.count(w->rep) || sent.count(w->rep)) continue;
-        EDL_TRY(broadcast_model(srcs[sent.size() % srcs.size()], w->rep));
+        if (local_targeted)
+          fresh.push_back(w->rep);  // filled by reshard_local once the ring is re-formed
+        else
+          EDL_TRY(broadcast_model(srcs[sent.size() % srcs.size()], w->rep));
         sent.insert(w->rep);
       }
       std::vector<size_t> order(ev->ids.size());
@@ -718,6 +734,7 @@ int Job::install_due(bool* switched) {
       log_.push_back(r);
     }
     rebuild_peers();
+    if (local_targeted) EDL_TRY(reshard_local(old_peers, fresh));
   }
   if (changed) {
     resplit();
@@ -2246,31 +2263,115 @@ int Job::add_copy(MultiCopyArgs* cp, void* dst, const void* src, size_t bytes, c
   return EDL_OK;
 }
 
-// The fp32 master (and momentum) is current on each replica only for its own shard
-// (own_segments under peers_.size() replicas).  For the replicas `after` a switch, copy from
-// this replica (peers_ index me) every piece of its old shard that lies in another replica's
-// new shard (own_segments under after.size()): after the copies land every replica holds its
-// new shard, with no all-gather of the whole model.
-int Job::add_reshard_pieces(MultiCopyArgs* cp, int me, const std::vector<PeerRep>& after,
+static bool same_replica(const PeerRep& a, const PeerRep& b) {
+  if (a.local != b.local) return false;
+  return a.local ? a.rep == b.rep : a.rank == b.rank;
+}
+
+// Bytes of old replica i's shard that lie in other replicas' new shards (old = replicas and
+// sharding before a switch, after = after it; own_segments sharding per layer).
+double Job::reshard_piece_bytes(const std::vector<PeerRep>& old, int i,
+                                const std::vector<PeerRep>& after, bool mom) const {
+  const int n_old = static_cast<int>(old.size()), n_new = static_cast<int>(after.size());
+  double b = 0;
+  for (int l = 0; l < L_; ++l) {
+    const size_t len8 = static_cast<size_t>(in_[l]) * out_[l] / 8;
+    size_t olo, ohi;
+    shard_range(len8, n_old, i, &olo, &ohi);
+    for (int j = 0; j < n_new; ++j) {
+      if (same_replica(after[j], old[i])) continue;
+      size_t nlo, nhi;
+      shard_range(len8, n_new, j, &nlo, &nhi);
+      const size_t a8 = std::max(olo, nlo), b8 = std::min(ohi, nhi);
+      if (b8 > a8) b += (b8 - a8) * 8.0 * (mom ? 8.0 : 4.0);
+    }
+  }
+  return b;
+}
+
+// Re-sharding copies source i (replica `old[i]`, this replica `r`) issues at a switch.  The
+// fp32 master (and momentum) is current on each replica only for its own shard; after the
+// switch every replica -- old or new -- only needs its NEW shard, so the old owner of each
+// piece of a new shard copies exactly that piece to its new owner.  The bf16 weights are
+// current and identical on every old replica: each new replica (`fresh`) gets them from all
+// sources, in shares that even out each source's NVLink egress with the master pieces it
+// sends (every process computes the same split; source i ships the [wlo_i, whi_i) part, in
+// units of 8 parameters, of the weights of all fresh replicas laid end to end).  A newcomer
+// receives 2 B/param of weights plus 4 B (8 with momentum) per parameter of its shard,
+// instead of the whole fp32 model after an all-gather ("broadcast the model").
+int Job::add_reshard_copies(MultiCopyArgs* cp, const std::vector<PeerRep>& old, int i,
+                            const std::vector<PeerRep>& after, const std::vector<PeerRep>& fresh,
                             Replica* r) {
-  const int n_old = static_cast<int>(peers_.size()), n_new = static_cast<int>(after.size());
+  const int n_old = static_cast<int>(old.size());
+  const bool mom = r->mom != nullptr;
+  const size_t p8 = P_ / 8, jn = fresh.size();  // MLP layers: in % 8 == 0, so P_ % 8 == 0
+  std::vector<double> mb(n_old);
+  double sum_m = 0;
+  for (int k = 0; k < n_old; ++k) sum_m += (mb[k] = reshard_piece_bytes(old, k, after, mom));
+  const double wtot = static_cast<double>(jn * p8) * 16.0;  // bytes of weights to ship
+  std::vector<double> quota(n_old);
+  double qsum = 0;
+  for (int k = 0; k < n_old; ++k) qsum += (quota[k] = std::max(0.0, (wtot + sum_m) / n_old - mb[k]));
+  size_t wlo = 0, whi = 0, acc = 0;
+  for (int k = 0; k <= i; ++k) {
+    const size_t share = qsum > 0 ? static_cast<size_t>(quota[k] / qsum * (jn * p8))
+                                  : (jn * p8) / n_old;
+    wlo = acc;
+    acc = (k == n_old - 1) ? jn * p8 : std::min(jn * p8, acc + share);
+    whi = acc;
+  }
+  for (size_t pos = wlo; pos < whi;) {  // split the range at replica boundaries
+    const size_t q = pos / p8, off = pos % p8, end = std::min(whi, (q + 1) * p8);
+    EDL_TRY(add_copy(cp, fresh[q].W + off * 8, r->W + off * 8,
+                     sizeof(__nv_bfloat16) * (end - pos) * 8, r->stream));
+    pos = end;
+  }
+  const int n_new = static_cast<int>(after.size());
   for (int l = 0; l < L_; ++l) {
     const size_t len8 = static_cast<size_t>(in_[l]) * out_[l] / 8, base = off_[l];
     size_t olo, ohi;  // my old shard of layer l
-    shard_range(len8, n_old, me, &olo, &ohi);
+    shard_range(len8, n_old, i, &olo, &ohi);
     for (int j = 0; j < n_new; ++j) {
-      if (after[j].rank == peers_[me].rank) continue;  // my new shard: already mine
+      if (same_replica(after[j], old[i])) continue;  // my new shard: already mine
       size_t nlo, nhi;
       shard_range(len8, n_new, j, &nlo, &nhi);
       const size_t a8 = std::max(olo, nlo), b8 = std::min(ohi, nhi);
       if (b8 <= a8) continue;
       const size_t at = base + a8 * 8, n = (b8 - a8) * 8;
       EDL_TRY(add_copy(cp, after[j].master + at, r->master + at, sizeof(float) * n, r->stream));
-      if (r->mom) {
+      if (mom) {
         if (!after[j].mom) return fail(EDL_EINVAL, "reshard: a replica has no momentum buffer");
         EDL_TRY(add_copy(cp, after[j].mom + at, r->mom + at, sizeof(float) * n, r->stream));
       }
     }
+  }
+  return EDL_OK;
+}
+
+// One process, several GPUs: after the membership change every replica of the new ring
+// (old ones re-sharded, `fresh` ones joining) gets exactly what it needs from the old
+// replicas (add_reshard_copies), each source's copies in one SM copy kernel on its stream,
+// and every new-ring replica's stream waits for all of them.
+int Job::reshard_local(const std::vector<PeerRep>& old, const std::vector<Replica*>& fresh) {
+  std::vector<PeerRep> fr;
+  for (const auto& p : peers_)
+    if (std::find(fresh.begin(), fresh.end(), p.rep) != fresh.end()) fr.push_back(p);
+  bool same = old.size() == peers_.size() && fr.empty();
+  for (size_t i = 0; same && i < old.size(); ++i) same = old[i].rep == peers_[i].rep;
+  if (same) return EDL_OK;  // the sharding did not change
+  for (size_t i = 0; i < old.size(); ++i) {
+    Replica* r = old[i].rep;
+    DeviceGuard g(r->device);
+    MultiCopyArgs cp;
+    EDL_TRY(add_reshard_copies(&cp, old, static_cast<int>(i), peers_, fr, r));
+    EDL_TRY(multi_copy(cp, r->stream));
+    launches_ += 1;
+    EDL_CUDA_TRY(cudaEventRecord(r->ev_sync, r->stream));
+  }
+  for (const auto& p : peers_) {
+    DeviceGuard g(p.rep->device);
+    for (const auto& o : old)
+      if (o.rep != p.rep) EDL_CUDA_TRY(cudaStreamWaitEvent(p.rep->stream, o.rep->ev_sync, 0));
   }
   return EDL_OK;
 }
@@ -2291,7 +2392,7 @@ int Job::reshard_in_mp(const Event* ev) {
   Replica* r = peers_[me].rep;
   DeviceGuard g(r->device);
   MultiCopyArgs cp;
-  EDL_TRY(add_reshard_pieces(&cp, me, after, r));
+  EDL_TRY(add_reshard_copies(&cp, peers_, me, after, {}, r));
   EDL_TRY(multi_copy(cp, r->stream));
   CollArgs a;
   for (const auto& p : peers_) a.flags[a.n_dst++] = p.flags;
@@ -2358,50 +2459,7 @@ int Job::install_out_mp(Event* ev) {
       for (const auto& q : joiners) after.push_back(q);
       std::sort(after.begin(), after.end(),
                 [](const PeerRep& a, const PeerRep& b) { return a.rank < b.rank; });
-      // The newcomers' bf16 weights come from every source, in shares that even out each
-      // source's NVLink egress with the master pieces it also sends (every process computes
-      // the same split): source i sends the [wlo_i, whi_i) part, in units of 8 parameters, of
-      // the weights of all newcomers laid end to end.
-      const size_t p8 = P_ / 8, jn = joiners.size();
-      const int n_new = static_cast<int>(after.size());
-      std::vector<double> mb(n_src, 0.0);  // master (+ momentum) bytes source i sends
-      for (int i = 0; i < n_src; ++i)
-        for (int l = 0; l < L_; ++l) {
-          const size_t len8 = static_cast<size_t>(in_[l]) * out_[l] / 8;
-          size_t olo, ohi;
-          shard_range(len8, n_src, i, &olo, &ohi);
-          for (int j = 0; j < n_new; ++j) {
-            if (after[j].rank == peers_[i].rank) continue;
-            size_t nlo, nhi;
-            shard_range(len8, n_new, j, &nlo, &nhi);
-            const size_t a8 = std::max(olo, nlo), b8 = std::min(ohi, nhi);
-            if (b8 > a8) mb[i] += (b8 - a8) * 8.0 * (r->mom ? 8.0 : 4.0);
-          }
-        }
-      const double wtot = static_cast<double>(jn * p8) * 16.0;  // bytes of weights to ship
-      double sum_m = 0;
-      for (double m : mb) sum_m += m;
-      std::vector<double> quota(n_src);
-      double qsum = 0;
-      for (int i = 0; i < n_src; ++i) {
-        quota[i] = std::max(0.0, (wtot + sum_m) / n_src - mb[i]);
-        qsum += quota[i];
-      }
-      size_t wlo = 0, whi = 0, acc = 0;
-      for (int i = 0; i <= me; ++i) {
-        const size_t share = qsum > 0 ? static_cast<size_t>(quota[i] / qsum * (jn * p8))
-                                      : (jn * p8) / n_src;
-        wlo = acc;
-        acc = (i == n_src - 1) ? jn * p8 : std::min(jn * p8, acc + share);
-        whi = acc;
-      }
-      for (size_t pos = wlo; pos < whi;) {  // split the range at newcomer boundaries
-        const size_t q = pos / p8, off = pos % p8, end = std::min(whi, (q + 1) * p8);
-        const size_t lo = off * 8, n = (end - pos) * 8;
-        EDL_TRY(add_copy(&cp, joiners[q].W + lo, r->W + lo, sizeof(__nv_bfloat16) * n, r->stream));
-        pos = end;
-      }
-      EDL_TRY(add_reshard_pieces(&cp, me, after, r));
+      EDL_TRY(add_reshard_copies(&cp, peers_, me, after, joiners, r));
       EDL_TRY(multi_copy(cp, r->stream));  // SM stores over NVLink, one launch
       launches_ += 1;
     }

@@ -330,8 +330,12 @@ class Job {
   int install_out_mp(Event* ev);
   int reshard_in_mp(const Event* ev);
   int add_copy(MultiCopyArgs* cp, void* dst, const void* src, size_t bytes, cudaStream_t s);
-  int add_reshard_pieces(MultiCopyArgs* cp, int me, const std::vector<PeerRep>& after,
+  double reshard_piece_bytes(const std::vector<PeerRep>& old, int i,
+                             const std::vector<PeerRep>& after, bool mom) const;
+  int add_reshard_copies(MultiCopyArgs* cp, const std::vector<PeerRep>& old, int i,
+                         const std::vector<PeerRep>& after, const std::vector<PeerRep>& fresh,
                          Replica* r);
+  int reshard_local(const std::vector<PeerRep>& old, const std::vector<Replica*>& fresh);
   Worker* find_worker(const std::string& id) const;
   int my_rank_ = 0;
   std::vector<void*> ipc_mapped_;
