@@ -20,7 +20,6 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -358,7 +357,7 @@ def run_b200(args, rank: int, world: int) -> None:
                     "(weight gradient + fused SGD update, one launch per layer)",
                     "achieved": gbs, "peak": peak_h, "unit": "GB/s", "frac": gbs / peak_h,
                     "traffic": _ncu_traffic("wgrad+sgd") if w is WORKLOAD else None,
-                    "traffic_source": NCU_FULL,
+                    "traffic_source": NCU_STEP,
                     "algorithmic_bytes_per_launch": alg, "launch_ms": per_launch_ms,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)"}
     else:
@@ -687,15 +686,27 @@ def elastic_leg_mp(args, rank: int, world: int, local: int, dist) -> dict:
 
 
 NCU_FULL = "profiles/r01_ncu_full.md"
+NCU_STEP = "profiles/r02_kernel_shares.md"
 
 
 def _ncu_traffic(family: str):
-    """Mean DRAM read + write bytes per launch of a kernel family in the committed
-    ncu --set full capture (profiles/r01_ncu_full.md), or None."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), NCU_FULL)
+    """DRAM read + write bytes per launch of a kernel family: from the round-2 launch list
+    with caches not flushed between kernels (profiles/r02_kernel_shares.md, DRAM table: the
+    dirty lines a launch leaves in L2 are counted where they are written back), else the
+    round-1 `ncu --set full` capture (profiles/r01_ncu_full.md), or None."""
+    here = os.path.dirname(os.path.abspath(__file__))
+    try:
+        in_dram = False
+        for line in open(os.path.join(here, NCU_STEP)):
+            in_dram = in_dram or line.startswith("## DRAM traffic")
+            cells = [c.strip() for c in line.split("|")]
+            if in_dram and len(cells) == 7 and family in cells[1] and cells[2].isdigit():
+                return (float(cells[4]) + float(cells[5])) * 1e6 / int(cells[2])
+    except (OSError, ValueError):
+        pass
     vals = []
     try:
-        for line in open(path):
+        for line in open(os.path.join(here, NCU_FULL)):
             cells = [c.strip() for c in line.split("|")]
             if len(cells) > 5 and family in cells[2]:
                 vals.append((float(cells[4]) + float(cells[5])) * 1e6)

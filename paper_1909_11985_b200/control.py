@@ -176,8 +176,9 @@ def wid(rank: int) -> str:
 
 
 class ElasticGroup:
-    """One per process.  `ranks_of_ring`: process ranks whose workers form the initial ring
-    (worker ids w<rank>); the leader is the lowest rank of the current ring."""
+    """One per process.  `ring_ranks`: process ranks whose workers form the initial ring
+    (worker ids w<rank>).  The leader is the holder of `lease` (LeaderLease) when one is
+    given, else the lowest rank of the current ring."""
 
     def __init__(self, store, rank: int, ring_ranks, t_a_ms: float = 500.0, poll_every: int = 8,
                  prefix: str = "edl/", lease: "LeaderLease" = None, job_key: str = "job"):
@@ -202,9 +203,6 @@ class ElasticGroup:
     # ------------------------------------------------------------------ store helpers
     def _k(self, *parts) -> str:
         return self.p + "/".join(str(x) for x in parts)
-
-    def _has(self, key: str) -> bool:
-        return self.store.check([self._k(key) if not key.startswith(self.p) else key])
 
     def _get(self, key: str) -> bytes:
         return self.store.get(key)
