@@ -308,28 +308,37 @@ __global__ void barrier_kernel(CollArgs a) { cross_replica_barrier(a, 0); }
 // [c*len/n, (c+1)*len/n) folds ranks c, c+1, ... left to right, allreduce.cpp:132-148),
 // ordered loss sum, barrier, then sgd_step on the local replica (trainer.cpp:56-61).
 __global__ void linear_allreduce_sgd_kernel(LinearCollArgs a) {
+  // block b owns elements [b*256, (b+1)*256) of [grad_sum, count]; the per-block barrier
+  // slots make block b of every replica meet (same grid everywhere)
   if (a.n_rep > 1) cross_replica_barrier(a.flags, a.me, a.n_rep, a.epoch, 0);
   const int n = a.n_src;
   const size_t len = static_cast<size_t>(a.dim) + 1;
-  for (size_t i = threadIdx.x; i < len; i += blockDim.x) {
+  auto ring_sum = [&](size_t i) {  // chunk c = [c*len/n, (c+1)*len/n) folds c, c+1, ...
     int c = 0;
     while (c + 1 < n && len * static_cast<size_t>(c + 1) / static_cast<size_t>(n) <= i) ++c;
     double acc = a.g[c][i];
     for (int k = 1; k < n; ++k) acc = __dadd_rn(acc, a.g[(c + k) % n][i]);
-    a.total[i] = acc;
+    return acc;
+  };
+  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  double v = 0.0;
+  if (i < len) {
+    v = ring_sum(i);
+    a.total[i] = v;
   }
-  if (threadIdx.x == 0 && a.loss_out) {
+  // every block needs the global count (element dim): the same ring-order sum, recomputed
+  __shared__ double count;
+  if (threadIdx.x == 0) count = ring_sum(len - 1);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.loss_out) {
     double acc = 0.0;
     for (int k = 0; k < n; ++k) acc = __dadd_rn(acc, *a.losses[k]);
     *a.loss_out = acc;
   }
   __syncthreads();
   if (a.n_rep > 1) cross_replica_barrier(a.flags, a.me, a.n_rep, a.epoch, 1);
-  const double count = a.total[a.dim];
   if (count == 0.0) return;
   const double sc = __ddiv_rn(a.eta, count);
-  for (int i = threadIdx.x; i < a.dim; i += blockDim.x)
-    a.w[i] = __dsub_rn(a.w[i], __dmul_rn(sc, a.total[i]));
+  if (i < static_cast<size_t>(a.dim)) a.w[i] = __dsub_rn(a.w[i], __dmul_rn(sc, v));
 }
 
 __global__ void __launch_bounds__(256) master_allgather_kernel(CollArgs a) {
@@ -629,7 +638,9 @@ int allreduce_sgd(const CollArgs& a, cudaStream_t s) {
 
 int linear_allreduce_sgd(const LinearCollArgs& a, cudaStream_t s) {
   if (a.n_src < 1 || a.n_src > kCollMaxSources) return fail(EDL_EINVAL, "linear allreduce: sources");
-  linear_allreduce_sgd_kernel<<<1, 256, 0, s>>>(a);
+  const unsigned blocks = static_cast<unsigned>((a.dim + 1 + 255) / 256);
+  if (blocks > static_cast<unsigned>(kCollMaxBlocks)) return fail(EDL_EINVAL, "linear allreduce: dim");
+  linear_allreduce_sgd_kernel<<<blocks, 256, 0, s>>>(a);
   EDL_CUDA_TRY(cudaGetLastError());
   return EDL_OK;
 }

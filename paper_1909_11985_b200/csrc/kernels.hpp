@@ -39,10 +39,15 @@ int gather_inline(const Dataset* ds, const EdlRun* runs, int n_runs, int64_t n_r
                   void* y_out, double* zero, cudaStream_t stream);
 
 // ---- linear model, f64, bit-identical to trainer.cpp
+// scale_ws: nullptr (C-ABI: one fused launch) or [2n] doubles (job: scales, then z)
 int linear_local_gradient(int kind, const double* w, const double* x, const double* y, int64_t n,
                           int dim, double* grad_out, double* scale_ws, cudaStream_t s);
 int linear_batch_loss(int kind, const double* w, const double* x, const double* y, int64_t n,
                       int dim, double* loss_out, double* ws, cudaStream_t s);
+// batch_loss from the z = w . a_j a preceding linear_local_gradient(..., ws) left in ws + n
+// (same w: the loss and the gradient of one mini-batch, trainer.cpp:41-54)
+int linear_batch_loss_from_z(int kind, const double* z, const double* y, int64_t n,
+                             double* loss_out, cudaStream_t s);
 int linear_sgd(double* w, const double* g, int64_t count, double eta, int dim, cudaStream_t s);
 // Ring-order allreduce (ring_order_reduce semantics) over n buffers of len doubles.
 int ring_allreduce_f64(const double* const* inputs, int n, size_t len, int op, double* out,

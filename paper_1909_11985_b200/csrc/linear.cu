@@ -15,6 +15,7 @@
 // bit-exact parity gate on the C1 job, not for throughput (BASELINE.json configs[0]).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "edl_internal.hpp"
@@ -154,6 +155,174 @@ batch_loss_fused_kernel(int kind, const double* __restrict__ w, const double* __
   if (threadIdx.x == 0) *out = acc;
 }
 
+// Job-path variants: the same operation order, with the batch streamed through shared memory
+// by asynchronous copies (cp.async, a 4-deep ring) so the dependent f64 adds -- the reference
+// folds left to right, trainer.cpp:18-28 -- never wait on memory.  One warp per 32 samples
+// stages 32-row x 64-dim tiles and every lane folds its own sample's products in dimension
+// order: z_j = sum_i w_i a_ji exactly as the reference.  z is kept for the loss (batch_loss
+// uses the same w, trainer.cpp:41-54).
+constexpr int kZChunk = 64;
+constexpr int kZStages = 4;
+constexpr int kZRow = kZChunk + 1;  // padded row: lanes reading their own rows hit distinct banks
+constexpr size_t kZSmem = sizeof(double) * kZStages * (32 * kZRow + kZChunk);
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__global__ void __launch_bounds__(32)
+sample_scale_z_kernel(int kind, const double* __restrict__ w, const double* __restrict__ x,
+                      const double* __restrict__ y, int64_t n, int dim,
+                      double* __restrict__ scale, double* __restrict__ zout) {
+  extern __shared__ double zsm[];  // [kZStages][32][kZRow] tiles, then [kZStages][kZChunk] w
+  double* wst = zsm + kZStages * 32 * kZRow;
+  const int lane = threadIdx.x;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.x) * 32, j = j0 + lane;
+  const int rows = n - j0 < 32 ? static_cast<int>(n - j0) : 32;
+  const int n_chunks = (dim + kZChunk - 1) / kZChunk;
+  auto load = [&](int c) {
+    const int c0 = c * kZChunk, cw = dim - c0 < kZChunk ? dim - c0 : kZChunk;
+    double* t = zsm + (c % kZStages) * 32 * kZRow;
+    if (rows == 32 && cw == kZChunk) {  // full tile: plain strides, no index arithmetic
+      const double* src = x + j0 * dim + c0 + lane;
+#pragma unroll 8
+      for (int r = 0; r < 32; ++r) {
+        cp_async8(t + r * kZRow + lane, src + static_cast<int64_t>(r) * dim);
+        cp_async8(t + r * kZRow + lane + 32, src + static_cast<int64_t>(r) * dim + 32);
+      }
+    } else {
+      for (int idx = lane; idx < rows * cw; idx += 32) {
+        const int r = idx / cw, k = idx - r * cw;
+        cp_async8(t + r * kZRow + k, x + (j0 + r) * dim + c0 + k);
+      }
+    }
+    for (int k = lane; k < cw; k += 32) cp_async8(wst + (c % kZStages) * kZChunk + k, w + c0 + k);
+  };
+  for (int c = 0; c < kZStages - 1; ++c) {
+    if (c < n_chunks) load(c);
+    cp_async_commit();  // (empty groups keep the wait count uniform)
+  }
+  double z = 0.0;
+  for (int c = 0; c < n_chunks; ++c) {
+    if (c + kZStages - 1 < n_chunks) load(c + kZStages - 1);
+    cp_async_commit();
+    cp_async_wait<kZStages - 1>();  // chunk c has landed (this lane's copies)
+    __syncwarp();                   // ... and every lane's
+    const int cw = dim - c * kZChunk < kZChunk ? dim - c * kZChunk : kZChunk;
+    const double* t = zsm + (c % kZStages) * 32 * kZRow + lane * kZRow;
+    const double* ws = wst + (c % kZStages) * kZChunk;
+    if (cw == kZChunk) {  // full chunk: constant trip count, the loads run ahead of the adds
+      if (lane < rows) {
+#pragma unroll
+        for (int i = 0; i < kZChunk; ++i) z = __dadd_rn(z, __dmul_rn(ws[i], t[i]));
+      }
+    } else if (lane < rows) {
+      for (int i = 0; i < cw; ++i) z = __dadd_rn(z, __dmul_rn(ws[i], t[i]));
+    }
+    __syncwarp();  // the stage is refilled next iteration
+  }
+  if (j >= n) return;
+  double s;
+  if (kind == EDL_MODEL_LEAST_SQUARES) {
+    s = __dsub_rn(z, y[j]);
+  } else {
+    const double m = __dmul_rn(-y[j], z);
+    s = __ddiv_rn(-y[j], __dadd_rn(1.0, exp(-m)));
+  }
+  scale[j] = s;
+  zout[j] = z;
+}
+
+// g_i = sum_j s_j a_ji in draw order, 64 features per CTA (64 CTAs at dim 4096): 32-sample x
+// 64-feature tiles stream through a 4-deep cp.async ring, each lane folds its feature's column.
+constexpr int kFRows = 32;
+constexpr size_t kFSmem = sizeof(double) * kZStages * (kFRows * 64 + kFRows);
+
+__global__ void __launch_bounds__(64)
+feature_sum_wide_kernel(const double* __restrict__ x, const double* __restrict__ scale,
+                        int64_t n, int dim, double* __restrict__ g) {
+  extern __shared__ double fsm[];  // [kZStages][kFRows][64] tiles, then [kZStages][kFRows] s
+  double* sst = fsm + kZStages * kFRows * 64;
+  const int t = threadIdx.x;
+  const int f0 = blockIdx.x * 64, i = f0 + t;
+  const int fw = dim - f0 < 64 ? dim - f0 : 64;
+  const int n_chunks = static_cast<int>((n + kFRows - 1) / kFRows);
+  auto load = [&](int c) {
+    const int64_t r0 = static_cast<int64_t>(c) * kFRows;
+    const int rows = n - r0 < kFRows ? static_cast<int>(n - r0) : kFRows;
+    double* tile = fsm + (c % kZStages) * kFRows * 64;
+    if (fw == 64) {  // full-width column block: thread t copies column t of every row
+      const double* src = x + r0 * dim + f0 + t;
+#pragma unroll 8
+      for (int r = 0; r < rows; ++r) cp_async8(tile + r * 64 + t, src + static_cast<int64_t>(r) * dim);
+    } else {
+      for (int idx = t; idx < rows * fw; idx += 64) {
+        const int r = idx / fw, k = idx - r * fw;
+        cp_async8(tile + r * 64 + k, x + (r0 + r) * dim + f0 + k);
+      }
+    }
+    for (int r = t; r < rows; r += 64) cp_async8(sst + (c % kZStages) * kFRows + r, scale + r0 + r);
+  };
+  for (int c = 0; c < kZStages - 1; ++c) {
+    if (c < n_chunks) load(c);
+    cp_async_commit();
+  }
+  double acc = 0.0;
+  for (int c = 0; c < n_chunks; ++c) {
+    if (c + kZStages - 1 < n_chunks) load(c + kZStages - 1);
+    cp_async_commit();
+    cp_async_wait<kZStages - 1>();
+    __syncthreads();
+    const int64_t r0 = static_cast<int64_t>(c) * kFRows;
+    const int rows = n - r0 < kFRows ? static_cast<int>(n - r0) : kFRows;
+    const double* tile = fsm + (c % kZStages) * kFRows * 64 + t;
+    const double* ss = sst + (c % kZStages) * kFRows;
+    if (t < fw && rows == kFRows) {
+#pragma unroll
+      for (int r = 0; r < kFRows; ++r) acc = __dadd_rn(acc, __dmul_rn(ss[r], tile[r * 64]));
+    } else if (t < fw) {
+      for (int r = 0; r < rows; ++r) acc = __dadd_rn(acc, __dmul_rn(ss[r], tile[r * 64]));
+    }
+    __syncthreads();
+  }
+  if (i < dim && t < fw) g[i] = acc;
+  if (i == 0) g[dim] = static_cast<double>(n);
+}
+
+// batch_loss from the z of the gradient pass: per-sample terms in parallel, folded in draw
+// order by one thread (trainer.cpp:41-54).
+__global__ void __launch_bounds__(256)
+loss_from_z_kernel(int kind, const double* __restrict__ z, const double* __restrict__ y,
+                   int64_t n, double* __restrict__ out) {
+  __shared__ double lv[256];
+  double acc = 0.0;
+  for (int64_t j0 = 0; j0 < n; j0 += 256) {
+    const int64_t j = j0 + threadIdx.x;
+    if (j < n) {
+      if (kind == EDL_MODEL_LEAST_SQUARES) {
+        const double e = __dsub_rn(z[j], y[j]);
+        lv[threadIdx.x] = __dmul_rn(__dmul_rn(0.5, e), e);
+      } else {
+        lv[threadIdx.x] = log1p(exp(__dmul_rn(-y[j], z[j])));
+      }
+    }
+    __syncthreads();
+    const int m = n - j0 < 256 ? static_cast<int>(n - j0) : 256;
+    if (threadIdx.x == 0)
+      for (int k = 0; k < m; ++k) acc = __dadd_rn(acc, lv[k]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = acc;
+}
+
 struct PtrArray {
   const double* p[64];
 };
@@ -187,11 +356,22 @@ int linear_local_gradient(int kind, const double* w, const double* x, const doub
     EDL_CUDA_TRY(cudaGetLastError());
     return EDL_OK;
   }
-  if (n > 0) {
-    sample_scale_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(kind, w, x, y, n,
-                                                                               dim, scale_ws);
+  // scale_ws holds [n] per-sample scales then [n] dot products z (linear_batch_loss_from_z)
+  static std::atomic<uint64_t> attr_set{0};  // dynamic smem above 48 KB, once per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_set.load() >> dev & 1)) {
+    EDL_CUDA_TRY(cudaFuncSetAttribute(sample_scale_z_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kZSmem));
+    EDL_CUDA_TRY(cudaFuncSetAttribute(feature_sum_wide_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmem));
+    attr_set.fetch_or(1ull << dev);
   }
-  feature_sum_kernel<<<(dim + 127) / 128, 128, 0, s>>>(x, scale_ws, n, dim, grad_out);
+  if (n > 0) {
+    sample_scale_z_kernel<<<static_cast<unsigned>((n + 31) / 32), 32, kZSmem, s>>>(
+        kind, w, x, y, n, dim, scale_ws, scale_ws + n);
+  }
+  feature_sum_wide_kernel<<<(dim + 63) / 64, 64, kFSmem, s>>>(x, scale_ws, n, dim, grad_out);
   EDL_CUDA_TRY(cudaGetLastError());
   return EDL_OK;
 }
@@ -207,6 +387,13 @@ int linear_batch_loss(int kind, const double* w, const double* x, const double* 
     sample_loss_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, s>>>(kind, w, x, y, n,
                                                                               dim, ws);
   ordered_total_kernel<<<1, 1, 0, s>>>(ws, n, loss_out);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
+
+int linear_batch_loss_from_z(int kind, const double* z, const double* y, int64_t n,
+                             double* loss_out, cudaStream_t s) {
+  loss_from_z_kernel<<<1, 256, 0, s>>>(kind, z, y, n, loss_out);
   EDL_CUDA_TRY(cudaGetLastError());
   return EDL_OK;
 }

@@ -406,11 +406,14 @@ int Job::build_replica(Replica* r) {
     EDL_CUDA_TRY(cudaMemset(r->w, 0, sizeof(double) * dim));  // w0 = 0
     EDL_TRY(dalloc(&r->xb, static_cast<size_t>(rows) * dim));
     EDL_TRY(dalloc(&r->yb, static_cast<size_t>(rows)));
-    EDL_TRY(dalloc(&r->ws, static_cast<size_t>(rows) + 1));
+    EDL_TRY(dalloc(&r->ws, 2 * static_cast<size_t>(rows) + 1));  // scales, then z
     EDL_TRY(dalloc(&r->total, static_cast<size_t>(dim) + 1));
   }
   EDL_TRY(dalloc(&r->loss_sum, 1));
-  EDL_CUDA_TRY(cudaStreamSynchronize(r->stream));
+  // the cudaMemset calls above run on the legacy default stream, which does not order the
+  // replica's non-blocking streams (nor peers reading the flags): wait for all of them here.
+  // (A first mini-batch racing the xent counter's memset summed row losses too early.)
+  EDL_CUDA_TRY(cudaDeviceSynchronize());
   return EDL_OK;
 }
 
@@ -1335,7 +1338,7 @@ int Job::load_checkpoint(const std::string& path) {
       if (mlen == sizeof(float) * P_)
         EDL_CUDA_TRY(cudaMemcpy(r->mom, b.data() + mom_at, mlen, cudaMemcpyHostToDevice));
       else
-        EDL_CUDA_TRY(cudaMemset(r->mom, 0, sizeof(float) * P_));
+        EDL_CUDA_TRY(cudaMemsetAsync(r->mom, 0, sizeof(float) * P_, r->stream));
     }
   }
   lm_ = std::move(lm);
@@ -1681,8 +1684,7 @@ int Job::run_worker_linear(Worker* w, int slot) {
   EDL_TRY(linear_local_gradient(cfg_.model, r->w, r->xb, r->yb, rows, cfg_.data.dim, w->g, r->ws,
                                 r->stream));
   m = mark(slot, 3, m, r->stream);
-  EDL_TRY(linear_batch_loss(cfg_.model, r->w, r->xb, r->yb, rows, cfg_.data.dim, w->loss, r->ws,
-                            r->stream));
+  EDL_TRY(linear_batch_loss_from_z(cfg_.model, r->ws + rows, r->yb, rows, w->loss, r->stream));
   m = mark(slot, 2, m, r->stream);
   (void)m;
   if (w->delay_us > 0) {
