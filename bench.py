@@ -305,11 +305,13 @@ def run_b200(args, rank: int, world: int) -> None:
     peaks = measured_peaks()
     peak_t = peaks.get("bf16_tflops_sustained", 1354.1)
     peak_h = peaks.get("hbm_gbs", 6555.5)
+    # split master (the library's default, EDL_SPLIT_MASTER=0 turns it off): the fused update
+    # reads and writes the bf16 weights W and the low 16 bits of the fp32 master, 8 B/param;
+    # the fp32 master itself: 4 B read + 4 B write + 2 B bf16 weight write = 10 B/param
+    upd_bpp = 8 if os.environ.get("EDL_SPLIT_MASTER", "1") != "0" else 10
     if world == 1:
-        # update fused into the weight-gradient GEMM epilogues: 4 B master read + 4 B
-        # master write + 2 B bf16 weight write per parameter, inside the backward phase
         upd = {"bound": "hbm", "where": "fused into wgrad GEMM epilogue (backward phase)",
-               "bytes_per_step": 10 * P}
+               "bytes_per_param": upd_bpp, "bytes_per_step": upd_bpp * P}
     else:
         # allreduce bus bytes per GPU per direction (bf16 reduce-scatter + all-gather,
         # 2(N-1)/N x 2P); the exchange's halves are timed where they run
@@ -342,23 +344,25 @@ def run_b200(args, rank: int, world: int) -> None:
                    "kernel": "fused reduce-scatter + sharded SGD + all-gather over NVLink P2P"}
         upd["exchange_mode"] = mode
 
-    # ---- roofline of the dominant kernel (profiles/r01_kernel_shares.md): at N=1 the fused
-    # weight-gradient GEMM + SGD update (51% of the step), HBM-bound: per launch (one layer,
-    # SURVEY 8(d)'s 10 B/param update) 10 B x 16.8M params + its two bf16 operands
+    # ---- roofline of the dominant kernel (profiles/r02_kernel_shares.md): at N=1 the fused
+    # weight-gradient GEMM + SGD update (~45% of the step), HBM-bound: per launch (one layer)
+    # 8 B/param over the split master (10 B with the fp32 one) x 16.8M params + its two bf16
+    # operands
     # dY [b][4096] and X [b][4096]; duration = the wgrad sub-phase / 8 launches, CUDA events
     # on the job stream.  With several GPUs the weight-gradient GEMMs write bf16 gradients
     # (tensor-bound) and the update moves to the NVLink collective (update_roofline).
     n_wgrad = w["layers"]
     per_launch_ms = wgrad_ms / n_wgrad if wgrad_ms > 0 else float("nan")
     if world == 1:
-        alg = 10 * (P // n_wgrad) + 2 * 2 * w["batch"] * w["hidden"]
+        alg = upd_bpp * (P // n_wgrad) + 2 * 2 * w["batch"] * w["hidden"]
         gbs = alg / (per_launch_ms / 1e3) / 1e9
         dominant = {"bound": "hbm", "kernel": "gemm_bf16_2sm_kernel<128,MN,MN,sgd> "
                     "(weight gradient + fused SGD update, one launch per layer)",
                     "achieved": gbs, "peak": peak_h, "unit": "GB/s", "frac": gbs / peak_h,
                     "traffic": _ncu_traffic("wgrad+sgd") if w is WORKLOAD else None,
                     "traffic_source": NCU_STEP,
-                    "algorithmic_bytes_per_launch": alg, "launch_ms": per_launch_ms,
+                    "algorithmic_bytes_per_launch": alg, "bytes_per_param": upd_bpp,
+                    "launch_ms": per_launch_ms,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)"}
     else:
         tf = 2 * w["batch"] * (P // n_wgrad) / (per_launch_ms / 1e3) / 1e12

@@ -369,6 +369,19 @@ int edl_gemm_wgrad_sgd(const void* dy, int32_t ld_dy, const void* x, int32_t ld_
                        float* master, void* W, int32_t ldw, int32_t M, int32_t N, int32_t K,
                        float scale, void* stream);
 
+/* The same over the split master a single-replica job keeps: the fp32
+ * master m is stored as its bf16 rounding W (the weights the GEMMs read) plus lo, the low 16
+ * bits of m, so the update moves 8 B per parameter instead of 10.  mode 1: (W, lo) in and
+ * out; 2: (W, lo) in, the fp32 master + W out; 3: the fp32 master in, (W, lo) out (master
+ * may be NULL for mode 1).  edl_master_split writes W = RNE(m) and lo; edl_master_join
+ * rebuilds m.  The one lossy case: an m that RNE rounds up
+ * from an exact tie (low half 0x8000, odd high half) comes back one fp32 ulp larger.        */
+int edl_gemm_wgrad_sgd_split(const void* dy, int32_t ld_dy, const void* x, int32_t ld_x,
+                             uint16_t* lo, void* W, float* master, int32_t mode, int32_t ldw,
+                             int32_t M, int32_t N, int32_t K, float scale, void* stream);
+int edl_master_split(const float* master, uint16_t* lo, void* W, size_t n, void* stream);
+int edl_master_join(const void* W, const uint16_t* lo, float* master, size_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -173,6 +173,9 @@ def _declare(L: C.CDLL) -> None:
         "edl_job_gather_master": ([vp], ci),
         "edl_job_set_params": ([vp, vp, sz], ci),
         "edl_gemm_wgrad_sgd": ([vp, i32, vp, i32, vp, vp, i32, i32, i32, i32, C.c_float, vp], ci),
+        "edl_gemm_wgrad_sgd_split": ([vp, i32, vp, i32, vp, vp, vp, i32, i32, i32, i32, i32, C.c_float, vp], ci),
+        "edl_master_split": ([vp, vp, vp, C.c_size_t, vp], ci),
+        "edl_master_join": ([vp, vp, vp, C.c_size_t, vp], ci),
         "edl_detect_straggler": ([P(f64), i32, i32, i32, f64, P(i32)], ci),
         "edl_job_save_checkpoint": ([vp, cp], ci),
         "edl_job_load_checkpoint": ([vp, cp], ci),

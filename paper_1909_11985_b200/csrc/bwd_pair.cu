@@ -419,7 +419,7 @@ bool gemm_pair_enabled() {
 bool gemm_pair_eligible(const GemmPlan& d, const GemmPlan& w) {
   return d.cg == 2 && d.bn == 128 && d.sk == 1 && !d.a_mn && d.b_mn && d.ep.mask &&
          !d.ep.out_f32 && !d.ep.relu && (d.mc == 1 || d.mc == 2) && d.M % 256 == 0 &&
-         d.N % 128 == 0 && d.K % kBK == 0 && w.ep.sgd && !w.ep.xchg && w.cg == 2 &&
+         d.N % 128 == 0 && d.K % kBK == 0 && w.ep.sgd && !w.ep.xchg && !w.lo && w.cg == 2 &&
          w.bn == 128 && w.mc == 1 && w.a_mn && w.b_mn && w.M % 256 == 0 && w.N % 128 == 0 &&
          w.K % kBK == 0;
 }

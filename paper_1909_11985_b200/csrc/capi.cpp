@@ -239,6 +239,12 @@ int edl_sgd_step(double* w, const double* g, int64_t count, double eta, int32_t 
                  void* stream) {
   return edl::linear_sgd(w, g, count, eta, dim, S(stream));
 }
+int edl_master_split(const float* master, uint16_t* lo, void* W, size_t n, void* stream) {
+  return edl::master_split(master, lo, static_cast<__nv_bfloat16*>(W), n, S(stream));
+}
+int edl_master_join(const void* W, const uint16_t* lo, float* master, size_t n, void* stream) {
+  return edl::master_join(static_cast<const __nv_bfloat16*>(W), lo, master, n, S(stream));
+}
 int edl_ring_allreduce_f64(const double* const* inputs, int32_t n, size_t len, int32_t op,
                            double* out, void* stream) {
   return edl::ring_allreduce_f64(inputs, n, len, op, out, S(stream));

@@ -81,6 +81,10 @@ struct GemmPlan {
   int M = 0, N = 0, K = 0, a_mn = 0, b_mn = 0, bn = 0, cg = 1;
   int mc = 1;  // CTA-pair kernel: pairs per cluster sharing A by TMA multicast (1 or 2)
   int sk = 1;  // CTA-pair kernel: 2 = split-K over two pairs, 256-wide tiles (gemm_sm100.cu)
+  // fused-SGD plan over the split master (tm: the 16-bit low halves, pm.m[0]: the fp32
+  // master): 1 = split in / out, 2 = split in, fp32 out, 3 = fp32 in, split out
+  int lo = 0;
+  bool lo_master = false;  // pm.m[0] is set (modes 2 and 3 allowed)
   EpiParams ep{};
 };
 int gemm_plan_init(GemmPlan* p, const void* A, int lda, int a_mn, const void* B, int ldb,
@@ -97,6 +101,12 @@ int gemm_plan_run_wait(const GemmPlan& p, cudaStream_t stream, const uint32_t* f
 // W (bf16) <- master, with no gradient buffer round trip through HBM.
 int gemm_plan_init_sgd(GemmPlan* p, const void* A, int lda, int a_mn, const void* B, int ldb,
                        int b_mn, float* master, __nv_bfloat16* W, int ldw, int M, int N, int K);
+// The same over the split master: the fp32 master m is kept as its bf16 rounding W (the
+// weights the GEMMs read) plus the low 16 bits of m (lo): 8 B per parameter per update
+// instead of 10 (gemm_sm100.cu; master_split_lo / master_join_lo convert).
+int gemm_plan_init_sgd_lo(GemmPlan* p, const void* A, int lda, const void* B, int ldb,
+                          uint16_t* lo, __nv_bfloat16* W, float* master, int ldw, int M, int N,
+                          int K);
 int gemm_pick_bn(int M, int N, bool b_mn);
 // Backward pair (bwd_pair.cu): the dgrad plan of layer l-1 (CTA pair, N tile 128, relu'
 // mask, bf16 out) and the fused wgrad + SGD plan of layer l in one persistent launch.

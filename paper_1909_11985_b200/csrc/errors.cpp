@@ -53,3 +53,17 @@ extern "C" int edl_gemm_wgrad_sgd(const void* dy, int32_t ld_dy, const void* x, 
   if (rc) return rc;
   return edl::gemm_plan_run(p, static_cast<cudaStream_t>(stream), scale);
 }
+
+extern "C" int edl_gemm_wgrad_sgd_split(const void* dy, int32_t ld_dy, const void* x,
+                                        int32_t ld_x, uint16_t* lo, void* W, float* master,
+                                        int32_t mode, int32_t ldw, int32_t M, int32_t N,
+                                        int32_t K, float scale, void* stream) {
+  if (mode < 1 || mode > 3 || (mode != 1 && !master))
+    return edl::fail(EDL_EINVAL, "split-master SGD: mode 1..3 (2 and 3 need the fp32 master)");
+  edl::GemmPlan p;
+  int rc = edl::gemm_plan_init_sgd_lo(&p, dy, ld_dy, x, ld_x, lo, static_cast<__nv_bfloat16*>(W),
+                                      master, ldw, M, N, K);
+  if (rc) return rc;
+  p.lo = mode;
+  return edl::gemm_plan_run(p, static_cast<cudaStream_t>(stream), scale);
+}

@@ -319,7 +319,7 @@ __device__ unsigned long long g_gemm_tl[296][16];
 #define TL(slot)
 #endif
 
-template <int BN, bool kSgd = false>
+template <int BN, bool kSgd = false, int kLo = 0>
 struct Cfg2 {
   static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "2-SM tiles: BN multiple of 64");
   static constexpr int kHalfN = BN / 2;
@@ -345,11 +345,18 @@ struct Cfg2 {
 #define EDL_SGD_WDIRECT 0
 #endif
   static constexpr bool kWDirect = kSgd && EDL_SGD_WDIRECT;
-  static constexpr uint32_t kSgdBufBytes = (kWDirect ? 2 : 3) * kEpiChunkBytes;
+  // split master (kLo, see the kernel): a buffer holds 2 x 4 KB (low halves + weights in,
+  // or fp32 master in, low halves + weights out); kLo = 2 (split in, fp32 master + weights
+  // out) needs 3 x 4 KB
+  static constexpr uint32_t kSgdBufBytes =
+      (kLo == 1 || kLo == 3 || kWDirect ? 2 : 3) * kEpiChunkBytes;
+#ifndef EDL_SGD_LO_BUFS
+#define EDL_SGD_LO_BUFS 1
+#endif
 #ifdef EDL_SGD_BUFS
   static constexpr int kSgdBufs = EDL_SGD_BUFS;
 #else
-  static constexpr int kSgdBufs = kEpiWarps == 8 && !kWDirect ? 1 : 2;
+  static constexpr int kSgdBufs = kLo ? EDL_SGD_LO_BUFS : (kEpiWarps == 8 && !kWDirect ? 1 : 2);
 #endif
   // master prefetch distance in chunks (1 .. kSgdBufs - 1)
 #ifdef EDL_SGD_PFD
@@ -380,14 +387,22 @@ struct Cfg2 {
 // mainloop each CTA owns one column half of the tile: it sends the other half of its fp32
 // partial to the matching CTA of the other pair through DSMEM (into that CTA's idle stage
 // buffers), receives that CTA's partial of its own half, adds, and runs the epilogue.
-template <int BN, bool A_MN, bool B_MN, bool kSgd, int kMc, int kSk = 1, bool kX = false>
-__global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
+template <int BN, bool A_MN, bool B_MN, bool kSgd, int kMc, int kSk = 1, bool kX = false,
+          int kLo = 0>
+__global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                          const __grid_constant__ CUtensorMap tmap_b,
                          const __grid_constant__ CUtensorMap tmap_c,
                          const __grid_constant__ CUtensorMap tmap_m, int M, int N, int K,
                          EpiParams ep, const __grid_constant__ PeerMaps pm) {
-  using C = Cfg2<BN, kSgd>;
+  using C = Cfg2<BN, kSgd, kLo>;
+  // kLo (fused SGD over the split master, tmap_m = the 16-bit low halves lo, pm.m[0] = the
+  // fp32 master): 1 = (W, lo) in and out; 2 = (W, lo) in, fp32 master + W out (the last
+  // mini-batch before a switch to another update path); 3 = fp32 master in, (W, lo) out
+  // (the first fused mini-batch after one)
+  static_assert(kLo == 0 || (kSgd && !kX && !C::kWDirect), "split master: fused-SGD plans");
+  constexpr bool kLoIn = kLo == 1 || kLo == 2;
+  constexpr bool kLoOut = kLo == 1 || kLo == 3;
   static_assert(kSk == 1 || (kSk == 2 && kMc == 1 && !kSgd && BN == 256),
                 "split-K: 256-wide plain tiles, no multicast");
   static_assert(!kX || (kSgd && kMc == 1 && kSk == 1), "fused exchange: fused-SGD plans");
@@ -652,8 +667,16 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
       if (!coords(j, &r0, &c0)) return;
       uint8_t* dst = wbase + (j % NB) * C::kSgdBufBytes;
       mbar_arrive_expect_tx(&mb[j % NB], 2 * kEpiChunkBytes);
-      tma_load_2d(dst, &tmap_m, &mb[j % NB], c0, r0);
-      tma_load_2d(dst + kEpiChunkBytes, &tmap_m, &mb[j % NB], c0 + 32, r0);
+      if constexpr (kLoIn) {  // low master halves (16-bit, 64-column box) + bf16 weights
+        tma_load_2d(dst, &tmap_m, &mb[j % NB], c0, r0);
+        tma_load_2d(dst + kEpiChunkBytes, &tmap_c, &mb[j % NB], c0, r0);
+      } else if constexpr (kLo == 3) {  // fp32 master through the plan's second map
+        tma_load_2d(dst, &pm.m[0], &mb[j % NB], c0, r0);
+        tma_load_2d(dst + kEpiChunkBytes, &pm.m[0], &mb[j % NB], c0 + 32, r0);
+      } else {
+        tma_load_2d(dst, &tmap_m, &mb[j % NB], c0, r0);
+        tma_load_2d(dst + kEpiChunkBytes, &tmap_m, &mb[j % NB], c0 + 32, r0);
+      }
     };
     // L2 prefetch of this warp's 32 master rows of tile t (BN columns, 32-column boxes): the
     // master stream is the kernel's HBM traffic, and pf_tiles tiles of lead time keep enough
@@ -662,8 +685,16 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
       if (t >= num_work) return;
       const int r0 = tile_m(t) * 256 + static_cast<int>(pr) * 128 + q * 32;
       const int c0 = tile_n(t) * BN + half * (BN / kHalves);
+      if constexpr (kLoIn) {  // 64-column boxes of the low halves and of the weights
 #pragma unroll
-      for (int c = 0; c < BN / kHalves; c += 32) tma_prefetch_2d(&tmap_m, c0 + c, r0);
+        for (int c = 0; c < BN / kHalves; c += 64) {
+          tma_prefetch_2d(&tmap_m, c0 + c, r0);
+          tma_prefetch_2d(&tmap_c, c0 + c, r0);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < BN / kHalves; c += 32) tma_prefetch_2d(&tmap_m, c0 + c, r0);
+      }
     };
     if (lane == 0) {
       for (int i = 0; i < ep.pf_tiles && !kX; ++i) l2_prefetch_tile(unit + i * n_units);
@@ -818,6 +849,115 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
         ++n_used;
         if (warp == 2) TRACE_ADD(7, t_ml);
         TRACE_T0(t_cs);
+        if constexpr (kLo != 0) {
+          // split master: m = (hi << 16) | lo with hi = W - (lo > 0x8000) (W = RNE(m)).  The
+          // update is the fp32 one; W' = RNE(m') and lo' = the low half of m', except a tie RNE
+          // rounds up (low half 0x8000, odd high half) is stored as 0x8001 (one fp32 ulp) so
+          // the decode stays unambiguous.  Each lane reads its whole row into g (g <- m'),
+          // then writes it: the output layout reuses the input rows in place.
+          uint8_t* r0b = buf + lane * 128;  // the lane's row in 4 KB block 0 (+ k * 4 KB)
+          if constexpr (kLo == 1) {  // in place, 8 columns at a time (fewest live registers)
+#pragma unroll
+            for (int j8 = 0; j8 < 8; ++j8) {
+              const int off = (j8 ^ (lane & 7)) << 4;
+              uint4* pl = reinterpret_cast<uint4*>(r0b + off);
+              uint4* pw = reinterpret_cast<uint4*>(r0b + kEpiChunkBytes + off);
+              const uint4 lv = *pl, wv = *pw;
+              const uint32_t wi[4] = {wv.x, wv.y, wv.z, wv.w};
+              const uint32_t li[4] = {lv.x, lv.y, lv.z, lv.w};
+              uint32_t wo[4], lo[4];
+#pragma unroll
+              for (int q2 = 0; q2 < 4; ++q2) {
+                uint32_t m0 = __byte_perm(li[q2], wi[q2], 0x5410);  // W0 << 16 | lo0
+                uint32_t m1 = __byte_perm(li[q2], wi[q2], 0x7632);  // W1 << 16 | lo1
+                m0 -= ((m0 & 0xFFFFu) + 0x7FFFu) & 0x10000u;        // hi -= (lo > 0x8000)
+                m1 -= ((m1 & 0xFFFFu) + 0x7FFFu) & 0x10000u;
+                const float f0 =
+                    __fsub_rn(__uint_as_float(m0), __fmul_rn(ep.scale, g[8 * j8 + 2 * q2]));
+                const float f1 =
+                    __fsub_rn(__uint_as_float(m1), __fmul_rn(ep.scale, g[8 * j8 + 2 * q2 + 1]));
+                wo[q2] = pack_bf16(f0, f1);
+                uint32_t b0 = __float_as_uint(f0), b1 = __float_as_uint(f1);
+                b0 |= (b0 & 0x1FFFFu) == 0x18000u ? 1u : 0u;  // rounded-up tie -> lo 0x8001
+                b1 |= (b1 & 0x1FFFFu) == 0x18000u ? 1u : 0u;
+                lo[q2] = __byte_perm(b0, b1, 0x5410);
+              }
+              *pl = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+              *pw = make_uint4(wo[0], wo[1], wo[2], wo[3]);
+            }
+          } else if constexpr (kLoIn) {
+#pragma unroll
+            for (int j8 = 0; j8 < 8; ++j8) {
+              const int off = (j8 ^ (lane & 7)) << 4;
+              const uint4 lv = *reinterpret_cast<const uint4*>(r0b + off);
+              const uint4 wv = *reinterpret_cast<const uint4*>(r0b + kEpiChunkBytes + off);
+              const uint32_t wi[4] = {wv.x, wv.y, wv.z, wv.w};
+              const uint32_t li[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+              for (int q2 = 0; q2 < 4; ++q2) {
+                uint32_t m0 = __byte_perm(li[q2], wi[q2], 0x5410);  // W0 << 16 | lo0
+                uint32_t m1 = __byte_perm(li[q2], wi[q2], 0x7632);  // W1 << 16 | lo1
+                m0 -= ((m0 & 0xFFFFu) + 0x7FFFu) & 0x10000u;        // hi -= (lo > 0x8000)
+                m1 -= ((m1 & 0xFFFFu) + 0x7FFFu) & 0x10000u;
+                float* gg = &g[8 * j8 + 2 * q2];
+                gg[0] = __fsub_rn(__uint_as_float(m0), __fmul_rn(ep.scale, gg[0]));
+                gg[1] = __fsub_rn(__uint_as_float(m1), __fmul_rn(ep.scale, gg[1]));
+              }
+            }
+          } else {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int k4 = 0; k4 < 8; ++k4) {
+                const float4 m = *reinterpret_cast<const float4*>(
+                    r0b + h * kEpiChunkBytes + ((k4 ^ (lane & 7)) << 4));
+                float* gg = &g[h * 32 + k4 * 4];
+                gg[0] = __fsub_rn(m.x, __fmul_rn(ep.scale, gg[0]));
+                gg[1] = __fsub_rn(m.y, __fmul_rn(ep.scale, gg[1]));
+                gg[2] = __fsub_rn(m.z, __fmul_rn(ep.scale, gg[2]));
+                gg[3] = __fsub_rn(m.w, __fmul_rn(ep.scale, gg[3]));
+              }
+          }
+          if constexpr (kLo == 1) {
+            // written above
+          } else if constexpr (kLoOut) {  // lo' -> block 0, W' -> block 1
+#pragma unroll
+            for (int j8 = 0; j8 < 8; ++j8) {
+              const int off = (j8 ^ (lane & 7)) << 4;
+              uint32_t wo[4], lo[4];
+#pragma unroll
+              for (int q2 = 0; q2 < 4; ++q2) {
+                const float f0 = g[8 * j8 + 2 * q2], f1 = g[8 * j8 + 2 * q2 + 1];
+                wo[q2] = pack_bf16(f0, f1);
+                uint32_t b0 = __float_as_uint(f0), b1 = __float_as_uint(f1);
+                b0 |= (b0 & 0x1FFFFu) == 0x18000u ? 1u : 0u;  // rounded-up tie -> lo 0x8001
+                b1 |= (b1 & 0x1FFFFu) == 0x18000u ? 1u : 0u;
+                lo[q2] = __byte_perm(b0, b1, 0x5410);
+              }
+              *reinterpret_cast<uint4*>(r0b + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+              *reinterpret_cast<uint4*>(r0b + kEpiChunkBytes + off) =
+                  make_uint4(wo[0], wo[1], wo[2], wo[3]);
+            }
+          } else {  // fp32 master -> blocks 0 / 1 (32 columns each), W' -> block 2
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int k4 = 0; k4 < 8; ++k4) {
+                const float* gg = &g[h * 32 + k4 * 4];
+                *reinterpret_cast<float4*>(r0b + h * kEpiChunkBytes + ((k4 ^ (lane & 7)) << 4)) =
+                    make_float4(gg[0], gg[1], gg[2], gg[3]);
+              }
+#pragma unroll
+            for (int j8 = 0; j8 < 8; ++j8) {
+              uint4 o;
+              o.x = pack_bf16(g[8 * j8 + 0], g[8 * j8 + 1]);
+              o.y = pack_bf16(g[8 * j8 + 2], g[8 * j8 + 3]);
+              o.z = pack_bf16(g[8 * j8 + 4], g[8 * j8 + 5]);
+              o.w = pack_bf16(g[8 * j8 + 6], g[8 * j8 + 7]);
+              *reinterpret_cast<uint4*>(r0b + 2 * kEpiChunkBytes + ((j8 ^ (lane & 7)) << 4)) = o;
+            }
+          }
+        } else {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint8_t* mrow = buf + h * kEpiChunkBytes + lane * 128;
@@ -837,9 +977,12 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
             g[h * 32 + k4 * 4 + 3] = m.w;
           }
         }
+        }
         if (warp == 2) TRACE_ADD(11, t_cs);
         TRACE_T0(t_w8);
-        if constexpr (C::kWDirect) {
+        if constexpr (kLo != 0) {
+          // outputs staged above
+        } else if constexpr (C::kWDirect) {
           int r0, c0;
           coords(j, &r0, &c0);
           uint4* wp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.C) +
@@ -872,9 +1015,18 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd>::kThreads2, 1)
         if (lane == 0) {
           int r0, c0;
           coords(j, &r0, &c0);
-          tma_store_2d(&tmap_m, buf, c0, r0);
-          tma_store_2d(&tmap_m, buf + kEpiChunkBytes, c0 + 32, r0);
-          if (!C::kWDirect) tma_store_2d(&tmap_c, buf + 2 * kEpiChunkBytes, c0, r0);
+          if constexpr (kLoOut) {
+            tma_store_2d(&tmap_m, buf, c0, r0);
+            tma_store_2d(&tmap_c, buf + kEpiChunkBytes, c0, r0);
+          } else if constexpr (kLo == 2) {
+            tma_store_2d(&pm.m[0], buf, c0, r0);
+            tma_store_2d(&pm.m[0], buf + kEpiChunkBytes, c0 + 32, r0);
+            tma_store_2d(&tmap_c, buf + 2 * kEpiChunkBytes, c0, r0);
+          } else {
+            tma_store_2d(&tmap_m, buf, c0, r0);
+            tma_store_2d(&tmap_m, buf + kEpiChunkBytes, c0 + 32, r0);
+            if (!C::kWDirect) tma_store_2d(&tmap_c, buf + 2 * kEpiChunkBytes, c0, r0);
+          }
           if (kX) {  // all-gather: the updated weights into every other replica
             for (int o = 0; o < ep.x_n; ++o)
               if (o != ep.route_me && !(ep.dbg & 8))  // EDL_GEMM_DBG=8: diagnostics only
@@ -1162,11 +1314,11 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
 // prepare_only: set the kernel's attributes on the current device and query its cluster
 // occupancy (this also loads the function), without launching -- gemm_prepare_device()
 template <int BN, bool A_MN, bool B_MN, bool kSgd = false, int kMc = 1, int kSk = 1,
-          bool kX = false>
+          bool kX = false, int kLo = 0>
 int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream, float scale = 0.f,
                     bool prepare_only = false) {
-  using Cf = Cfg2<BN, kSgd>;
-  auto kern = gemm_bf16_2sm_kernel<BN, A_MN, B_MN, kSgd, kMc, kSk, kX>;
+  using Cf = Cfg2<BN, kSgd, kLo>;
+  auto kern = gemm_bf16_2sm_kernel<BN, A_MN, B_MN, kSgd, kMc, kSk, kX, kLo>;
   constexpr int kCl = 2 * kMc * kSk;  // CTAs per cluster
   // per device: the attribute lives in each context.  Atomic: a newcomer's replica is
   // prepared on a side thread while the step thread launches on the other devices.
@@ -1432,6 +1584,9 @@ int gemm_prepare_device() {
   if (!rc) rc = launch_gemm_2sm<128, false, true, false, 2>(p, nullptr, 0.f, true);
   if (!rc) rc = launch_gemm_2sm<128, true, true, false, 1>(p, nullptr, 0.f, true);
   if (!rc) rc = launch_gemm_2sm<128, true, true, true, 1>(p, nullptr, 0.f, true);
+  if (!rc) rc = launch_gemm_2sm<128, true, true, true, 1, 1, false, 1>(p, nullptr, 0.f, true);
+  if (!rc) rc = launch_gemm_2sm<128, true, true, true, 1, 1, false, 2>(p, nullptr, 0.f, true);
+  if (!rc) rc = launch_gemm_2sm<128, true, true, true, 1, 1, false, 3>(p, nullptr, 0.f, true);
   if (!rc) rc = launch_gemm_2sm<128, false, false, false, 1>(p, nullptr, 0.f, true);
   if (!rc) rc = launch_gemm_2sm<128, false, true, false, 1>(p, nullptr, 0.f, true);
   if (!rc) rc = gemm_pair_prepare_device(nullptr);
@@ -1477,6 +1632,25 @@ int gemm_plan_init_sgd(GemmPlan* p, const void* A, int lda, int a_mn, const void
   return EDL_OK;
 }
 
+int gemm_plan_init_sgd_lo(GemmPlan* p, const void* A, int lda, const void* B, int ldb,
+                          uint16_t* lo, __nv_bfloat16* W, float* master, int ldw, int M, int N,
+                          int K) {
+  if (M <= 0 || N <= 0 || K <= 0 || (ldw * 2) % 16) return fail(EDL_EINVAL, "split-master SGD: shape");
+  int rc = gemm_plan_init(p, A, lda, 1, B, ldb, 1, W, ldw, M, N, K, 0, 0, nullptr, 0, 1128);
+  if (rc) return rc;
+  p->mc = 1;
+  rc = make_tmap_t(&p->tm, lo, M, N, ldw, 64, 32, false);
+  if (rc) return fail(rc, "split-master SGD: tensor map of the low halves");
+  if (master) {  // the conversion launches (gemm_plan_lo_mode 2 / 3) read or write it
+    rc = make_tmap_t(&p->pm.m[0], master, M, N, ldw, 32, 32, true);
+    if (rc) return fail(rc, "split-master SGD: tensor map of the fp32 master");
+  }
+  p->ep.sgd = 1;
+  p->lo = 1;
+  p->lo_master = master != nullptr;
+  return EDL_OK;
+}
+
 int gemm_plan_run(const GemmPlan& p, cudaStream_t stream, float sgd_scale) {
   const int a_mn = p.a_mn, b_mn = p.b_mn;
   if (p.ep.sgd) {
@@ -1484,6 +1658,13 @@ int gemm_plan_run(const GemmPlan& p, cudaStream_t stream, float sgd_scale) {
       return fail(EDL_EINVAL, "gemm: fused SGD plans are CTA-pair, N tile 128/256, MN-major A/B");
     // opt-in (EDL_SGD_BRES=1): the B-resident kernel (wgrad_sgd.cu) streams ~1/3 fewer
     // operand bytes per parameter; measured slower, the epilogue bounds this GEMM
+    if (p.lo) {
+      if (p.bn != 128 || p.mc != 1 || p.ep.xchg) return fail(EDL_EINVAL, "gemm: split-master plan shape");
+      if (p.lo != 1 && !p.lo_master) return fail(EDL_EINVAL, "gemm: split-master conversion needs the fp32 master");
+      if (p.lo == 2) return launch_gemm_2sm<128, true, true, true, 1, 1, false, 2>(p, stream, sgd_scale);
+      if (p.lo == 3) return launch_gemm_2sm<128, true, true, true, 1, 1, false, 3>(p, stream, sgd_scale);
+      return launch_gemm_2sm<128, true, true, true, 1, 1, false, 1>(p, stream, sgd_scale);
+    }
     if (wgrad_sgd_bres_eligible(p)) return wgrad_sgd_bres_run(p, stream, sgd_scale);
     if (p.ep.xchg) {
       if (p.bn != 128 || p.mc != 1) return fail(EDL_EINVAL, "gemm: fused-exchange plan shape");

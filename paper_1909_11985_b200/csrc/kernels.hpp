@@ -73,6 +73,10 @@ int sum_rows(const float* row_loss, int rows, double* loss_out, cudaStream_t s);
 //   mu != 0:  v = mu*v + sum(g)*inv_count;  master -= eta * v
 // bf16 working copy of an fp32 master (checkpoint restore).
 int master_to_bf16(const float* master, __nv_bfloat16* w, size_t n, cudaStream_t s);
+// split master: W = RNE(m) and lo = low 16 bits of m (m: fp32 master); join: m from (W, lo)
+int master_split(const float* master, uint16_t* lo, __nv_bfloat16* w, size_t n, cudaStream_t s);
+int master_join(const __nv_bfloat16* w, const uint16_t* lo, float* master, size_t n,
+                cudaStream_t s);
 // current device: load the step's kernels now (lazy module loading would otherwise put it on
 // the first mini-batch a newly added GPU runs -- the scale-out switch step)
 int mlp_prepare_device();

@@ -208,13 +208,94 @@ __global__ void master_to_bf16_kernel(const float* __restrict__ m, __nv_bfloat16
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
     w[i] = __float2bfloat16_rn(m[i]);
 }
+// split master (gemm_plan_init_sgd_lo): m <-> (W = RNE(m), lo = low 16 bits of m).  A tie
+// that RNE rounds up (lo = 0x8000, odd high half) is stored as lo = 0x8001 (one fp32 ulp
+// above m, the same W), so hi = W - (lo > 0x8000) recovers the high half.
+__device__ __forceinline__ uint32_t split_lo_bits(uint32_t mb) {
+  const uint32_t l = mb & 0xFFFFu;
+  return (l == 0x8000u && (mb & 0x10000u)) ? 0x8001u : l;
+}
+__device__ __forceinline__ float join_lo(uint32_t wb, uint32_t lb) {
+  return __uint_as_float(((wb - (lb > 0x8000u ? 1u : 0u)) << 16) | lb);
+}
+// 8 values per thread per iteration (32 B of master, 16 B of W, 16 B of lo), scalar tail
+__global__ void master_split_kernel(const float* __restrict__ m, uint16_t* __restrict__ lo,
+                                    __nv_bfloat16* __restrict__ w, size_t n) {
+  const size_t n8 = n / 8;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n8; i += stride) {
+    const float4 a = reinterpret_cast<const float4*>(m)[2 * i];
+    const float4 b = reinterpret_cast<const float4*>(m)[2 * i + 1];
+    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t wo[4], lw[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+      wo[k] = *reinterpret_cast<uint32_t*>(&h);
+      lw[k] = split_lo_bits(__float_as_uint(v[2 * k])) |
+              (split_lo_bits(__float_as_uint(v[2 * k + 1])) << 16);
+    }
+    reinterpret_cast<uint4*>(w)[i] = make_uint4(wo[0], wo[1], wo[2], wo[3]);
+    reinterpret_cast<uint4*>(lo)[i] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+  }
+  if (blockIdx.x == 0)
+    for (size_t i = n8 * 8 + threadIdx.x; i < n; i += blockDim.x) {
+      w[i] = __float2bfloat16_rn(m[i]);
+      lo[i] = static_cast<uint16_t>(split_lo_bits(__float_as_uint(m[i])));
+    }
+}
+__global__ void master_join_kernel(const __nv_bfloat16* __restrict__ w,
+                                   const uint16_t* __restrict__ lo, float* __restrict__ m,
+                                   size_t n) {
+  const size_t n8 = n / 8;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n8; i += stride) {
+    const uint4 wv = reinterpret_cast<const uint4*>(w)[i];
+    const uint4 lv = reinterpret_cast<const uint4*>(lo)[i];
+    const uint32_t wi[4] = {wv.x, wv.y, wv.z, wv.w}, li[4] = {lv.x, lv.y, lv.z, lv.w};
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[2 * k] = join_lo(wi[k] & 0xFFFFu, li[k] & 0xFFFFu);
+      v[2 * k + 1] = join_lo(wi[k] >> 16, li[k] >> 16);
+    }
+    reinterpret_cast<float4*>(m)[2 * i] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(m)[2 * i + 1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+  if (blockIdx.x == 0)
+    for (size_t i = n8 * 8 + threadIdx.x; i < n; i += blockDim.x)
+      m[i] = join_lo(__bfloat16_as_ushort(w[i]), lo[i]);
+}
 }  // namespace
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int master_split(const float* master, uint16_t* lo, __nv_bfloat16* w, size_t n, cudaStream_t s) {
+  if (n == 0) return EDL_OK;
+  if (!aligned16(master) || !aligned16(lo) || !aligned16(w))
+    return fail(EDL_EINVAL, "master split: buffers must be 16-byte aligned");
+  master_split_kernel<<<148 * 8, 256, 0, s>>>(master, lo, w, n);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
+
+int master_join(const __nv_bfloat16* w, const uint16_t* lo, float* master, size_t n,
+                cudaStream_t s) {
+  if (n == 0) return EDL_OK;
+  if (!aligned16(master) || !aligned16(lo) || !aligned16(w))
+    return fail(EDL_EINVAL, "master join: buffers must be 16-byte aligned");
+  master_join_kernel<<<148 * 8, 256, 0, s>>>(w, lo, master, n);
+  EDL_CUDA_TRY(cudaGetLastError());
+  return EDL_OK;
+}
 
 int mlp_prepare_device() {
   cudaFuncAttributes fa;
   EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, xent_kernel<16>));
   EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, xent_kernel<64>));
   EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, master_to_bf16_kernel));
+  EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, master_split_kernel));
+  EDL_CUDA_TRY(cudaFuncGetAttributes(&fa, master_join_kernel));
   return EDL_OK;
 }
 

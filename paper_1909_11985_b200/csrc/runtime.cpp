@@ -59,6 +59,16 @@ int dalloc(T** p, size_t count) {
     if (_rc != EDL_OK) return _rc; \
   } while (0)
 
+// EDL_SPLIT_MASTER=0 keeps the fp32 master in the fused update (10 B per parameter)
+bool split_master_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("EDL_SPLIT_MASTER");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on != 0;
+}
+
 std::vector<int64_t> split_batch_vec(int64_t B, int p) {
   std::vector<int64_t> out(static_cast<size_t>(p), B / p);
   for (int64_t r = 0; r < B % p; ++r) out[static_cast<size_t>(r)] += 1;
@@ -375,6 +385,10 @@ int Job::build_replica(Replica* r) {
   if (mlp_) {
     EDL_TRY(dalloc(&r->master, P_));
     EDL_TRY(dalloc(&r->W, P_));
+    // split master for the single-replica fused update (not with approximate recovery,
+    // which snapshots the fp32 master before every mini-batch)
+    if (split_master_enabled() && cfg_.momentum == 0.0 && !cfg_.appx_recovery)
+      EDL_TRY(dalloc(&r->mlo, P_));
     EDL_TRY(dalloc(&r->recv, P_));
     // exchange mode 4 reads "0xFFFF = not arrived yet" from the receive slots
     EDL_CUDA_TRY(cudaMemset(r->recv, 0xFF, sizeof(__nv_bfloat16) * P_));
@@ -460,6 +474,7 @@ void Job::free_replica(Replica* r) {
   if (r->stream) cudaStreamSynchronize(r->stream);
   dataset_destroy(r->ds);
   cudaFree(r->master);
+  cudaFree(r->mlo);
   cudaFree(r->W);
   cudaFree(r->recv);
   cudaFree(r->mom);
@@ -605,6 +620,8 @@ int Job::install_due(bool* switched) {
   *switched = false;
   bool changed = false;
   while (!events_.empty() && events_.front()->switch_t <= static_cast<int64_t>(t_)) {
+    // re-sharding, broadcasts and copies below read the fp32 master
+    EDL_TRY(master_sync());
     std::unique_ptr<Event> ev = std::move(events_.front());
     events_.pop_front();
     // newcomers hosted by their own processes (scale-out across processes)
@@ -627,7 +644,7 @@ int Job::install_due(bool* switched) {
     const std::vector<PeerRep> old_peers = peers_;
     std::vector<Replica*> fresh;  // replicas that join the collective at this switch
     if (ev->out && multi) {
-      EDL_TRY(join_side());  // the deferred push collective updates master / W
+      EDL_TRY(master_current());  // the deferred push collective / split master
     } else if (!ev->out && !all_local && mlp_ && !dry_ && peers_.size() > 1) {
       EDL_TRY(join_side());
       EDL_TRY(reshard_in_mp(ev.get()));  // targeted: each survivor gets its new shard only
@@ -771,7 +788,10 @@ int Job::ensure_plans(Worker* w, int64_t rows) {
           const char* e = getenv("EDL_DGRAD_L2PF");
           l2pf = e ? atoi(e) : 0;
         }
-        if (l2pf) {
+        if (l2pf && r->mlo) {
+          r->dgrad[l].ep.l2pf = r->mlo + off_[l];
+          r->dgrad[l].ep.l2pf_bytes = sizeof(uint16_t) * static_cast<size_t>(in_[l]) * out_[l];
+        } else if (l2pf) {
           r->dgrad[l].ep.l2pf = r->master + off_[l];
           r->dgrad[l].ep.l2pf_bytes = sizeof(float) * static_cast<size_t>(in_[l]) * out_[l];
         }
@@ -846,9 +866,14 @@ int Job::ensure_plans(Worker* w, int64_t rows) {
     for (int l = 0; l < L_; ++l) {
       const bool last = l == L_ - 1;
       const __nv_bfloat16* dy = last ? r->dlog : r->dx[(l + 1) % 3];
-      EDL_TRY(gemm_plan_init_sgd(&w->wgrad_sgd[l], dy, out_[l], 1, r->act[l], in_[l], 1,
-                                 r->master + off_[l], r->W + off_[l], in_[l], out_[l], in_[l],
-                                 static_cast<int>(rows)));
+      if (r->mlo)  // split master: 8 B per parameter per update instead of 10
+        EDL_TRY(gemm_plan_init_sgd_lo(&w->wgrad_sgd[l], dy, out_[l], r->act[l], in_[l],
+                                      r->mlo + off_[l], r->W + off_[l], r->master + off_[l],
+                                      in_[l], out_[l], in_[l], static_cast<int>(rows)));
+      else
+        EDL_TRY(gemm_plan_init_sgd(&w->wgrad_sgd[l], dy, out_[l], 1, r->act[l], in_[l], 1,
+                                   r->master + off_[l], r->W + off_[l], in_[l], out_[l],
+                                   in_[l], static_cast<int>(rows)));
     }
     w->sgd_plan_rows = rows;
   }
@@ -959,7 +984,7 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
     cudaEvent_t mw = prof ? mark_begin(r->stream) : nullptr;  // wgrad sub-phase
     if (fused_here) {
       // dW + sgd_step in one kernel (layer 0 ends the backward: nothing left to overlap)
-      EDL_TRY(gemm_plan_run(w->wgrad_sgd[l], r->stream, step_scale_));
+      EDL_TRY(run_sgd_plan(w->wgrad_sgd[l], r));
       if (mw) mark(slot, 5, mw, r->stream);
     } else if (overlap_mode_ == 4) {
       // dW + reduce-scatter + sharded SGD + weight all-gather in one kernel per layer
@@ -977,6 +1002,8 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
       if (overlap_ && last) EDL_TRY(launch_layer_coll(r, l));
     }
   }
+  // the fused launches above left the master split or, before a switch, in fp32
+  if (fused_update_ && r->mlo) r->lo_live = split_step_ && sgd_out_split_;
   if (w->delay_us > 0) {
     EDL_TRY(spin(static_cast<uint64_t>(w->delay_us * 1e3), r->stream));
     launches_ += 1;
@@ -1178,7 +1205,7 @@ int Job::take_pre_snapshot() {
 
 // Immediate scale-in of `ids` (failed workers): shards back at their reported offsets.
 int Job::remove_members(const std::vector<std::string>& ids) {
-  EDL_TRY(join_side());  // the deferred push collective updates master / W
+  EDL_TRY(master_current());  // the deferred push collective / split master
   std::vector<std::string> keep;
   for (const auto& id : ring_) {
     if (std::find(ids.begin(), ids.end(), id) == ids.end()) {
@@ -1212,7 +1239,7 @@ bool get(const std::string& b, size_t* o, T* v) {
 }  // namespace
 
 int Job::save_checkpoint(const std::string& path) {
-  EDL_TRY(join_side());  // the deferred push collective updates master / W
+  EDL_TRY(master_current());  // the deferred push collective / split master
   if (path.empty()) return fail(EDL_EINVAL, "checkpoint: empty path");
   // one process per GPU: a collective -- every ring process saves at the same boundary (the
   // fp32 master / momentum shards are all-gathered, then each process writes the identical
@@ -1266,7 +1293,7 @@ int Job::save_checkpoint(const std::string& path) {
 }
 
 int Job::load_checkpoint(const std::string& path) {
-  EDL_TRY(join_side());  // the deferred push collective updates master / W
+  EDL_TRY(master_current());  // the deferred push collective / split master
   // one process per GPU: every ring process loads the same checkpoint (each replica then
   // holds the whole model, which the sharded update keeps consistent from here)
   if (!events_.empty()) return fail(EDL_RETRY, "checkpoint: a scaling operation is pending");
@@ -1365,7 +1392,7 @@ int Job::load_checkpoint(const std::string& path) {
 }
 
 int Job::recover(const std::vector<std::string>& failed, bool approximate, EdlRecovery* out) {
-  EDL_TRY(join_side());  // the deferred push collective updates master / W
+  EDL_TRY(master_current());  // the deferred push collective / split master
   bool all_local = true;
   for (const auto& p : peers_) all_local = all_local && p.local;
   // one process per GPU: consistent recovery only -- each survivor drops the failed
@@ -1876,10 +1903,40 @@ int Job::join_side() {
   return EDL_OK;
 }
 
+int Job::master_sync() {
+  for (auto& [dev, r] : reps_) {
+    if (!r->lo_live) continue;
+    DeviceGuard g(dev);
+    EDL_TRY(master_join(r->W, r->mlo, r->master, P_, r->stream));
+    r->lo_live = false;
+  }
+  return EDL_OK;
+}
+
+int Job::run_sgd_plan(const GemmPlan& p, Replica* r) {
+  if (!p.lo) return gemm_plan_run(p, r->stream, step_scale_);
+  if (!p.lo_master) return fail(EDL_EINVAL, "split master: plan without the fp32 master map");
+  const bool in_split = r->lo_live, out_split = sgd_out_split_ && split_step_;
+  if (in_split && out_split) return gemm_plan_run(p, r->stream, step_scale_);
+  GemmPlan q = p;
+  if (!in_split && !out_split) {  // plain fp32 master kernel
+    q.tm = p.pm.m[0];
+    q.lo = 0;
+  } else {
+    q.lo = in_split ? 2 : 3;
+  }
+  return gemm_plan_run(q, r->stream, step_scale_);
+}
+
+int Job::master_current() {
+  EDL_TRY(join_side());
+  return master_sync();
+}
+
 // All-gather of the sharded fp32 master among the local replicas, enqueued on their streams
 // (no host sync): before a topology switch changes the sharding, and for checkpoints.
 int Job::consolidate_master() {
-  EDL_TRY(join_side());  // the deferred push collective updates master / W
+  EDL_TRY(master_current());  // the deferred push collective / split master
   if (!mlp_ || peers_.size() < 2 || dry_) return EDL_OK;
   const uint32_t epoch = ++coll_epoch_;
   const int n_rep = static_cast<int>(peers_.size());
@@ -1909,7 +1966,7 @@ int Job::consolidate_master() {
 // lowest existing replica, ordered after the source's work so far; the source's next write
 // to its model is its next collective, whose barrier waits for the newcomer.
 int Job::broadcast_model(Replica* src, Replica* dst) {
-  EDL_TRY(join_side());  // the deferred push collective updates master / W
+  EDL_TRY(master_current());  // the deferred push collective / split master
   if (dry_ || src == dst) return EDL_OK;
   {
     DeviceGuard dg(src->device);
@@ -2141,6 +2198,15 @@ int Job::step(EdlStepReport* out) {
   // 1.23M samples/s; splitting each copy over 2-3 copy engines was slower still
   ag_ce_ = ag_defer_ && defer_env == 2;
   if (!ag_defer_) EDL_TRY(join_side());
+  // split master: the fused update keeps the master as (W, lo) from one fused mini-batch to
+  // the next.  The launch before a switch writes the fp32 master instead (kLo = 2) and the
+  // first fused launch after one reads it (kLo = 3), so a switch costs no conversion pass;
+  // any other reader of the master joins it first (master_sync)
+  split_step_ = fused_update_ && !overlap_;
+  sgd_out_split_ = true;
+  for (const auto& ev : events_)
+    if (ev->switch_t >= 0 && ev->switch_t <= static_cast<int64_t>(t_) + 1) sgd_out_split_ = false;
+  if (!split_step_) EDL_TRY(master_sync());
   step_count_ = count;
   if (overlap_mode_ == 1) {  // same epochs on every process
     layer_epoch0_ = coll_epoch_ + 1;
@@ -2638,7 +2704,7 @@ int Job::scale(bool out, const std::vector<std::string>& ids, const std::vector<
 }
 
 int Job::params(const std::string& worker, void* host, size_t bytes) {
-  EDL_TRY(join_side());  // the deferred push collective updates master / W
+  EDL_TRY(master_current());  // the deferred push collective / split master
   auto it = workers_.find(worker);
   if (it == workers_.end()) return fail(EDL_UNKNOWN_WORKER, "params: unknown worker " + worker);
   if (it->second->remote) return fail(EDL_EINVAL, "params: worker hosted by another process");
@@ -2661,7 +2727,7 @@ int Job::params(const std::string& worker, void* host, size_t bytes) {
 // Checkpoint restore (stop-resume baseline, recovery): every replica takes the parameters;
 // MLP replicas re-derive their bf16 working weights from the fp32 master.
 int Job::set_params(const void* host, size_t bytes) {
-  EDL_TRY(join_side());  // the deferred push collective updates master / W
+  EDL_TRY(master_current());  // the deferred push collective / split master
   const size_t need = mlp_ ? sizeof(float) * P_ : sizeof(double) * P_;
   if (bytes < need) return fail(EDL_EINVAL, "set_params: buffer too small");
   for (auto& [dev, r] : reps_) {
@@ -2963,7 +3029,7 @@ int Job::import_handles(const uint8_t* blob, size_t len) {
 }
 
 int Job::gather_master() {
-  EDL_TRY(join_side());  // the deferred push collective updates master / W
+  EDL_TRY(master_current());  // the deferred push collective / split master
   if (!mlp_ || peers_.size() < 2 || dry_) return EDL_OK;
   Replica* r = primary();
   bool all_local = true;

@@ -46,6 +46,10 @@ struct Replica {
   // MLP
   float* master = nullptr;
   __nv_bfloat16* W = nullptr;
+  // split master (single-replica fused update): the low 16 bits of the fp32 master; while
+  // lo_live the master is (W, mlo) and `master` is stale (Job::master_sync rebuilds it)
+  uint16_t* mlo = nullptr;
+  bool lo_live = false;
   float* mom = nullptr;
   uint32_t* flags = nullptr;
   int64_t rows_cap = 0;
@@ -253,6 +257,10 @@ class Job {
   // Single ring member + plain SGD: the update is fused into the weight-gradient GEMMs
   // (there is nothing to all-reduce); set per step.
   bool fused_update_ = false;
+  // split master this mini-batch (fused update, no per-layer overlap), and whether its fused
+  // launches leave the master split (false: a switch is due next, write the fp32 master)
+  bool split_step_ = false;
+  bool sgd_out_split_ = true;
   float step_scale_ = 0.f;
   // Overlapped update (EDL_OVERLAP, default on): layer l's update (and, with several
   // replicas, its NVLink reduce-scatter / all-gather) runs on the replica's side stream as
@@ -347,6 +355,13 @@ class Job {
   int enable_peer_devices(int dev, const std::vector<int>& devs);
   void rebuild_peers();
   int consolidate_master();  // async all-gather of the sharded fp32 master (local replicas)
+  // rebuild the fp32 master of every replica that holds it split (stream-ordered)
+  int master_sync();
+  // join_side + master_sync: before anything reads or writes the master / weights outside
+  // the fused step pipeline
+  int master_current();
+  // the fused wgrad + SGD launch of one layer in this mini-batch's split-master mode
+  int run_sgd_plan(const GemmPlan& p, Replica* r);
  public:
   // orders every local replica's stream after its deferred push collective (no host sync):
   // before anything that reads the master / weights / loss outside the step pipeline

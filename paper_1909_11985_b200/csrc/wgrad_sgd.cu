@@ -327,7 +327,7 @@ bool wgrad_sgd_bres_eligible(const GemmPlan& p) {
     const char* e = getenv("EDL_SGD_BRES");
     on = e ? atoi(e) != 0 : 0;
   }
-  return on && p.ep.sgd && !p.ep.xchg && p.cg == 2 && p.bn == 128 && p.mc == 1 && p.a_mn &&
+  return on && p.ep.sgd && !p.ep.xchg && !p.lo && p.cg == 2 && p.bn == 128 && p.mc == 1 && p.a_mn &&
          p.b_mn && p.M % 256 == 0 && p.N % 128 == 0 && p.K % kBK == 0 && p.K <= kMaxKb * kBK;
 }
 
