@@ -335,7 +335,11 @@ struct Cfg2 {
 #ifndef EDL_SGD_EPI_WARPS
 #define EDL_SGD_EPI_WARPS 8
 #endif
-  static constexpr int kEpiWarps = kSgd ? EDL_SGD_EPI_WARPS : 4;
+  // the split-master epilogue (kLo != 0) runs EDL_SGD_LO_WARPS (16: four per quarter)
+#ifndef EDL_SGD_LO_WARPS
+#define EDL_SGD_LO_WARPS 16
+#endif
+  static constexpr int kEpiWarps = kLo ? EDL_SGD_LO_WARPS : (kSgd ? EDL_SGD_EPI_WARPS : 4);
   static constexpr int kThreads2 = 64 + 32 * kEpiWarps;
   // epilogue staging per warp: plain 2 x 4 KB; fused SGD kSgdBufs x (8 KB master + 4 KB W).
   // EDL_SGD_WDIRECT: the bf16 weights go from registers straight to global memory (each lane
@@ -345,11 +349,11 @@ struct Cfg2 {
 #define EDL_SGD_WDIRECT 0
 #endif
   static constexpr bool kWDirect = kSgd && EDL_SGD_WDIRECT;
-  // split master (kLo, see the kernel): a buffer holds 2 x 4 KB (low halves + weights in,
-  // or fp32 master in, low halves + weights out); kLo = 2 (split in, fp32 master + weights
-  // out) needs 3 x 4 KB
+  // split master (kLo, see the kernel): a warp's 32 x 32 chunk, 4 KB (2 KB low halves +
+  // 2 KB weights, or 4 KB of fp32 master in); kLo = 2 writes 4 KB of fp32 master + 2 KB of
+  // weights: 6 KB
   static constexpr uint32_t kSgdBufBytes =
-      (kLo == 1 || kLo == 3 || kWDirect ? 2 : 3) * kEpiChunkBytes;
+      kLo == 2 ? 6144u : kLo ? 4096u : (kWDirect ? 2 : 3) * kEpiChunkBytes;
 #ifndef EDL_SGD_LO_BUFS
 #define EDL_SGD_LO_BUFS 1
 #endif
@@ -376,7 +380,13 @@ struct Cfg2 {
   static constexpr int kMaxStages = kSgd ? EDL_SGD_STAGES : EDL_GEMM2_MAX_STAGES;
   static constexpr int kStages = kFit > kMaxStages ? kMaxStages : kFit;
   static constexpr uint32_t kAccCols = BN;
-  static constexpr uint32_t kTmemCols = (2 * kAccCols <= 256) ? 256 : 512;
+  // TMEM accumulator ring: 2 tiles; the fused-SGD kernel may use EDL_SGD_ACC (up to 512
+  // columns) so the MMA can run further ahead of its epilogue
+#ifndef EDL_SGD_ACC
+#define EDL_SGD_ACC 2
+#endif
+  static constexpr int kAcc = (kSgd && EDL_SGD_ACC * BN <= 512) ? EDL_SGD_ACC : 2;
+  static constexpr uint32_t kTmemCols = (kAcc * kAccCols <= 256) ? 256 : 512;
   static constexpr uint32_t kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 512;
 };
 
@@ -415,9 +425,9 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(epi + C::kEpiBytes);
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* tfull_bar = empty_bar + C::kStages;
-  uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* sgd_bar = tempty_bar + 2;  // fused SGD: master-load barriers per epilogue warp
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgd_bar + 16);
+  uint64_t* tempty_bar = tfull_bar + C::kAcc;
+  uint64_t* sgd_bar = tempty_bar + C::kAcc;  // fused SGD: master-load barriers per epilogue warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgd_bar + 32);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -462,11 +472,11 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], kMc);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < C::kAcc; ++a) {
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 2 * C::kEpiWarps);  // lane 0 of every epilogue warp, both CTAs
     }
-    for (int a = 0; a < 16; ++a) mbar_init(&sgd_bar[a], kSk == 2 && a < 2 ? 4 : 1);
+    for (int a = 0; a < 32; ++a) mbar_init(&sgd_bar[a], kSk == 2 && a < 2 ? 4 : 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_2sm<C::kTmemCols>(tmem_slot);
@@ -591,8 +601,8 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
       const bool issuer = elect_one();
       TRACE_T0(t_mma);
       for (int wi = 0, w = seq_tile(0); w < num_work; w = seq_tile(++wi), ++local) {
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
+        const int acc = local % C::kAcc;
+        const uint32_t acc_phase = (local / C::kAcc) & 1;
         TRACE_T0(t_te);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         TRACE_ADD(1, t_te);
@@ -626,7 +636,187 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
       TRACE_ADD(2, t_mma);
       TL(3);
     }
-  } else if (kSgd) {
+  } else if constexpr (kSgd && kLo != 0) {
+    // ------------------------------------------------------------ fused SGD, split master
+    // m = (hi << 16) | lo with hi = W - (lo > 0x8000) and W = RNE(m) (the bf16 weights the
+    // GEMMs read); the update is the fp32 one, then W' = RNE(m'), lo' = the low half of m'
+    // except a tie RNE rounds up (low half 0x8000, odd high half), stored as 0x8001 (one
+    // fp32 ulp) so the decode stays unambiguous.  kLo = 1: (W, lo) in and out; 2: (W, lo) in,
+    // fp32 master + W out; 3: fp32 master in, (W, lo) out.  16 epilogue warps, four per TMEM
+    // lane quarter, each 32 rows x 32 columns of a tile: twice the warps of the fp32-master
+    // epilogue, whose per-warp chain (TMEM load -> staged load -> update -> store) is
+    // latency-bound.  Staging rows are 64 B (16-bit) or 128 B (fp32) under the TMA's
+    // swizzle (64 B: SWIZZLE_64B): 16-byte unit u of row r sits at sw(row_bytes * r + 16 u).
+    const int q = warp & 3;           // TMEM lane quarter
+    const int ew = warp - 2;          // epilogue warp index
+    constexpr int kQW = C::kEpiWarps / 4;
+    const int cq = ew / 4;            // column slot of this warp inside the quarter
+    constexpr int kCW = 32;           // columns per chunk
+    static_assert(BN % (kCW * kQW) == 0, "split-master SGD: column chunks split across warps");
+    constexpr int kCPW = BN / (kCW * kQW);
+    constexpr uint32_t kH = 32 * 64;   // 32 rows x 32 16-bit values
+    constexpr uint32_t kF = 32 * 128;  // 32 rows x 32 fp32 values
+    constexpr int NB = C::kSgdBufs;
+    uint8_t* wbase = epi + ew * NB * C::kSgdBufBytes;
+    uint64_t* mb = sgd_bar + ew * NB;
+    // TMA swizzle of a 1024-aligned staging block: 128-byte rows (fp32) XOR the 16-byte unit
+    // with address bits 7-9, 64-byte rows (16-bit, SWIZZLE_64B) with bits 7-8
+    auto sw = [](uint32_t a) -> uint32_t { return a ^ (((a >> 7) & 7u) << 4); };
+    auto sw64 = [](uint32_t a) -> uint32_t { return a ^ (((a >> 7) & 3u) << 4); };
+    auto coords = [&](int j, int* r0, int* c0) -> bool {
+      const int t = seq_tile(j / kCPW);
+      if (t >= num_work) return false;
+      *r0 = tile_m(t) * 256 + static_cast<int>(pr) * 128 + q * 32;
+      *c0 = tile_n(t) * BN + (cq * kCPW + j % kCPW) * kCW;
+      return true;
+    };
+    auto load = [&](int j) {  // lane 0
+      int r0, c0;
+      if (!coords(j, &r0, &c0)) return;
+      uint8_t* dst = wbase + (j % NB) * C::kSgdBufBytes;
+      if constexpr (kLoIn) {
+        mbar_arrive_expect_tx(&mb[j % NB], 2 * kH);
+        tma_load_2d(dst, &tmap_m, &mb[j % NB], c0, r0);          // lo
+        tma_load_2d(dst + kH, &pm.m[1], &mb[j % NB], c0, r0);    // W
+      } else {
+        mbar_arrive_expect_tx(&mb[j % NB], kF);
+        tma_load_2d(dst, &pm.m[0], &mb[j % NB], c0, r0);         // fp32 master
+      }
+    };
+    if (lane == 0 && !skip_epi) {
+      for (int p0 = 0; p0 < (NB > 1 ? NB - 1 : 1); ++p0) load(p0);
+    }
+    int j = 0;
+    int local = 0;
+    TRACE_T0(t_epi);
+    for (int wi = 0, w = seq_tile(0); w < num_work; w = seq_tile(++wi), ++local) {
+      const int acc = local % C::kAcc;
+      const uint32_t acc_phase = (local / C::kAcc) & 1;
+      TRACE_T0(t_tf);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      if (warp == 2) TRACE_ADD(5, t_tf);
+      tc_fence_after();
+      const uint32_t t_row =
+          tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * C::kAccCols;
+#pragma unroll 1
+      for (int cc = 0; cc < (skip_epi ? 0 : kCPW); ++cc, ++j) {
+        const int b = j % NB;
+        if (NB > 1 && lane == 0) {
+          tma_store_wait_read<0>();  // the buffer refilled next was stored from last
+          load(j + NB - 1);
+        }
+        float g[32];
+        TRACE_T0(t_ld);
+        {
+          uint32_t r[32];
+          tmem_ld32(t_row + static_cast<uint32_t>((cq * kCPW + cc) * kCW), r);
+          tmem_ld_wait();
+          // same numerics as the unfused path: the gradient is rounded to bf16 first
+#pragma unroll
+          for (int e = 0; e < 32; ++e) g[e] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(r[e])));
+        }
+        if (warp == 2) TRACE_ADD(9, t_ld);
+        TRACE_T0(t_ml);
+        mbar_wait(&mb[b], (j / NB) & 1);
+        if (warp == 2) TRACE_ADD(7, t_ml);
+        TRACE_T0(t_cs);
+        uint8_t* buf = wbase + b * C::kSgdBufBytes;
+        const uint32_t bo = static_cast<uint32_t>(buf - smem);  // 1024-aligned
+        (void)bo;
+        // read + update: g <- m'
+        if constexpr (kLoIn) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint4 lv = *reinterpret_cast<const uint4*>(buf + sw64(64u * lane + 16u * u));
+            const uint4 wv = *reinterpret_cast<const uint4*>(buf + kH + sw64(64u * lane + 16u * u));
+            const uint32_t li[4] = {lv.x, lv.y, lv.z, lv.w};
+            const uint32_t wi[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2) {
+              uint32_t m0 = __byte_perm(li[q2], wi[q2], 0x5410);  // W0 << 16 | lo0
+              uint32_t m1 = __byte_perm(li[q2], wi[q2], 0x7632);  // W1 << 16 | lo1
+              m0 -= ((m0 & 0xFFFFu) + 0x7FFFu) & 0x10000u;        // hi -= (lo > 0x8000)
+              m1 -= ((m1 & 0xFFFFu) + 0x7FFFu) & 0x10000u;
+              float* gg = &g[8 * u + 2 * q2];
+              gg[0] = __fsub_rn(__uint_as_float(m0), __fmul_rn(ep.scale, gg[0]));
+              gg[1] = __fsub_rn(__uint_as_float(m1), __fmul_rn(ep.scale, gg[1]));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float4 m = *reinterpret_cast<const float4*>(buf + sw(128u * lane + 16u * u));
+            float* gg = &g[4 * u];
+            gg[0] = __fsub_rn(m.x, __fmul_rn(ep.scale, gg[0]));
+            gg[1] = __fsub_rn(m.y, __fmul_rn(ep.scale, gg[1]));
+            gg[2] = __fsub_rn(m.z, __fmul_rn(ep.scale, gg[2]));
+            gg[3] = __fsub_rn(m.w, __fmul_rn(ep.scale, gg[3]));
+          }
+        }
+        if (warp == 2) TRACE_ADD(11, t_cs);
+        __syncwarp();  // outputs overwrite other lanes' input rows (kLo 2 / 3)
+        if constexpr (kLoOut) {  // lo' -> [0, 2 KB), W' -> [2 KB, 4 KB)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint32_t wo[4], lo[4];
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2) {
+              const float f0 = g[8 * u + 2 * q2], f1 = g[8 * u + 2 * q2 + 1];
+              wo[q2] = pack_bf16(f0, f1);
+              uint32_t b0 = __float_as_uint(f0), b1 = __float_as_uint(f1);
+              b0 |= (b0 & 0x1FFFFu) == 0x18000u ? 1u : 0u;  // rounded-up tie -> lo 0x8001
+              b1 |= (b1 & 0x1FFFFu) == 0x18000u ? 1u : 0u;
+              lo[q2] = __byte_perm(b0, b1, 0x5410);
+            }
+            *reinterpret_cast<uint4*>(buf + sw64(64u * lane + 16u * u)) =
+                make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            *reinterpret_cast<uint4*>(buf + kH + sw64(64u * lane + 16u * u)) =
+                make_uint4(wo[0], wo[1], wo[2], wo[3]);
+          }
+        } else {  // fp32 master -> [0, 4 KB), W' -> [4 KB, 6 KB)
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            *reinterpret_cast<float4*>(buf + sw(128u * lane + 16u * u)) =
+                make_float4(g[4 * u], g[4 * u + 1], g[4 * u + 2], g[4 * u + 3]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint4 o;
+            o.x = pack_bf16(g[8 * u + 0], g[8 * u + 1]);
+            o.y = pack_bf16(g[8 * u + 2], g[8 * u + 3]);
+            o.z = pack_bf16(g[8 * u + 4], g[8 * u + 5]);
+            o.w = pack_bf16(g[8 * u + 6], g[8 * u + 7]);
+            *reinterpret_cast<uint4*>(buf + kF + sw64(64u * lane + 16u * u)) = o;
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          int r0, c0;
+          coords(j, &r0, &c0);
+          if constexpr (kLoOut) {
+            tma_store_2d(&tmap_m, buf, c0, r0);
+            tma_store_2d(&pm.m[1], buf + kH, c0, r0);
+          } else {
+            tma_store_2d(&pm.m[0], buf, c0, r0);
+            tma_store_2d(&pm.m[1], buf + kF, c0, r0);
+          }
+          tma_store_commit();
+          if (NB == 1) {  // single buffer: refill it for this warp's next chunk
+            TRACE_T0(t_wr);
+            tma_store_wait_read<0>();
+            if (warp == 2) TRACE_ADD(6, t_wr);
+            load(j + 1);
+          }
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(&tempty_bar[acc], 2 * pidx);
+    }
+    if (lane == 0) tma_store_wait<0>();
+    if (warp == 2) TRACE_ADD(8, t_epi);
+  } else if constexpr (kSgd) {
     // ------------------------------------------------------------ fused SGD epilogue
     // Per warp (32 rows of the CTA's 128) and 64-column chunk: TMA-load the fp32 master
     // chunk (prefetched one chunk ahead, across tiles), fold master -= scale * bf16(acc) in
@@ -667,16 +857,8 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
       if (!coords(j, &r0, &c0)) return;
       uint8_t* dst = wbase + (j % NB) * C::kSgdBufBytes;
       mbar_arrive_expect_tx(&mb[j % NB], 2 * kEpiChunkBytes);
-      if constexpr (kLoIn) {  // low master halves (16-bit, 64-column box) + bf16 weights
-        tma_load_2d(dst, &tmap_m, &mb[j % NB], c0, r0);
-        tma_load_2d(dst + kEpiChunkBytes, &tmap_c, &mb[j % NB], c0, r0);
-      } else if constexpr (kLo == 3) {  // fp32 master through the plan's second map
-        tma_load_2d(dst, &pm.m[0], &mb[j % NB], c0, r0);
-        tma_load_2d(dst + kEpiChunkBytes, &pm.m[0], &mb[j % NB], c0 + 32, r0);
-      } else {
-        tma_load_2d(dst, &tmap_m, &mb[j % NB], c0, r0);
-        tma_load_2d(dst + kEpiChunkBytes, &tmap_m, &mb[j % NB], c0 + 32, r0);
-      }
+      tma_load_2d(dst, &tmap_m, &mb[j % NB], c0, r0);
+      tma_load_2d(dst + kEpiChunkBytes, &tmap_m, &mb[j % NB], c0 + 32, r0);
     };
     // L2 prefetch of this warp's 32 master rows of tile t (BN columns, 32-column boxes): the
     // master stream is the kernel's HBM traffic, and pf_tiles tiles of lead time keep enough
@@ -685,16 +867,8 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
       if (t >= num_work) return;
       const int r0 = tile_m(t) * 256 + static_cast<int>(pr) * 128 + q * 32;
       const int c0 = tile_n(t) * BN + half * (BN / kHalves);
-      if constexpr (kLoIn) {  // 64-column boxes of the low halves and of the weights
 #pragma unroll
-        for (int c = 0; c < BN / kHalves; c += 64) {
-          tma_prefetch_2d(&tmap_m, c0 + c, r0);
-          tma_prefetch_2d(&tmap_c, c0 + c, r0);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < BN / kHalves; c += 32) tma_prefetch_2d(&tmap_m, c0 + c, r0);
-      }
+      for (int c = 0; c < BN / kHalves; c += 32) tma_prefetch_2d(&tmap_m, c0 + c, r0);
     };
     if (lane == 0) {
       for (int i = 0; i < ep.pf_tiles && !kX; ++i) l2_prefetch_tile(unit + i * n_units);
@@ -709,8 +883,8 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
     int local = 0;
     TRACE_T0(t_epi);
     for (int wi = 0, w = seq_tile(0); w < num_work; w = seq_tile(++wi), ++local) {
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
+      const int acc = local % C::kAcc;
+      const uint32_t acc_phase = (local / C::kAcc) & 1;
       if (lane == 0 && ep.pf_tiles > 0 && !kX) l2_prefetch_tile(w + ep.pf_tiles * n_units);
       TRACE_T0(t_tf);
       mbar_wait(&tfull_bar[acc], acc_phase);
@@ -849,115 +1023,6 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
         ++n_used;
         if (warp == 2) TRACE_ADD(7, t_ml);
         TRACE_T0(t_cs);
-        if constexpr (kLo != 0) {
-          // split master: m = (hi << 16) | lo with hi = W - (lo > 0x8000) (W = RNE(m)).  The
-          // update is the fp32 one; W' = RNE(m') and lo' = the low half of m', except a tie RNE
-          // rounds up (low half 0x8000, odd high half) is stored as 0x8001 (one fp32 ulp) so
-          // the decode stays unambiguous.  Each lane reads its whole row into g (g <- m'),
-          // then writes it: the output layout reuses the input rows in place.
-          uint8_t* r0b = buf + lane * 128;  // the lane's row in 4 KB block 0 (+ k * 4 KB)
-          if constexpr (kLo == 1) {  // in place, 8 columns at a time (fewest live registers)
-#pragma unroll
-            for (int j8 = 0; j8 < 8; ++j8) {
-              const int off = (j8 ^ (lane & 7)) << 4;
-              uint4* pl = reinterpret_cast<uint4*>(r0b + off);
-              uint4* pw = reinterpret_cast<uint4*>(r0b + kEpiChunkBytes + off);
-              const uint4 lv = *pl, wv = *pw;
-              const uint32_t wi[4] = {wv.x, wv.y, wv.z, wv.w};
-              const uint32_t li[4] = {lv.x, lv.y, lv.z, lv.w};
-              uint32_t wo[4], lo[4];
-#pragma unroll
-              for (int q2 = 0; q2 < 4; ++q2) {
-                uint32_t m0 = __byte_perm(li[q2], wi[q2], 0x5410);  // W0 << 16 | lo0
-                uint32_t m1 = __byte_perm(li[q2], wi[q2], 0x7632);  // W1 << 16 | lo1
-                m0 -= ((m0 & 0xFFFFu) + 0x7FFFu) & 0x10000u;        // hi -= (lo > 0x8000)
-                m1 -= ((m1 & 0xFFFFu) + 0x7FFFu) & 0x10000u;
-                const float f0 =
-                    __fsub_rn(__uint_as_float(m0), __fmul_rn(ep.scale, g[8 * j8 + 2 * q2]));
-                const float f1 =
-                    __fsub_rn(__uint_as_float(m1), __fmul_rn(ep.scale, g[8 * j8 + 2 * q2 + 1]));
-                wo[q2] = pack_bf16(f0, f1);
-                uint32_t b0 = __float_as_uint(f0), b1 = __float_as_uint(f1);
-                b0 |= (b0 & 0x1FFFFu) == 0x18000u ? 1u : 0u;  // rounded-up tie -> lo 0x8001
-                b1 |= (b1 & 0x1FFFFu) == 0x18000u ? 1u : 0u;
-                lo[q2] = __byte_perm(b0, b1, 0x5410);
-              }
-              *pl = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-              *pw = make_uint4(wo[0], wo[1], wo[2], wo[3]);
-            }
-          } else if constexpr (kLoIn) {
-#pragma unroll
-            for (int j8 = 0; j8 < 8; ++j8) {
-              const int off = (j8 ^ (lane & 7)) << 4;
-              const uint4 lv = *reinterpret_cast<const uint4*>(r0b + off);
-              const uint4 wv = *reinterpret_cast<const uint4*>(r0b + kEpiChunkBytes + off);
-              const uint32_t wi[4] = {wv.x, wv.y, wv.z, wv.w};
-              const uint32_t li[4] = {lv.x, lv.y, lv.z, lv.w};
-#pragma unroll
-              for (int q2 = 0; q2 < 4; ++q2) {
-                uint32_t m0 = __byte_perm(li[q2], wi[q2], 0x5410);  // W0 << 16 | lo0
-                uint32_t m1 = __byte_perm(li[q2], wi[q2], 0x7632);  // W1 << 16 | lo1
-                m0 -= ((m0 & 0xFFFFu) + 0x7FFFu) & 0x10000u;        // hi -= (lo > 0x8000)
-                m1 -= ((m1 & 0xFFFFu) + 0x7FFFu) & 0x10000u;
-                float* gg = &g[8 * j8 + 2 * q2];
-                gg[0] = __fsub_rn(__uint_as_float(m0), __fmul_rn(ep.scale, gg[0]));
-                gg[1] = __fsub_rn(__uint_as_float(m1), __fmul_rn(ep.scale, gg[1]));
-              }
-            }
-          } else {
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-              for (int k4 = 0; k4 < 8; ++k4) {
-                const float4 m = *reinterpret_cast<const float4*>(
-                    r0b + h * kEpiChunkBytes + ((k4 ^ (lane & 7)) << 4));
-                float* gg = &g[h * 32 + k4 * 4];
-                gg[0] = __fsub_rn(m.x, __fmul_rn(ep.scale, gg[0]));
-                gg[1] = __fsub_rn(m.y, __fmul_rn(ep.scale, gg[1]));
-                gg[2] = __fsub_rn(m.z, __fmul_rn(ep.scale, gg[2]));
-                gg[3] = __fsub_rn(m.w, __fmul_rn(ep.scale, gg[3]));
-              }
-          }
-          if constexpr (kLo == 1) {
-            // written above
-          } else if constexpr (kLoOut) {  // lo' -> block 0, W' -> block 1
-#pragma unroll
-            for (int j8 = 0; j8 < 8; ++j8) {
-              const int off = (j8 ^ (lane & 7)) << 4;
-              uint32_t wo[4], lo[4];
-#pragma unroll
-              for (int q2 = 0; q2 < 4; ++q2) {
-                const float f0 = g[8 * j8 + 2 * q2], f1 = g[8 * j8 + 2 * q2 + 1];
-                wo[q2] = pack_bf16(f0, f1);
-                uint32_t b0 = __float_as_uint(f0), b1 = __float_as_uint(f1);
-                b0 |= (b0 & 0x1FFFFu) == 0x18000u ? 1u : 0u;  // rounded-up tie -> lo 0x8001
-                b1 |= (b1 & 0x1FFFFu) == 0x18000u ? 1u : 0u;
-                lo[q2] = __byte_perm(b0, b1, 0x5410);
-              }
-              *reinterpret_cast<uint4*>(r0b + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-              *reinterpret_cast<uint4*>(r0b + kEpiChunkBytes + off) =
-                  make_uint4(wo[0], wo[1], wo[2], wo[3]);
-            }
-          } else {  // fp32 master -> blocks 0 / 1 (32 columns each), W' -> block 2
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-              for (int k4 = 0; k4 < 8; ++k4) {
-                const float* gg = &g[h * 32 + k4 * 4];
-                *reinterpret_cast<float4*>(r0b + h * kEpiChunkBytes + ((k4 ^ (lane & 7)) << 4)) =
-                    make_float4(gg[0], gg[1], gg[2], gg[3]);
-              }
-#pragma unroll
-            for (int j8 = 0; j8 < 8; ++j8) {
-              uint4 o;
-              o.x = pack_bf16(g[8 * j8 + 0], g[8 * j8 + 1]);
-              o.y = pack_bf16(g[8 * j8 + 2], g[8 * j8 + 3]);
-              o.z = pack_bf16(g[8 * j8 + 4], g[8 * j8 + 5]);
-              o.w = pack_bf16(g[8 * j8 + 6], g[8 * j8 + 7]);
-              *reinterpret_cast<uint4*>(r0b + 2 * kEpiChunkBytes + ((j8 ^ (lane & 7)) << 4)) = o;
-            }
-          }
-        } else {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint8_t* mrow = buf + h * kEpiChunkBytes + lane * 128;
@@ -977,12 +1042,9 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
             g[h * 32 + k4 * 4 + 3] = m.w;
           }
         }
-        }
         if (warp == 2) TRACE_ADD(11, t_cs);
         TRACE_T0(t_w8);
-        if constexpr (kLo != 0) {
-          // outputs staged above
-        } else if constexpr (C::kWDirect) {
+        if constexpr (C::kWDirect) {
           int r0, c0;
           coords(j, &r0, &c0);
           uint4* wp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.C) +
@@ -1015,18 +1077,9 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
         if (lane == 0) {
           int r0, c0;
           coords(j, &r0, &c0);
-          if constexpr (kLoOut) {
-            tma_store_2d(&tmap_m, buf, c0, r0);
-            tma_store_2d(&tmap_c, buf + kEpiChunkBytes, c0, r0);
-          } else if constexpr (kLo == 2) {
-            tma_store_2d(&pm.m[0], buf, c0, r0);
-            tma_store_2d(&pm.m[0], buf + kEpiChunkBytes, c0 + 32, r0);
-            tma_store_2d(&tmap_c, buf + 2 * kEpiChunkBytes, c0, r0);
-          } else {
-            tma_store_2d(&tmap_m, buf, c0, r0);
-            tma_store_2d(&tmap_m, buf + kEpiChunkBytes, c0 + 32, r0);
-            if (!C::kWDirect) tma_store_2d(&tmap_c, buf + 2 * kEpiChunkBytes, c0, r0);
-          }
+          tma_store_2d(&tmap_m, buf, c0, r0);
+          tma_store_2d(&tmap_m, buf + kEpiChunkBytes, c0 + 32, r0);
+          if (!C::kWDirect) tma_store_2d(&tmap_c, buf + 2 * kEpiChunkBytes, c0, r0);
           if (kX) {  // all-gather: the updated weights into every other replica
             for (int o = 0; o < ep.x_n; ++o)
               if (o != ep.route_me && !(ep.dbg & 8))  // EDL_GEMM_DBG=8: diagnostics only
@@ -1057,8 +1110,8 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
     int buf = 0;
     int local = 0;
     for (int w = unit; w < num_work; w += n_units, ++local) {
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
+      const int acc = local % C::kAcc;
+      const uint32_t acc_phase = (local / C::kAcc) & 1;
       const int row0 = tile_m(w) * 256 + static_cast<int>(pr) * 128 + q * 32;
       const int n0 = tile_n(w) * BN;
       mbar_wait(&tfull_bar[acc], acc_phase);
@@ -1249,9 +1302,12 @@ int make_tmap_t(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, 
   cuuint64_t strides[1] = {ld * esz};
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
+  // the swizzle span matches the box row: 128-byte rows SWIZZLE_128B, 64-byte rows 64B
+  const CUtensorMapSwizzle swz =
+      box_cols * esz >= 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   CUresult r = fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                   const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? EDL_OK : EDL_ECUDA;
 }
@@ -1639,8 +1695,12 @@ int gemm_plan_init_sgd_lo(GemmPlan* p, const void* A, int lda, const void* B, in
   int rc = gemm_plan_init(p, A, lda, 1, B, ldb, 1, W, ldw, M, N, K, 0, 0, nullptr, 0, 1128);
   if (rc) return rc;
   p->mc = 1;
-  rc = make_tmap_t(&p->tm, lo, M, N, ldw, 64, 32, false);
+  // 32 x 32 boxes (one epilogue warp's chunk): the low halves and the weights (pm.m[1]; the
+  // plan's own 64-column weight map tc stays for the fp32-master kernel)
+  rc = make_tmap_t(&p->tm, lo, M, N, ldw, 32, 32, false);
   if (rc) return fail(rc, "split-master SGD: tensor map of the low halves");
+  rc = make_tmap_t(&p->pm.m[1], W, M, N, ldw, 32, 32, false);
+  if (rc) return fail(rc, "split-master SGD: tensor map of the weights");
   if (master) {  // the conversion launches (gemm_plan_lo_mode 2 / 3) read or write it
     rc = make_tmap_t(&p->pm.m[0], master, M, N, ldw, 32, 32, true);
     if (rc) return fail(rc, "split-master SGD: tensor map of the fp32 master");

@@ -24,14 +24,19 @@ PROF = os.path.join(ROOT, "profiles")
 
 
 def family(name: str) -> str:
-    m = re.search(r"(gemm_bf16_2sm_kernel|gemm_bf16_tn_kernel)<(\d+), \(?(?:bool\))?(\d|true|false)\)?, "
-                  r"\(?(?:bool\))?(\d|true|false)\)?(?:, \(?(?:bool\))?(\d|true|false)\)?)?", name)
+    name = re.sub(r"\((?:int|bool)\)", "", name)  # ncu's "(int)128, (bool)1" spelling
+    m = re.search(r"(gemm_bf16_2sm_kernel|gemm_bf16_tn_kernel)<(\d+), (\d|true|false), "
+                  r"(\d|true|false)(?:, (\d|true|false))?", name)
     if m:
         kind, bn, a, b, sgd = m.groups()
         a = a in ("1", "true")
         b = b in ("1", "true")
         sgd = sgd in ("1", "true")
         role = "wgrad+sgd" if sgd else ("wgrad" if a and b else ("dgrad" if b else "fwd"))
+        lo = re.search(r"gemm_bf16_2sm_kernel<[^>]*, (\d)>", name)
+        if sgd and lo and lo.group(1) != "0":
+            role += {"1": ", split master", "2": ", split in / fp32 out",
+                     "3": ", fp32 in / split out"}.get(lo.group(1), "")
         return f"{kind}<BN={bn}> [{role}]"
     for k in ("allreduce_sgd", "xent_kernel", "sum_rows", "gather_kernel", "gen_bf16", "gen_f64",
               "init_kernel", "ordered_sum", "linear_allreduce"):
@@ -43,28 +48,38 @@ def family(name: str) -> str:
 def launches(path: str, tag: str) -> None:
     shutil.copy(path, os.path.join(PROF, f"{tag}_launches.csv"))
     rows = []
+    dram = collections.defaultdict(lambda: [0.0, 0.0])  # launch ID -> [read MB, write MB]
     with open(path) as f:
         text = f.read()
     start = text.find('"ID"')
     rdr = csv.DictReader(io.StringIO(text[start:]))
+    scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "KB": 1e-3, "MB": 1.0,
+             "GB": 1e3, "B": 1e-6}
     for r in rdr:
-        if r.get("Metric Name") != "gpu__time_duration.sum":
-            continue
+        name = r.get("Metric Name")
         try:
             v = float(r["Metric Value"].replace(",", ""))
-        except ValueError:
+        except (ValueError, KeyError):
             continue
         unit = r.get("Metric Unit", "")
+        if name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            dram[r["ID"]][0 if name.endswith("read.sum") else 1] += v * scale.get(unit, 1e-6)
+            continue
+        if name != "gpu__time_duration.sum":
+            continue
         us = v / 1000.0 if unit in ("ns", "nsecond") else (v * 1000.0 if unit in ("ms", "msecond") else v)
-        rows.append((r["Kernel Name"], us))
+        rows.append((r["Kernel Name"], us, r["ID"]))
     # one mini-batch = the launches between two consecutive gather kernels (last full one)
-    idx = [i for i, (n, _) in enumerate(rows) if "gather_kernel" in n or "gather_inline_kernel" in n]
+    idx = [i for i, (n, _, _) in enumerate(rows) if "gather_kernel" in n or "gather_inline_kernel" in n]
     step = rows[idx[-2]:idx[-1]] if len(idx) >= 2 else rows
     agg = collections.OrderedDict()
-    for n, us in step:
+    agg_dram = collections.OrderedDict()
+    for n, us, lid in step:
         k = family(n)
         c, t = agg.get(k, (0, 0.0))
         agg[k] = (c + 1, t + us)
+        rd, wr = agg_dram.get(k, (0.0, 0.0))
+        agg_dram[k] = (rd + dram[lid][0], wr + dram[lid][1])
     total = sum(t for _, t in agg.values())
     out = [f"# {tag}: kernel shares of one mini-batch (ncu launch list, cold-cache, serialised)\n",
            f"Source: `{os.path.basename(path)}` from `ncu --metrics gpu__time_duration.sum "
@@ -76,6 +91,19 @@ def launches(path: str, tag: str) -> None:
     for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         out.append(f"| {k} | {c} | {t:.1f} | {t / c:.1f} | {100 * t / total:.1f}% |")
     out.append(f"| **total** | {sum(c for c, _ in agg.values())} | {total:.1f} | | 100% |")
+    if dram:
+        out += ["", "## DRAM traffic over one mini-batch (`--cache-control none`: caches not "
+                "flushed between kernels, so dirty lines a kernel leaves in L2 are counted where "
+                "they are written back; the sum over the mini-batch is the true HBM traffic)", "",
+                "| kernel family | launches | us (serialised) | DRAM read MB | DRAM write MB |",
+                "|---|---|---|---|---|"]
+        for k, (c, t) in agg.items():
+            rd, wr = agg_dram[k]
+            out.append(f"| {k} | {c} | {t:.1f} | {rd:.1f} | {wr:.1f} |")
+        trd = sum(v[0] for v in agg_dram.values())
+        twr = sum(v[1] for v in agg_dram.values())
+        out.append(f"| **total** | | | **{trd:.1f}** | **{twr:.1f}** |")
+        out.append(f"\nMeasured HBM traffic per mini-batch: {(trd + twr) / 1e3:.2f} GB read + write.")
     with open(os.path.join(PROF, f"{tag}_kernel_shares.md"), "w") as f:
         f.write("\n".join(out) + "\n")
     print("\n".join(out))
