@@ -319,7 +319,7 @@ __device__ unsigned long long g_gemm_tl[296][16];
 #define TL(slot)
 #endif
 
-template <int BN, bool kSgd = false, int kLo = 0>
+template <int BN, bool kSgd = false, int kLo = 0, bool kAres = false>
 struct Cfg2 {
   static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "2-SM tiles: BN multiple of 64");
   static constexpr int kHalfN = BN / 2;
@@ -328,7 +328,12 @@ struct Cfg2 {
   static constexpr uint32_t kBBytesK = static_cast<uint32_t>(kHalfN) * BK * 2;  // per CTA
   static constexpr uint32_t kBBytesMN = kBBoxesMN * kMnBlockBytes;
   static constexpr uint32_t kBSlot = kBBytesK > kBBytesMN ? kBBytesK : kBBytesMN;
-  static constexpr uint32_t kStageBytes = kABytes + ((kBSlot + 1023) / 1024) * 1024;
+  // kAres (A-resident fused SGD): the whole A panel of the current row block (up to K = 512:
+  // 8 k-blocks x 16 KB per CTA) stays in shared memory; the stages hold B only
+  static constexpr int kAresMaxKb = 8;
+  static constexpr uint32_t kAPanel = kAres ? kAresMaxKb * kABytes : 0;
+  static constexpr uint32_t kStageBytes =
+      (kAres ? 0 : kABytes) + ((kBSlot + 1023) / 1024) * 1024;
   // epilogue warps: 4 (one per TMEM lane quarter); the fused-SGD epilogue is latency-bound
   // (TMEM loads, master loads, smem shared with the mainloop) and runs two warps per quarter,
   // each owning half of the tile's columns
@@ -373,11 +378,15 @@ struct Cfg2 {
 #ifndef EDL_GEMM2_MAX_STAGES
 #define EDL_GEMM2_MAX_STAGES 6
 #endif
-  static constexpr int kFit = (224 * 1024 - kEpiBytes) / kStageBytes;
+  static constexpr int kFit = (224 * 1024 - kEpiBytes - kAPanel) / kStageBytes;
 #ifndef EDL_SGD_STAGES
 #define EDL_SGD_STAGES EDL_GEMM2_MAX_STAGES
 #endif
-  static constexpr int kMaxStages = kSgd ? EDL_SGD_STAGES : EDL_GEMM2_MAX_STAGES;
+#ifndef EDL_ARES_STAGES
+#define EDL_ARES_STAGES 4
+#endif
+  static constexpr int kMaxStages =
+      kAres ? EDL_ARES_STAGES : kSgd ? EDL_SGD_STAGES : EDL_GEMM2_MAX_STAGES;
   static constexpr int kStages = kFit > kMaxStages ? kMaxStages : kFit;
   static constexpr uint32_t kAccCols = BN;
   // TMEM accumulator ring: 2 tiles; the fused-SGD kernel may use EDL_SGD_ACC (up to 512
@@ -387,7 +396,7 @@ struct Cfg2 {
 #endif
   static constexpr int kAcc = (kSgd && EDL_SGD_ACC * BN <= 512) ? EDL_SGD_ACC : 2;
   static constexpr uint32_t kTmemCols = (kAcc * kAccCols <= 256) ? 256 : 512;
-  static constexpr uint32_t kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 512;
+  static constexpr uint32_t kSmemBytes = kAPanel + kStages * kStageBytes + kEpiBytes + 1024 + 512;
 };
 
 // kSk = 2 (split-K): a cluster of 4 CTAs = 2 pairs computes ONE 256 x BN tile, pair p over
@@ -398,14 +407,20 @@ struct Cfg2 {
 // partial to the matching CTA of the other pair through DSMEM (into that CTA's idle stage
 // buffers), receives that CTA's partial of its own half, adds, and runs the epilogue.
 template <int BN, bool A_MN, bool B_MN, bool kSgd, int kMc, int kSk = 1, bool kX = false,
-          int kLo = 0>
-__global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
+          int kLo = 0, bool kAres = false>
+__global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo, kAres>::kThreads2, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                          const __grid_constant__ CUtensorMap tmap_b,
                          const __grid_constant__ CUtensorMap tmap_c,
                          const __grid_constant__ CUtensorMap tmap_m, int M, int N, int K,
                          EpiParams ep, const __grid_constant__ PeerMaps pm) {
-  using C = Cfg2<BN, kSgd, kLo>;
+  using C = Cfg2<BN, kSgd, kLo, kAres>;
+  // kAres: A-resident variant of the split-master fused SGD (mode 1 / 3): each CTA pair takes
+  // a contiguous range of tiles in row-major order and keeps the A panel of the current row
+  // block (dY^T: 256 rows x K) in shared memory, reloading it only when the row block changes;
+  // only B streams.  Operand bytes from L2 per tile: 128 KB instead of 384 KB.
+  static_assert(!kAres || ((kLo == 1 || kLo == 3) && kMc == 1 && kSk == 1),
+                "A-resident: split-master SGD plans");
   // kLo (fused SGD over the split master, tmap_m = the 16-bit low halves lo, pm.m[0] = the
   // fp32 master): 1 = (W, lo) in and out; 2 = (W, lo) in, fp32 master + W out (the last
   // mini-batch before a switch to another update path); 3 = fp32 master in, (W, lo) out
@@ -421,13 +436,17 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* epi = smem + C::kStages * C::kStageBytes;  // 1024-aligned staging
+  uint8_t* a_panel = smem;                // kAres: the resident A panel
+  uint8_t* sbase = smem + C::kAPanel;     // the stage ring
+  uint8_t* epi = sbase + C::kStages * C::kStageBytes;  // 1024-aligned staging
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(epi + C::kEpiBytes);
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* tfull_bar = empty_bar + C::kStages;
   uint64_t* tempty_bar = tfull_bar + C::kAcc;
   uint64_t* sgd_bar = tempty_bar + C::kAcc;  // fused SGD: master-load barriers per epilogue warp
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sgd_bar + 32);
+  uint64_t* a_full = sgd_bar + 32;   // kAres: A panel landed
+  uint64_t* a_empty = a_full + 1;    // kAres: the MMAs reading the A panel are done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_empty + 1);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -441,14 +460,19 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
   const int n_tiles = (N + BN - 1) / BN;  // the host guarantees n_tiles % kMc == 0
   const int num_work = m_tiles * (n_tiles / kMc);
   const int num_kb = (K + BK - 1) / BK;
-  auto tile_m = [&](int w) { return w % m_tiles; };
+  auto tile_m = [&](int w) { return kAres ? w / n_tiles : w % m_tiles; };
   auto tile_n = [&](int w) {
+    if (kAres) return w % n_tiles;
     return (w / m_tiles) * kMc + (kMc >= 2 ? static_cast<int>(pidx) : 0);
   };
   // the unit's work sequence: tiles unit, unit + n_units, ...  (Running the fused
   // exchange's routed tiles first was measured slower: it separates the epilogue-heavy own
-  // tiles from the mainloop-heavy routed ones instead of overlapping them.)
+  // tiles from the mainloop-heavy routed ones instead of overlapping them.)  kAres: the
+  // contiguous range [unit * W / U, (unit + 1) * W / U) of the row-major tile order.
+  const int ares_lo = static_cast<int>(static_cast<long>(unit) * num_work / n_units);
+  const int ares_hi = static_cast<int>(static_cast<long>(unit + 1) * num_work / n_units);
   auto seq_tile = [&](int i) -> int {
+    if (kAres) return ares_lo + i < ares_hi ? ares_lo + i : num_work;
     const int t = unit + i * n_units;
     return t < num_work ? t : num_work;
   };
@@ -477,6 +501,8 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
       mbar_init(&tempty_bar[a], 2 * C::kEpiWarps);  // lane 0 of every epilogue warp, both CTAs
     }
     for (int a = 0; a < 32; ++a) mbar_init(&sgd_bar[a], kSk == 2 && a < 2 ? 4 : 1);
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_2sm<C::kTmemCols>(tmem_slot);
@@ -491,7 +517,109 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
   // Producer and MMA loops run warp-uniform (all 32 lanes wait on the barriers; elect.sync
   // picks the issuing lane) so descriptors and coordinates stay in uniform registers and
   // each UTCHMMA / UTMALDG issues without a per-instruction R2UR waterfall.
-  if (warp == 0) {
+  if (warp == 0 && kAres) {
+    // ------------------------------------------------------------ TMA producer, A resident
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t tx_b = 2 * (B_MN ? C::kBBytesMN : C::kBBytesK);
+    const uint32_t tx_a = 2 * static_cast<uint32_t>(num_kb) * C::kABytes;
+    int cur_m = -1, panel = 0;
+    for (int wi = 0, w = seq_tile(0); w < num_work; w = seq_tile(++wi)) {
+      const int m = tile_m(w);
+      const int m0 = m * 256 + static_cast<int>(pr) * 128;
+      const int n0 = tile_n(w) * BN + static_cast<int>(pr) * C::kHalfN;
+      if (m != cur_m) {  // a new row block: its A panel, once the MMAs on the old one are done
+        if (panel > 0) mbar_wait(a_empty, (panel - 1) & 1);
+        if (elect_one()) {
+          if (leader) mbar_arrive_expect_tx(a_full, tx_a);
+          for (int kb = 0; kb < num_kb; ++kb) {
+            uint8_t* sa = a_panel + kb * C::kABytes;
+            if (A_MN) {
+              tma_load_2d_2sm(sa, &tmap_a, a_full, m0, kb * BK);
+              tma_load_2d_2sm(sa + kMnBlockBytes, &tmap_a, a_full, m0 + 64, kb * BK);
+            } else {
+              tma_load_2d_2sm(sa, &tmap_a, a_full, kb * BK, m0);
+            }
+          }
+        }
+        __syncwarp();
+        cur_m = m;
+        ++panel;
+      }
+      for (int kb = kb_begin; kb < kb_end; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (elect_one()) {
+          uint8_t* sb = sbase + stage * C::kStageBytes;
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], tx_b);
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < C::kBBoxesMN; ++j)
+              tma_load_2d_2sm(sb + j * kMnBlockBytes, &tmap_b, &full_bar[stage], n0 + 64 * j,
+                              kb * BK);
+          } else {
+            tma_load_2d_2sm(sb, &tmap_b, &full_bar[stage], kb * BK, n0);
+          }
+        }
+        __syncwarp();
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1 && kAres) {
+    if (leader) {
+      // ------------------------------------------------------------ MMA issuer, A resident
+      constexpr uint32_t idesc = idesc_bf16_f32(256, BN, A_MN, B_MN);
+      const uint32_t sa0 = smem_u32(a_panel), sb0 = smem_u32(sbase);
+      const uint64_t a0 = A_MN ? smem_desc_sw128(sa0, kMnBlockBytes, 1024) : smem_desc_sw128(sa0, 16, 1024);
+      const uint64_t b0 = B_MN ? smem_desc_sw128(sb0, kMnBlockBytes, 1024) : smem_desc_sw128(sb0, 16, 1024);
+      constexpr uint32_t kStepA = A_MN ? 2048 : 32, kStepB = B_MN ? 2048 : 32;
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      int cur_m = -1, panel = 0;
+      const bool issuer = elect_one();
+      for (int wi = 0, w = seq_tile(0); w < num_work; w = seq_tile(++wi), ++local) {
+        const int acc = local % C::kAcc;
+        const uint32_t acc_phase = (local / C::kAcc) & 1;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const int m = tile_m(w);
+        if (m != cur_m) {
+          mbar_wait(a_full, panel & 1);
+          tc_fence_after();
+          cur_m = m;
+          ++panel;
+        }
+        const uint32_t d_tmem = tmem_base + acc * C::kAccCols;
+        for (int kb = kb_begin; kb < kb_end; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint64_t sob = static_cast<uint64_t>(stage * C::kStageBytes) >> 4;
+          const uint64_t soa = static_cast<uint64_t>(kb * C::kABytes) >> 4;
+          if (issuer) {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16_2sm(d_tmem, a0 + soa + ((k * kStepA) >> 4), b0 + sob + ((k * kStepB) >> 4),
+                            idesc, (kb != kb_begin || k != 0) ? 1u : 0u);
+            umma_commit_2sm(&empty_bar[stage], pair_mask);
+          }
+          __syncwarp();
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (issuer) umma_commit_2sm(&tfull_bar[acc], pair_mask);
+        // the row block ends here: the producer may overwrite the A panel once these MMAs
+        // have read it
+        const int wn = seq_tile(wi + 1);
+        if (wn < num_work && tile_m(wn) != m && issuer) umma_commit_2sm(a_empty, pair_mask);
+        __syncwarp();
+      }
+    }
+  } else if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
     int stage = 0;
     uint32_t phase = 0;
@@ -531,7 +659,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
           pf_lo += n;
         }
         if (elect_one()) {
-          uint8_t* sa = smem + stage * C::kStageBytes;
+          uint8_t* sa = sbase + stage * C::kStageBytes;
           uint8_t* sb = sa + C::kABytes;
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], tx);
           if (kMc >= 2) {  // my 1/kMc of the A slice, to me and my twins in the other pairs
@@ -589,7 +717,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo>::kThreads2, 1)
       constexpr uint32_t idesc = idesc_bf16_f32(256, BN, A_MN, B_MN);
       // descriptors of stage 0 / k = 0; stage s, k-step k add (s*stage + k*step) >> 4 to the
       // 14-bit start-address field (smem offsets < 256 KB never carry out of it)
-      const uint32_t s0 = smem_u32(smem);
+      const uint32_t s0 = smem_u32(sbase);
       const uint64_t a0 = A_MN ? smem_desc_sw128(s0, kMnBlockBytes, 1024) : smem_desc_sw128(s0, 16, 1024);
       const uint64_t b0 = B_MN ? smem_desc_sw128(s0 + C::kABytes, kMnBlockBytes, 1024)
                                : smem_desc_sw128(s0 + C::kABytes, 16, 1024);
@@ -1370,11 +1498,11 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int 
 // prepare_only: set the kernel's attributes on the current device and query its cluster
 // occupancy (this also loads the function), without launching -- gemm_prepare_device()
 template <int BN, bool A_MN, bool B_MN, bool kSgd = false, int kMc = 1, int kSk = 1,
-          bool kX = false, int kLo = 0>
+          bool kX = false, int kLo = 0, bool kAres = false>
 int launch_gemm_2sm(const GemmPlan& p, cudaStream_t stream, float scale = 0.f,
                     bool prepare_only = false) {
-  using Cf = Cfg2<BN, kSgd, kLo>;
-  auto kern = gemm_bf16_2sm_kernel<BN, A_MN, B_MN, kSgd, kMc, kSk, kX, kLo>;
+  using Cf = Cfg2<BN, kSgd, kLo, kAres>;
+  auto kern = gemm_bf16_2sm_kernel<BN, A_MN, B_MN, kSgd, kMc, kSk, kX, kLo, kAres>;
   constexpr int kCl = 2 * kMc * kSk;  // CTAs per cluster
   // per device: the attribute lives in each context.  Atomic: a newcomer's replica is
   // prepared on a side thread while the step thread launches on the other devices.
@@ -1485,6 +1613,16 @@ static bool gemm_multicast_enabled() {
   return on != 0;
 }
 
+
+// EDL_SGD_ARES: the A-resident split-master fused SGD kernel
+static bool sgd_ares_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("EDL_SGD_ARES");
+    on = e ? atoi(e) != 0 : 0;
+  }
+  return on != 0;
+}
 
 // L2 prefetch distances; EDL_GEMM_PF_KB / EDL_GEMM_PF_TILES override (tuning runs).
 static void gemm_prefetch_defaults(EpiParams* ep) {
@@ -1643,6 +1781,10 @@ int gemm_prepare_device() {
   if (!rc) rc = launch_gemm_2sm<128, true, true, true, 1, 1, false, 1>(p, nullptr, 0.f, true);
   if (!rc) rc = launch_gemm_2sm<128, true, true, true, 1, 1, false, 2>(p, nullptr, 0.f, true);
   if (!rc) rc = launch_gemm_2sm<128, true, true, true, 1, 1, false, 3>(p, nullptr, 0.f, true);
+  if (!rc && sgd_ares_enabled()) {
+    rc = launch_gemm_2sm<128, true, true, true, 1, 1, false, 1, true>(p, nullptr, 0.f, true);
+    if (!rc) rc = launch_gemm_2sm<128, true, true, true, 1, 1, false, 3, true>(p, nullptr, 0.f, true);
+  }
   if (!rc) rc = launch_gemm_2sm<128, false, false, false, 1>(p, nullptr, 0.f, true);
   if (!rc) rc = launch_gemm_2sm<128, false, true, false, 1>(p, nullptr, 0.f, true);
   if (!rc) rc = gemm_pair_prepare_device(nullptr);
@@ -1722,7 +1864,13 @@ int gemm_plan_run(const GemmPlan& p, cudaStream_t stream, float sgd_scale) {
       if (p.bn != 128 || p.mc != 1 || p.ep.xchg) return fail(EDL_EINVAL, "gemm: split-master plan shape");
       if (p.lo != 1 && !p.lo_master) return fail(EDL_EINVAL, "gemm: split-master conversion needs the fp32 master");
       if (p.lo == 2) return launch_gemm_2sm<128, true, true, true, 1, 1, false, 2>(p, stream, sgd_scale);
-      if (p.lo == 3) return launch_gemm_2sm<128, true, true, true, 1, 1, false, 3>(p, stream, sgd_scale);
+      // A-resident variant (EDL_SGD_ARES, K <= 512 in whole k-blocks)
+      const bool ares = sgd_ares_enabled() && p.K % BK == 0 && p.K <= 512;
+      if (p.lo == 3) {
+        if (ares) return launch_gemm_2sm<128, true, true, true, 1, 1, false, 3, true>(p, stream, sgd_scale);
+        return launch_gemm_2sm<128, true, true, true, 1, 1, false, 3>(p, stream, sgd_scale);
+      }
+      if (ares) return launch_gemm_2sm<128, true, true, true, 1, 1, false, 1, true>(p, stream, sgd_scale);
       return launch_gemm_2sm<128, true, true, true, 1, 1, false, 1>(p, stream, sgd_scale);
     }
     if (wgrad_sgd_bres_eligible(p)) return wgrad_sgd_bres_run(p, stream, sgd_scale);

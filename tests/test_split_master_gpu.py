@@ -132,3 +132,19 @@ def test_split_fused_update_matches_fp32_master(L, M, N, K):
                                       C.c_float(0.0), _s()) == 2
     assert L.edl_gemm_wgrad_sgd_split(P(dy), M, P(x), N, P(lo), P(Wl), P(ms), 4, N, M, N, K,
                                       C.c_float(0.0), _s()) == 2
+
+
+def test_split_fused_update_a_resident_variant():
+    """The opt-in A-resident kernel (EDL_SGD_ARES=1: the dY panel of a row block stays in
+    shared memory, only X streams) runs the same checks; the switch is read once per process,
+    so the checks run in a child process."""
+    import os
+    import subprocess
+    import sys
+    if os.environ.get("EDL_SGD_ARES") == "1":
+        pytest.skip("already the A-resident variant")
+    env = dict(os.environ, EDL_SGD_ARES="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-k",
+                        "matches_fp32_master", os.path.abspath(__file__)],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
