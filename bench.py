@@ -690,12 +690,12 @@ def elastic_leg_mp(args, rank: int, world: int, local: int, dist) -> dict:
 
 
 NCU_FULL = "profiles/r01_ncu_full.md"
-NCU_STEP = "profiles/r02s_kernel_shares.md"
+NCU_STEP = "profiles/r02f_kernel_shares.md"
 
 
 def _ncu_traffic(family: str):
     """DRAM read + write bytes per launch of a kernel family: from the round-2 launch list
-    with caches not flushed between kernels (profiles/r02s_kernel_shares.md, DRAM table: the
+    with caches not flushed between kernels (profiles/r02f_kernel_shares.md, DRAM table: the
     dirty lines a launch leaves in L2 are counted where they are written back), else the
     round-1 `ncu --set full` capture (profiles/r01_ncu_full.md), or None."""
     here = os.path.dirname(os.path.abspath(__file__))

@@ -15,15 +15,21 @@ import subprocess
 OPS = ["UTCHMMA", "UTCBAR", "UTMALDG", "UTMASTG", "UTMAPF", "UBLKCP", "UBLKPF", "LDTM",
        "SYNCS", "LDL", "STL"]
 HOT = [
-    ("gemm_bf16_2sm_kernel<128, false, false, false, 2, 1, false>", "fwd GEMM (K-major A/B, A multicast)"),
-    ("gemm_bf16_2sm_kernel<128, false, true, false, 2, 1, false>", "dgrad GEMM (MN-major B, A multicast)"),
-    ("gemm_bf16_2sm_kernel<128, true, true, true, 1, 1, false>", "wgrad + fused SGD (N=1 dominant)"),
-    ("gemm_bf16_2sm_kernel<128, true, true, false, 1, 1, false>", "wgrad (N>1, reduce-scatter routed)"),
-    ("gemm_bf16_2sm_kernel<128, true, true, true, 1, 1, true>", "wgrad + fused exchange (mode 4)"),
+    ("gemm_bf16_2sm_kernel<128, false, false, false, 2, 1, false, 0, false>", "fwd GEMM (K-major A/B, A multicast)"),
+    ("gemm_bf16_2sm_kernel<128, false, true, false, 2, 1, false, 0, false>", "dgrad GEMM (MN-major B, A multicast)"),
+    ("gemm_bf16_2sm_kernel<128, true, true, true, 1, 1, false, 1, false>", "wgrad + fused SGD, split master (N=1 dominant)"),
+    ("gemm_bf16_2sm_kernel<128, true, true, true, 1, 1, false, 2, false>", "wgrad + fused SGD, split in / fp32 out (before a switch)"),
+    ("gemm_bf16_2sm_kernel<128, true, true, true, 1, 1, false, 3, false>", "wgrad + fused SGD, fp32 in / split out (after a switch)"),
+    ("gemm_bf16_2sm_kernel<128, true, true, true, 1, 1, false, 1, true>", "wgrad + fused SGD, split master, A resident (opt-in)"),
+    ("gemm_bf16_2sm_kernel<128, true, true, true, 1, 1, false, 0, false>", "wgrad + fused SGD, fp32 master"),
+    ("gemm_bf16_2sm_kernel<128, true, true, false, 1, 1, false, 0, false>", "wgrad (N>1, reduce-scatter routed)"),
+    ("gemm_bf16_2sm_kernel<128, true, true, true, 1, 1, true, 0, false>", "wgrad + fused exchange (mode 4)"),
     ("push_allreduce_sgd_kernel<false>", "push all-gather + sharded SGD (N>1)"),
     ("push_allreduce_sgd_kernel<true>", "push all-gather + sharded SGD + momentum"),
     ("xent_kernel<16>", "softmax-CE + loss sum"),
     ("gather_inline_kernel", "leased-run gather"),
+    ("master_split_kernel", "split master: fp32 -> (W, lo)"),
+    ("master_join_kernel", "split master: (W, lo) -> fp32"),
     ("wgrad_sgd_bres_kernel", "B-resident wgrad + SGD (opt-in)"),
     ("bwd_pair_kernel", "dgrad l-1 + wgrad/SGD l pair (opt-in)"),
 ]

@@ -33,10 +33,14 @@ def family(name: str) -> str:
         b = b in ("1", "true")
         sgd = sgd in ("1", "true")
         role = "wgrad+sgd" if sgd else ("wgrad" if a and b else ("dgrad" if b else "fwd"))
-        lo = re.search(r"gemm_bf16_2sm_kernel<[^>]*, (\d)>", name)
-        if sgd and lo and lo.group(1) != "0":
+        targs = re.search(r"gemm_bf16_2sm_kernel<([^>]*)>", name)
+        args = [a.strip() for a in targs.group(1).split(",")] if targs else []
+        lo = args[7] if len(args) > 7 else "0"
+        if sgd and lo != "0":
             role += {"1": ", split master", "2": ", split in / fp32 out",
-                     "3": ", fp32 in / split out"}.get(lo.group(1), "")
+                     "3": ", fp32 in / split out"}.get(lo, "")
+            if len(args) > 8 and args[8] in ("1", "true"):
+                role += ", A resident"
         return f"{kind}<BN={bn}> [{role}]"
     for k in ("allreduce_sgd", "xent_kernel", "sum_rows", "gather_kernel", "gen_bf16", "gen_f64",
               "init_kernel", "ordered_sum", "linear_allreduce"):
