@@ -253,8 +253,19 @@ __global__ void gather_inline_kernel(const uint8_t* __restrict__ src,
     const uint8_t* s = src + id * row_bytes;
     uint8_t* d = dst + static_cast<size_t>(r) * row_bytes;
     if ((row_bytes & 15) == 0) {
-      for (size_t off = threadIdx.x * 16; off < row_bytes; off += blockDim.x * 16)
-        *reinterpret_cast<uint4*>(d + off) = __ldg(reinterpret_cast<const uint4*>(s + off));
+      // every load of the row issued before the first store (4 x 16 B in flight per thread)
+      const size_t n16 = row_bytes / 16;
+      const uint4* s16 = reinterpret_cast<const uint4*>(s);
+      uint4* d16 = reinterpret_cast<uint4*>(d);
+      for (size_t base = threadIdx.x; base < n16; base += 4 * blockDim.x) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (base + u * blockDim.x < n16) v[u] = __ldg(s16 + base + u * blockDim.x);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (base + u * blockDim.x < n16) d16[base + u * blockDim.x] = v[u];
+      }
     } else {
       for (size_t off = threadIdx.x; off < row_bytes; off += blockDim.x) d[off] = s[off];
     }
