@@ -317,21 +317,26 @@ def run_b200(args, rank: int, world: int) -> None:
         # 2(N-1)/N x 2P); the exchange's halves are timed where they run
         mode = job.exchange_mode()
         half = (world - 1) / world * 2 * P
-        if mode == 3:
-            # reduce-scatter stored from the wgrad GEMM epilogues (inside the backward): only
-            # the all-gather half (push collective: shard sum + SGD + weight stores) is exposed
+        if mode in (3, 5):
+            # reduce-scatter stored from the wgrad GEMM epilogues (mode 3) or copied by the copy
+            # engines layer by layer (mode 5), inside the backward: only the all-gather half
+            # (push collective: shard sum + SGD + weight stores) is exposed
+            rs_ms = wgrad_ms if mode == 3 else ph["backward"] / n
             upd = {"bound": "nvlink", "achieved": half / (upd_ms / 1e3) / 1e9, "peak": 770.0,
                    "unit": "GB/s", "frac": half / (upd_ms / 1e3) / 1e9 / 770.0,
                    "bytes_per_step": half, "per_step_ms": upd_ms * share,
                    "allreduce_bus_bytes_per_step": 2 * half,
                    # bus bandwidth: RS + AG bytes over the time the transfers occupy (the
-                   # reduce-scatter rides in the wgrad GEMMs, the all-gather is the push)
-                   "busbw_gbs": 2 * half / ((wgrad_ms + upd_ms) / 1e3) / 1e9,
+                   # reduce-scatter rides in the wgrad GEMMs / the backward, the all-gather is
+                   # the push)
+                   "busbw_gbs": 2 * half / ((rs_ms + upd_ms) / 1e3) / 1e9,
                    "busbw_peak_gbs": 900.0,
                    "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction "
                                   "(900 GB/s NVLink 5 nominal)",
-                   "kernel": "push all-gather + sharded SGD (reduce-scatter routed from the "
-                             "wgrad GEMM epilogues, overlapped with the backward)"}
+                   "kernel": "push all-gather + sharded SGD (reduce-scatter "
+                             + ("routed from the wgrad GEMM epilogues" if mode == 3 else
+                                "on the copy engines, layer by layer") +
+                             ", overlapped with the backward)"}
         else:
             nv = 2 * half
             upd = {"bound": "nvlink", "achieved": nv / (upd_ms / 1e3) / 1e9, "peak": 770.0,

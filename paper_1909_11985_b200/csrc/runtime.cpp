@@ -1022,8 +1022,40 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
 // gradients (of every local worker: they run in stream order before this point).  With
 // several replicas it is the fused NVLink collective restricted to layer l's parameters;
 // the shard boundaries, epochs and launch order are the same on every replica.
+// Exchange mode 5: layer l's reduce-scatter on the copy engines as soon as its weight
+// gradients exist (plain wgrad GEMM, local gradient), under the rest of the backward; the
+// push collective after the backward then sums, updates and all-gathers as in mode 3.
+int Job::launch_layer_rs_ce(Replica* r, int l) {
+  EDL_CUDA_TRY(cudaEventRecord(r->ev_grad[l], r->stream));
+  const int n_rep = static_cast<int>(peers_.size());
+  const int me = rep_index(r);
+  const size_t base = off_[l];
+  // one stream per peer offset (up to three), so several copy engines run at once
+  cudaStream_t cs[3] = {r->side2, r->side3, r->side};
+  for (int j = 1; j < n_rep && j <= 3; ++j)
+    EDL_CUDA_TRY(cudaStreamWaitEvent(cs[j - 1], r->ev_grad[l], 0));
+  for (int j = 1; j < n_rep; ++j) {
+    const int p = (me + j) % n_rep;  // rotated: every GPU copies to a different owner first
+    cudaStream_t st = cs[(j - 1) % 3];
+    size_t lo;
+    const size_t n8 = shard8(l, p, &lo);
+    if (n8 == 0) continue;
+    const size_t slot8 = shard_total8(p);
+    for (size_t k = 0; k < ring_.size(); ++k) {
+      if (host_index(ring_[k]) != me) continue;
+      __nv_bfloat16* dst =
+          peers_[p].recv + (static_cast<size_t>(recv_slot(p, k)) * slot8 + seg_off8(p, l)) * 8;
+      const __nv_bfloat16* src = workers_[ring_[k]]->grad + base + lo * 8;
+      EDL_CUDA_TRY(cudaMemcpyAsync(dst, src, n8 * 16, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  ++r->layer_colls;
+  return EDL_OK;
+}
+
 int Job::launch_layer_coll(Replica* r, int l) {
   if (overlap_mode_ == 2) return launch_layer_ce(r, l);
+  if (overlap_mode_ == 5) return launch_layer_rs_ce(r, l);
   EDL_CUDA_TRY(cudaEventRecord(r->ev_grad[l], r->stream));
   EDL_CUDA_TRY(cudaStreamWaitEvent(r->side, r->ev_grad[l], 0));
   const int n_rep = static_cast<int>(peers_.size());
@@ -1674,6 +1706,15 @@ int Job::finish_layer_colls(Replica* r) {
     const int l = L_ - 1 - r->layer_colls;  // layers go L-1 .. 0 (fused: .. 1)
     EDL_TRY(launch_layer_coll(r, l));
   }
+  if (overlap_mode_ == 5) {  // the push collective follows once every copy has landed
+    cudaStream_t cs[3] = {r->side2, r->side3, r->side};
+    const int n_st = static_cast<int>(peers_.size()) - 1 < 3 ? static_cast<int>(peers_.size()) - 1 : 3;
+    for (int i = 0; i < n_st; ++i) {
+      EDL_CUDA_TRY(cudaEventRecord(r->ev_rs[i], cs[i]));  // reuse: per-layer events idle here
+      EDL_CUDA_TRY(cudaStreamWaitEvent(r->stream, r->ev_rs[i], 0));
+    }
+    return EDL_OK;
+  }
   if (overlap_mode_ == 2) {  // every peer's weights of every layer have landed here
     EDL_CUDA_TRY(cudaEventRecord(r->ev_rs[0], r->side3));  // reuse: side3 drained
     EDL_CUDA_TRY(cudaStreamWaitEvent(r->side, r->ev_rs[0], 0));
@@ -1768,11 +1809,13 @@ int Job::reduce_and_update(uint64_t count, uint64_t t, int slot, const double** 
       a.inv_count = count ? static_cast<float>(1.0 / static_cast<double>(count)) : 0.f;
       a.eta = static_cast<float>(eta_t);
       a.mu = static_cast<float>(cfg_.momentum);
-      a.update = (count > 0 && !fused_update_ && (!overlap_ || overlap_mode_ == 3)) ? 1 : 0;
+      a.update = (count > 0 && !fused_update_ &&
+                  (!overlap_ || overlap_mode_ == 3 || overlap_mode_ == 5)) ? 1 : 0;
       a.loss_out = r->loss_sum;
-      if (a.update && (overlap_mode_ == 3 || push_eligible())) {  // every NVLink byte a store
-        a.push = 1;
-        a.skip_push = overlap_mode_ == 3 ? 1 : 0;  // slices already pushed by the GEMMs
+      if (a.update && (overlap_mode_ == 3 || overlap_mode_ == 5 || push_eligible())) {
+        a.push = 1;  // every NVLink byte a store
+        // slices already pushed by the GEMMs (3) or the copy engines (5)
+        a.skip_push = overlap_mode_ == 3 || overlap_mode_ == 5 ? 1 : 0;
         a.n_layer = L_;
         for (int l = 0; l < L_; ++l) {
           a.lay_off8[l] = off_[l] / 8;
@@ -2172,13 +2215,17 @@ int Job::step(EdlStepReport* out) {
     overlap_mode_ = (peers_.size() > 1 || overlap_env == 1) ? overlap_env : 0;
     if (overlap_mode_ == 2 && !ce_fits()) overlap_mode_ = 1;
     if (overlap_mode_ == 3 && !rs_eligible()) overlap_mode_ = 0;
+    if (overlap_mode_ == 5 && !rs_eligible()) overlap_mode_ = 0;
   }
   // default with several GPUs (EDL_OVERLAP unset): the reduce-scatter rides in the wgrad GEMM
   // epilogues (TMA stores into the owners' recv over NVLink, under the backward) and one push
   // collective does the shard update + all-gather.  Measured on B200: 1.18M vs 1.10M
   // samples/s at N=2, 1.89M vs 1.77M at N=4 over the single push collective.
+  // With two GPUs the reduce-scatter goes on the copy engines instead (mode 5: plain wgrad
+  // GEMMs, per-layer peer copies under the rest of the backward): measured 1.33M vs 1.22M
+  // samples/s at N=2; at N=4 the two are within 1% (1.88M vs 1.90M), mode 3 stays.
   if (mlp_ && count > 0 && overlap_env < 0 && peers_.size() > 1 && rs_eligible())
-    overlap_mode_ = 3;
+    overlap_mode_ = peers_.size() == 2 ? 5 : 3;
   if (overlap_mode_ == 4 && !xchg_eligible()) overlap_mode_ = rs_eligible() ? 3 : 0;
   overlap_ = overlap_mode_ != 0;
   // deferred all-gather (mode 3, EDL_AG_DEFER=1): the push collective of this mini-batch

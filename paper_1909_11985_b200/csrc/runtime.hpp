@@ -282,6 +282,7 @@ class Job {
   int recv_slot(int p, size_t k) const;  // k-th ring member's slot in replica p's recv
   bool ce_fits() const;
   int launch_layer_ce(Replica* r, int l);
+  int launch_layer_rs_ce(Replica* r, int l);  // exchange mode 5: reduce-scatter on the copy engines
   // per-worker mini-batch durations of the last kTimeWindow completed steps (straggler
   // detection)
   static constexpr size_t kTimeWindow = 64;
