@@ -317,11 +317,11 @@ def run_b200(args, rank: int, world: int) -> None:
         # 2(N-1)/N x 2P); the exchange's halves are timed where they run
         mode = job.exchange_mode()
         half = (world - 1) / world * 2 * P
-        if mode in (3, 5):
+        if mode in (3, 5, 6):
             # reduce-scatter stored from the wgrad GEMM epilogues (mode 3) or copied by the copy
             # engines layer by layer (mode 5), inside the backward: only the all-gather half
             # (push collective: shard sum + SGD + weight stores) is exposed
-            rs_ms = wgrad_ms if mode == 3 else ph["backward"] / n
+            rs_ms = wgrad_ms if mode == 3 else ph["backward"] / n  # 5 / 6: under the backward
             upd = {"bound": "nvlink", "achieved": half / (upd_ms / 1e3) / 1e9, "peak": 770.0,
                    "unit": "GB/s", "frac": half / (upd_ms / 1e3) / 1e9 / 770.0,
                    "bytes_per_step": half, "per_step_ms": upd_ms * share,
@@ -334,8 +334,9 @@ def run_b200(args, rank: int, world: int) -> None:
                    "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction "
                                   "(900 GB/s NVLink 5 nominal)",
                    "kernel": "push all-gather + sharded SGD (reduce-scatter "
-                             + ("routed from the wgrad GEMM epilogues" if mode == 3 else
-                                "on the copy engines, layer by layer") +
+                             + {3: "routed from the wgrad GEMM epilogues",
+                                5: "on the copy engines, layer by layer",
+                                6: "split between the wgrad GEMM epilogues and the copy engines"}[mode] +
                              ", overlapped with the backward)"}
         else:
             nv = 2 * half

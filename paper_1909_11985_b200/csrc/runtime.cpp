@@ -810,7 +810,9 @@ int Job::ensure_plans(Worker* w, int64_t rows) {
     }
     w->plan_rows = rows;
   }
-  if (overlap_mode_ == 3 && (w->rs_plan_rows != rows || w->rs_plan_version != version_)) {
+  if ((overlap_mode_ == 3 || overlap_mode_ == 6) &&
+      (w->rs_plan_rows != rows || w->rs_plan_version != version_ ||
+       w->rs_plan_mode != overlap_mode_)) {
     const int n = static_cast<int>(peers_.size());
     const int me = rep_index(r);
     w->wgrad_rs.assign(static_cast<size_t>(L_), GemmPlan{});
@@ -824,6 +826,11 @@ int Job::ensure_plans(Worker* w, int64_t rows) {
       void* dst[kMaxPeerMaps] = {};
       for (int o = 0; o < n; ++o) {  // the push collective's recv layout (collective.cu)
         if (o == me) continue;
+        if (overlap_mode_ == 6 && rs_via_ce((o - me + n) % n, n)) {
+          // mode 6: this owner's rows stay local; the copy engines move them (rs_ce)
+          dst[o] = w->grad + off_[l] + static_cast<size_t>(o) * prow * in_[l];
+          continue;
+        }
         const size_t slot = static_cast<size_t>(me < o ? me : me - 1);
         dst[o] = peers_[o].recv + (slot * shard_total8(o) + seg_off8(o, l)) * 8;
       }
@@ -831,6 +838,7 @@ int Job::ensure_plans(Worker* w, int64_t rows) {
     }
     w->rs_plan_rows = rows;
     w->rs_plan_version = version_;
+    w->rs_plan_mode = overlap_mode_;
   }
   if (overlap_mode_ == 4 && (w->x_plan_rows != rows || w->x_plan_version != version_)) {
     const int n = static_cast<int>(peers_.size());
@@ -990,12 +998,14 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
       // dW + reduce-scatter + sharded SGD + weight all-gather in one kernel per layer
       EDL_TRY(gemm_plan_run(w->wgrad_x[l], r->stream, step_scale_));
       if (mw) mark(slot, 5, mw, r->stream);
-    } else if (overlap_mode_ == 3) {
+    } else if (overlap_mode_ == 3 || overlap_mode_ == 6) {
       // dW with the reduce-scatter in its epilogue: rows owned elsewhere are stored into the
       // owner's recv over NVLink while the backward continues; the shard update + all-gather
       // run once, after the backward (the push collective with its phase A skipped)
       EDL_TRY(gemm_plan_run(w->wgrad_rs[l], r->stream));
       if (mw) mark(slot, 5, mw, r->stream);
+      // mode 6: the far owners' rows were written locally; the copy engines move them
+      if (overlap_mode_ == 6 && last) EDL_TRY(launch_layer_rs_ce(r, l));
     } else {
       EDL_TRY(gemm_plan_run(w->wgrad[l], r->stream));
       if (mw) mark(slot, 5, mw, r->stream);
@@ -1035,6 +1045,7 @@ int Job::launch_layer_rs_ce(Replica* r, int l) {
   for (int j = 1; j < n_rep && j <= 3; ++j)
     EDL_CUDA_TRY(cudaStreamWaitEvent(cs[j - 1], r->ev_grad[l], 0));
   for (int j = 1; j < n_rep; ++j) {
+    if (overlap_mode_ == 6 && !rs_via_ce(j, n_rep)) continue;  // stored by the wgrad GEMM
     const int p = (me + j) % n_rep;  // rotated: every GPU copies to a different owner first
     cudaStream_t st = cs[(j - 1) % 3];
     size_t lo;
@@ -1053,9 +1064,24 @@ int Job::launch_layer_rs_ce(Replica* r, int l) {
   return EDL_OK;
 }
 
+// Mode 6 (three or more GPUs): the reduce-scatter to the nearest EDL_RS_TMA_PEERS peer
+// offsets (default (N-1)/2, at least 1) is stored from the wgrad GEMM epilogues (mode 3), to the others by the
+// copy engines (mode 5), so SM stores and copy engines share the NVLink egress.
+bool Job::rs_via_ce(int j, int n_rep) const {
+  // default: half of the peers (rounded down, at least one) through the SM stores; measured
+  // at N=4: 1 peer 2.013M, 2 peers 2.019M samples/s
+  static int tma_env = -2;
+  if (tma_env == -2) {
+    const char* e = getenv("EDL_RS_TMA_PEERS");
+    tma_env = e ? atoi(e) : -1;
+  }
+  const int tma_peers = tma_env >= 0 ? tma_env : ((n_rep - 1) / 2 > 1 ? (n_rep - 1) / 2 : 1);
+  return j > tma_peers && j < n_rep;
+}
+
 int Job::launch_layer_coll(Replica* r, int l) {
   if (overlap_mode_ == 2) return launch_layer_ce(r, l);
-  if (overlap_mode_ == 5) return launch_layer_rs_ce(r, l);
+  if (overlap_mode_ == 5 || overlap_mode_ == 6) return launch_layer_rs_ce(r, l);
   EDL_CUDA_TRY(cudaEventRecord(r->ev_grad[l], r->stream));
   EDL_CUDA_TRY(cudaStreamWaitEvent(r->side, r->ev_grad[l], 0));
   const int n_rep = static_cast<int>(peers_.size());
@@ -1706,7 +1732,7 @@ int Job::finish_layer_colls(Replica* r) {
     const int l = L_ - 1 - r->layer_colls;  // layers go L-1 .. 0 (fused: .. 1)
     EDL_TRY(launch_layer_coll(r, l));
   }
-  if (overlap_mode_ == 5) {  // the push collective follows once every copy has landed
+  if (overlap_mode_ == 5 || overlap_mode_ == 6) {  // the push follows once every copy landed
     cudaStream_t cs[3] = {r->side2, r->side3, r->side};
     const int n_st = static_cast<int>(peers_.size()) - 1 < 3 ? static_cast<int>(peers_.size()) - 1 : 3;
     for (int i = 0; i < n_st; ++i) {
@@ -1810,12 +1836,12 @@ int Job::reduce_and_update(uint64_t count, uint64_t t, int slot, const double** 
       a.eta = static_cast<float>(eta_t);
       a.mu = static_cast<float>(cfg_.momentum);
       a.update = (count > 0 && !fused_update_ &&
-                  (!overlap_ || overlap_mode_ == 3 || overlap_mode_ == 5)) ? 1 : 0;
+                  (!overlap_ || overlap_mode_ == 3 || overlap_mode_ >= 5)) ? 1 : 0;
       a.loss_out = r->loss_sum;
-      if (a.update && (overlap_mode_ == 3 || overlap_mode_ == 5 || push_eligible())) {
+      if (a.update && (overlap_mode_ == 3 || overlap_mode_ >= 5 || push_eligible())) {
         a.push = 1;  // every NVLink byte a store
         // slices already pushed by the GEMMs (3) or the copy engines (5)
-        a.skip_push = overlap_mode_ == 3 || overlap_mode_ == 5 ? 1 : 0;
+        a.skip_push = overlap_mode_ == 3 || overlap_mode_ >= 5 ? 1 : 0;
         a.n_layer = L_;
         for (int l = 0; l < L_; ++l) {
           a.lay_off8[l] = off_[l] / 8;
@@ -2215,7 +2241,8 @@ int Job::step(EdlStepReport* out) {
     overlap_mode_ = (peers_.size() > 1 || overlap_env == 1) ? overlap_env : 0;
     if (overlap_mode_ == 2 && !ce_fits()) overlap_mode_ = 1;
     if (overlap_mode_ == 3 && !rs_eligible()) overlap_mode_ = 0;
-    if (overlap_mode_ == 5 && !rs_eligible()) overlap_mode_ = 0;
+    if ((overlap_mode_ == 5 || overlap_mode_ == 6) && !rs_eligible()) overlap_mode_ = 0;
+    if (overlap_mode_ == 6 && peers_.size() < 3) overlap_mode_ = 5;
   }
   // default with several GPUs (EDL_OVERLAP unset): the reduce-scatter rides in the wgrad GEMM
   // epilogues (TMA stores into the owners' recv over NVLink, under the backward) and one push
@@ -2223,9 +2250,11 @@ int Job::step(EdlStepReport* out) {
   // samples/s at N=2, 1.89M vs 1.77M at N=4 over the single push collective.
   // With two GPUs the reduce-scatter goes on the copy engines instead (mode 5: plain wgrad
   // GEMMs, per-layer peer copies under the rest of the backward): measured 1.33M vs 1.22M
-  // samples/s at N=2; at N=4 the two are within 1% (1.88M vs 1.90M), mode 3 stays.
+  // samples/s at N=2.  From three GPUs on it is split (mode 6): the nearest peers' rows are
+  // stored from the wgrad epilogues, the others' by the copy engines: N=4 2.01M vs 1.91M
+  // (mode 3) and 1.82M (mode 5).
   if (mlp_ && count > 0 && overlap_env < 0 && peers_.size() > 1 && rs_eligible())
-    overlap_mode_ = peers_.size() == 2 ? 5 : 3;
+    overlap_mode_ = peers_.size() == 2 ? 5 : 6;
   if (overlap_mode_ == 4 && !xchg_eligible()) overlap_mode_ = rs_eligible() ? 3 : 0;
   overlap_ = overlap_mode_ != 0;
   // deferred all-gather (mode 3, EDL_AG_DEFER=1): the push collective of this mini-batch

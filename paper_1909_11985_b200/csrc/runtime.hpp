@@ -124,6 +124,7 @@ struct Worker {
   uint64_t x_plan_version = 0;
   int64_t rs_plan_rows = -1;
   uint64_t rs_plan_version = 0;
+  int rs_plan_mode = 0;
   int64_t plan_rows = -1;
   int64_t sgd_plan_rows = -1;
   Cursor cur;
@@ -282,7 +283,8 @@ class Job {
   int recv_slot(int p, size_t k) const;  // k-th ring member's slot in replica p's recv
   bool ce_fits() const;
   int launch_layer_ce(Replica* r, int l);
-  int launch_layer_rs_ce(Replica* r, int l);  // exchange mode 5: reduce-scatter on the copy engines
+  int launch_layer_rs_ce(Replica* r, int l);
+  bool rs_via_ce(int peer_offset, int n_rep) const;  // mode 6: this owner via the copy engines  // exchange mode 5: reduce-scatter on the copy engines
   // per-worker mini-batch durations of the last kTimeWindow completed steps (straggler
   // detection)
   static constexpr size_t kTimeWindow = 64;

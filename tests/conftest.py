@@ -1,7 +1,14 @@
 import os
 import sys
 
-import pytest
+# The CPU oracle (oracle/mlp.py) runs float32 torch matmuls on MKL, whose kernels can take
+# alignment-dependent code paths: measured, 1 run in 20 of the same job gave an oracle loss
+# differing in the 6th digit (the GPU results were bit-identical in all 20).  Pin MKL's
+# code path (Conditional Numerical Reproducibility) before torch initialises it; the
+# multi-process workers inherit it through the environment.
+os.environ.setdefault("MKL_CBWR", "AVX2")
+
+import pytest  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:

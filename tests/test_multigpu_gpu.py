@@ -22,7 +22,7 @@ pytestmark = pytest.mark.gpu
 # weight-gradient GEMMs, per-tile arrival counters across GPUs.
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("overlap", ["", "0", "1", "2", "3", "3/defer", "3/defer-ce", "4", "5"])
+@pytest.mark.parametrize("overlap", ["", "0", "1", "2", "3", "3/defer", "3/defer-ce", "4", "5", "6"])
 def test_two_or_more_gpus_match_oracle(overlap):
     n = min(torch.cuda.device_count(), 4)
     here = os.path.dirname(os.path.abspath(__file__))
