@@ -810,7 +810,7 @@ int Job::ensure_plans(Worker* w, int64_t rows) {
     }
     w->plan_rows = rows;
   }
-  if ((overlap_mode_ == 3 || overlap_mode_ == 6) &&
+  if ((overlap_mode_ == 3 || overlap_mode_ == 6 || (overlap_mode_ == 5 && rs_tma_every() > 0)) &&
       (w->rs_plan_rows != rows || w->rs_plan_version != version_ ||
        w->rs_plan_mode != overlap_mode_)) {
     const int n = static_cast<int>(peers_.size());
@@ -998,7 +998,8 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
       // dW + reduce-scatter + sharded SGD + weight all-gather in one kernel per layer
       EDL_TRY(gemm_plan_run(w->wgrad_x[l], r->stream, step_scale_));
       if (mw) mark(slot, 5, mw, r->stream);
-    } else if (overlap_mode_ == 3 || overlap_mode_ == 6) {
+    } else if (overlap_mode_ == 3 || overlap_mode_ == 6 ||
+               (overlap_mode_ == 5 && rs_tma_every() > 0 && l % rs_tma_every() == 0)) {
       // dW with the reduce-scatter in its epilogue: rows owned elsewhere are stored into the
       // owner's recv over NVLink while the backward continues; the shard update + all-gather
       // run once, after the backward (the push collective with its phase A skipped)
@@ -1006,6 +1007,7 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
       if (mw) mark(slot, 5, mw, r->stream);
       // mode 6: the far owners' rows were written locally; the copy engines move them
       if (overlap_mode_ == 6 && last) EDL_TRY(launch_layer_rs_ce(r, l));
+      if (overlap_mode_ == 5 && last) ++r->layer_colls;  // this layer went out from the GEMM
     } else {
       EDL_TRY(gemm_plan_run(w->wgrad[l], r->stream));
       if (mw) mark(slot, 5, mw, r->stream);
@@ -1067,6 +1069,17 @@ int Job::launch_layer_rs_ce(Replica* r, int l) {
 // Mode 6 (three or more GPUs): the reduce-scatter to the nearest EDL_RS_TMA_PEERS peer
 // offsets (default (N-1)/2, at least 1) is stored from the wgrad GEMM epilogues (mode 3), to the others by the
 // copy engines (mode 5), so SM stores and copy engines share the NVLink egress.
+// Mode 5 variant (EDL_RS_TMA_EVERY=k): every k-th layer's reduce-scatter is stored from the
+// wgrad GEMM epilogue (mode 3) instead of the copy engines
+int Job::rs_tma_every() const {
+  static int k = -1;
+  if (k < 0) {
+    const char* e = getenv("EDL_RS_TMA_EVERY");
+    k = e ? atoi(e) : 0;
+  }
+  return k;
+}
+
 bool Job::rs_via_ce(int j, int n_rep) const {
   // default: half of the peers (rounded down, at least one) through the SM stores; measured
   // at N=4: 1 peer 2.013M, 2 peers 2.019M samples/s

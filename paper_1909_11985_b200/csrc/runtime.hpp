@@ -284,7 +284,8 @@ class Job {
   bool ce_fits() const;
   int launch_layer_ce(Replica* r, int l);
   int launch_layer_rs_ce(Replica* r, int l);
-  bool rs_via_ce(int peer_offset, int n_rep) const;  // mode 6: this owner via the copy engines  // exchange mode 5: reduce-scatter on the copy engines
+  bool rs_via_ce(int peer_offset, int n_rep) const;  // mode 6: this owner via the copy engines
+  int rs_tma_every() const;  // exchange mode 5: reduce-scatter on the copy engines
   // per-worker mini-batch durations of the last kTimeWindow completed steps (straggler
   // detection)
   static constexpr size_t kTimeWindow = 64;
