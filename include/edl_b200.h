@@ -293,7 +293,11 @@ void* edl_job_stream(const EdlJob* job);
 /* How the N>1 gradient exchange of this job runs (valid after the first step): 0 one fused
  * reduce-scatter + SGD + all-gather kernel after the backward, 1 per-layer side-stream
  * collectives, 2 per-layer copy-engine transfers, 3 reduce-scatter routed from the
- * weight-gradient GEMM epilogues + push all-gather (the default with one member per GPU). */
+ * weight-gradient GEMM epilogues + push all-gather, 4 the whole exchange inside the
+ * weight-gradient GEMMs, 5 reduce-scatter as per-layer copy-engine peer copies under the
+ * backward + push all-gather (the default with one member per GPU on two GPUs), 6 the
+ * reduce-scatter split between the GEMM epilogues (nearest peers) and the copy engines
+ * (the default from three GPUs).                                                          */
 int edl_job_exchange_mode(const EdlJob* job);
 /* Orders the job stream (edl_job_stream) after all device work of the launched mini-batches,
  * including the push collective that exchange mode 3 defers onto a side stream to overlap

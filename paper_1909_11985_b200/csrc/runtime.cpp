@@ -983,7 +983,7 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
       EDL_TRY(gemm_plan_run(q, r->stream));
     }
     const bool fused_here = fused_update_ && (!overlap_ || l == 0);
-    if (!fused_here && overlap_mode_ == 3 && r->side_pending) {
+    if (!fused_here && (overlap_mode_ == 3 || overlap_mode_ == 5) && r->side_pending) {
       // the previous push collective reads every replica's recv until its final barrier
       // (waited on before the wgrad sub-phase mark so the wait is not timed as GEMM work)
       EDL_CUDA_TRY(cudaStreamWaitEvent(r->stream, r->ev_push, 0));
@@ -2280,7 +2280,7 @@ int Job::step(EdlStepReport* out) {
     const char* e = getenv("EDL_AG_DEFER");
     defer_env = e && *e ? atoi(e) : 0;
   }
-  ag_defer_ = overlap_mode_ == 3 && defer_env != 0 && !cfg_.appx_recovery;
+  ag_defer_ = (overlap_mode_ == 3 || overlap_mode_ == 5) && defer_env != 0 && !cfg_.appx_recovery;
   // EDL_AG_DEFER=2: the all-gather half on the copy engines (launch_ag_ce).  Opt-in: measured
   // on B200 at N=2 the copies slow the forward GEMMs they overlap (GEMM time per mini-batch
   // 0.61 -> 0.74 ms) more than they save on the push kernel (0.26 -> 0.20 ms): 1.10M vs

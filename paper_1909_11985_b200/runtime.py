@@ -234,7 +234,9 @@ class Job:
 
     def exchange_mode(self) -> int:
         """0 fused collective after the backward, 1/2 per-layer overlap, 3 reduce-scatter
-        routed from the wgrad GEMM epilogues (include/edl_b200.h edl_job_exchange_mode)."""
+        routed from the wgrad GEMM epilogues, 4 exchange inside the wgrad GEMMs, 5 reduce-
+        scatter on the copy engines, 6 split between the two (include/edl_b200.h
+        edl_job_exchange_mode)."""
         return int(self._L.edl_job_exchange_mode(self._h))
 
     def join(self) -> None:
