@@ -811,8 +811,21 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo, kAres>::kThreads2, 1)
         tma_load_2d(dst, &pm.m[0], &mb[j % NB], c0, r0);         // fp32 master
       }
     };
+    // L2 prefetch (ep.pf_tiles tiles ahead, EDL_GEMM_PF_TILES) of this warp's chunk: the
+    // staged TMA load then hits L2 instead of paying the HBM latency
+    auto l2pf = [&](int jj) {
+      int r0, c0;
+      if (!coords(jj, &r0, &c0)) return;
+      if constexpr (kLoIn) {
+        tma_prefetch_2d(&tmap_m, c0, r0);
+        tma_prefetch_2d(&pm.m[1], c0, r0);
+      } else {
+        tma_prefetch_2d(&pm.m[0], c0, r0);
+      }
+    };
     if (lane == 0 && !skip_epi) {
       for (int p0 = 0; p0 < (NB > 1 ? NB - 1 : 1); ++p0) load(p0);
+      for (int p0 = 1; p0 <= ep.pf_tiles * kCPW; ++p0) l2pf(p0);
     }
     int j = 0;
     int local = 0;
@@ -935,6 +948,7 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo, kAres>::kThreads2, 1)
             if (warp == 2) TRACE_ADD(6, t_wr);
             load(j + 1);
           }
+          if (ep.pf_tiles > 0) l2pf(j + 1 + ep.pf_tiles * kCPW);
         }
         __syncwarp();
       }
