@@ -24,7 +24,9 @@ constexpr size_t kAgFlagOffset = kCollBarrierWords + kCeFlagWords;  // in words
 // scale-out across processes: source replica j of the old ring stores [2j] = its collective
 // epoch, then [2j+1] = the new topology version, into a joining replica's flags once the
 // joiner's model slice is copied (join_words)
-constexpr size_t kJoinFlagWords = 2ull * kCollMaxReplicas;
+// per source replica j: [2j] collective epoch, [2j+1] topology version; [2R + j] 1 when
+// source j shipped the low master halves instead of the fp32 master (Job::lo_reshard)
+constexpr size_t kJoinFlagWords = 3ull * kCollMaxReplicas;
 constexpr size_t kJoinFlagOffset = kCollBarrierWords + kCeFlagWords + kAgFlagWords;
 constexpr size_t kCollFlagBytes =
     (kCollBarrierWords + kCeFlagWords + kAgFlagWords + kJoinFlagWords) * sizeof(uint32_t);

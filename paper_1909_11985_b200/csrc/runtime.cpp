@@ -128,6 +128,7 @@ int Job::create_joining(const EdlJobConfig& cfg, const std::vector<std::string>&
   me.flags = r->flags;
   me.recv = r->recv;
   me.mom = r->mom;
+  me.mlo = r->mlo;
   me.rep = r;
   j->known_peers_.push_back(me);
   j->peers_.clear();
@@ -229,6 +230,7 @@ int Job::init(const EdlJobConfig& cfg, const std::vector<std::string>& ring,
     me.flags = r->flags;
     me.recv = r->recv;
     me.mom = r->mom;
+    me.mlo = r->mlo;
     me.rep = r;
     peers_.push_back(me);
     known_peers_.push_back(me);
@@ -336,6 +338,7 @@ void Job::rebuild_peers() {
     p.flags = r->flags;
     p.recv = r->recv;
     p.mom = r->mom;
+    p.mlo = r->mlo;
     p.rep = r.get();
     v.push_back(p);
   }
@@ -620,8 +623,9 @@ int Job::install_due(bool* switched) {
   *switched = false;
   bool changed = false;
   while (!events_.empty() && events_.front()->switch_t <= static_cast<int64_t>(t_)) {
-    // re-sharding, broadcasts and copies below read the fp32 master
-    EDL_TRY(master_sync());
+    // re-sharding, broadcasts and copies below read the fp32 master (a scale-out across
+    // processes from a split-master replica ships the low halves instead: lo_reshard)
+    if (!lo_reshard(*events_.front())) EDL_TRY(master_sync());
     std::unique_ptr<Event> ev = std::move(events_.front());
     events_.pop_front();
     // newcomers hosted by their own processes (scale-out across processes)
@@ -644,7 +648,9 @@ int Job::install_due(bool* switched) {
     const std::vector<PeerRep> old_peers = peers_;
     std::vector<Replica*> fresh;  // replicas that join the collective at this switch
     if (ev->out && multi) {
-      EDL_TRY(master_current());  // the deferred push collective / split master
+      // the deferred push collective; the split master is joined above or shipped as is
+      // (install_out_mp, lo_reshard)
+      EDL_TRY(join_side());
     } else if (!ev->out && !all_local && mlp_ && !dry_ && peers_.size() > 1) {
       EDL_TRY(join_side());
       EDL_TRY(reshard_in_mp(ev.get()));  // targeted: each survivor gets its new shard only
@@ -948,6 +954,12 @@ int Job::run_worker_mlp(Worker* w, int slot, bool last) {
     for (int l = 0; l < L_; ++l)
       EDL_TRY(gemm_plan_run_wait(r->fwd[l], r->stream, ag_layer_flags(r->flags, l), n_rep,
                                  r->ag_wait_epoch));
+  } else if (join_.pending) {
+    // a newcomer's first mini-batch: layer l's weights are still arriving from the source,
+    // which writes the layer's flag word after them (install_out_mp)
+    for (int l = 0; l < L_; ++l)
+      EDL_TRY(gemm_plan_run_wait(r->fwd[l], r->stream, ag_layer_flags(r->flags, l),
+                                 join_.n_src, static_cast<uint32_t>(join_.version)));
   } else {
     for (int l = 0; l < L_; ++l) EDL_TRY(gemm_plan_run(r->fwd[l], r->stream));
   }
@@ -1985,6 +1997,84 @@ int Job::join_side() {
   return EDL_OK;
 }
 
+// EDL_JOIN_PIPELINE=0: a newcomer waits on the host for the whole model before its first
+// mini-batch instead of starting its forward GEMMs on per-layer flags
+bool Job::join_pipeline_enabled() const {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("EDL_JOIN_PIPELINE");
+    on = e ? atoi(e) != 0 : 1;
+    // per-layer side-stream collectives (EDL_OVERLAP=1) take their epochs before the forward
+    const char* o = getenv("EDL_OVERLAP");
+    if (o && atoi(o) == 1) on = 0;
+  }
+  return on != 0;
+}
+
+// Newcomer (one process per GPU): wait until every source has written its join words (after
+// all of its copies), adopt the collective epoch, and rebuild the fp32 master of this
+// replica's shard when the source shipped the low halves.
+int Job::finish_join() {
+  if (!join_.pending) return EDL_OK;
+  Replica* r = reps_.begin()->second.get();
+  DeviceGuard g(r->device);
+  std::vector<uint32_t> words(kJoinFlagWords);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    EDL_CUDA_TRY(cudaMemcpy(words.data(), r->flags + kJoinFlagOffset,
+                            sizeof(uint32_t) * kJoinFlagWords, cudaMemcpyDeviceToHost));
+    bool all = true;
+    for (int j = 0; j < join_.n_src; ++j) all = all && words[2 * j + 1] == join_.version;
+    if (all) break;
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60))
+      return fail(EDL_TIMEOUT, "scale_out: the model did not arrive from the ring");
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+  coll_epoch_ = words[0];
+  for (int j = 1; j < join_.n_src; ++j)
+    if (words[2 * j] != coll_epoch_)
+      return fail(EDL_VERSION_MISMATCH, "scale_out: sources disagree on the collective epoch");
+  if (mlp_ && join_.n_src == 1 && words[2 * kCollMaxReplicas] == 1u) {
+    // the source shipped the weights and the low halves of my shard: rebuild its fp32
+    r->lo_live = true;  // (W, lo) is this shard's master until the join below
+    EDL_TRY(join_own_shard(r, join_.me_new, join_.n_new));
+  }
+  join_.pending = false;
+  return EDL_OK;
+}
+
+// Scale-out across processes from a single replica that holds the split master (the fused
+// single-replica update ran up to the switch): every process decides the same from the
+// configuration and the ring, so sources and newcomers agree without a message.
+bool Job::lo_reshard(const Event& ev) const {
+  static int env = -1;  // EDL_LO_RESHARD=0: ship the fp32 master as before
+  if (env < 0) {
+    const char* e = getenv("EDL_LO_RESHARD");
+    env = e ? atoi(e) != 0 : 1;
+  }
+  if (!env || !mlp_ || dry_ || !ev.out || cfg_.momentum != 0.0 || cfg_.appx_recovery ||
+      !split_master_enabled() || peers_.size() != 1)
+    return false;
+  bool multi = joining_;
+  for (const auto& w : ev.prepared) multi = multi || (w && w->remote);
+  return multi;
+}
+
+// fp32 master of replica r's shard (me of n) from its weights and low halves
+int Job::join_own_shard(Replica* r, int me, int n) {
+  if (!r->lo_live) return EDL_OK;
+  if (!r->mlo) return fail(EDL_EINVAL, "split master: no low-half buffer");
+  DeviceGuard g(r->device);
+  CollArgs a;
+  own_segments(me, n, &a);
+  for (int k = 0; k < a.n_seg; ++k) {
+    const size_t at = a.seg_lo8[k] * 8, len = (a.seg_hi8[k] - a.seg_lo8[k]) * 8;
+    EDL_TRY(master_join(r->W + at, r->mlo + at, r->master + at, len, r->stream));
+  }
+  r->lo_live = false;
+  return EDL_OK;
+}
+
 int Job::master_sync() {
   for (auto& [dev, r] : reps_) {
     if (!r->lo_live) continue;
@@ -2185,7 +2275,33 @@ int Job::step_host_only(bool switched, EdlStepReport* out) {
   return EDL_OK;
 }
 
+namespace {
+// EDL_HOST_TRACE=1: host time of the step's phases on stderr (switch-stall diagnostics)
+struct HostTrace {
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  std::string line;
+  HostTrace() {
+    static int env = -1;
+    if (env < 0) {
+      const char* e = getenv("EDL_HOST_TRACE");
+      env = e ? atoi(e) : 0;
+    }
+    on = env != 0;
+    t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    line += std::string(" ") + what + "=" +
+            std::to_string(std::chrono::duration<double, std::micro>(now - last).count()).substr(0, 6);
+    last = now;
+  }
+};
+}  // namespace
+
 int Job::step(EdlStepReport* out) {
+  HostTrace ht;
   if (dry_) return step_dry(out);
   const int slot = static_cast<int>(launched_ % kSlots);
   // pinned staging for this slot is free once the mini-batch that used it kSlots ago is done
@@ -2194,7 +2310,17 @@ int Job::step(EdlStepReport* out) {
 
   if (exited_) return fail(EDL_EINVAL, "job: this process's workers have left the ring");
   bool switched = false;
+  ht.mark("pre");
+  // the previous switch's model copies to newcomers (side3) before this mini-batch
+  for (auto& [dev, rr] : reps_) {
+    if (!rr->copies_pending) continue;
+    DeviceGuard dg(dev);
+    EDL_CUDA_TRY(cudaEventRecord(rr->ev_sync, rr->side3));
+    EDL_CUDA_TRY(cudaStreamWaitEvent(rr->stream, rr->ev_sync, 0));
+    rr->copies_pending = false;
+  }
   EDL_TRY(install_due(&switched));
+  ht.mark("install");
   if (joining_) return step_host_only(switched, out);  // newcomer before its switch
   if (peers_.empty() || !peers_[rep_index()].local) {
     // one process per GPU, scale-in: this process's members left at this switch (their
@@ -2294,7 +2420,8 @@ int Job::step(EdlStepReport* out) {
   split_step_ = fused_update_ && !overlap_;
   sgd_out_split_ = true;
   for (const auto& ev : events_)
-    if (ev->switch_t >= 0 && ev->switch_t <= static_cast<int64_t>(t_) + 1) sgd_out_split_ = false;
+    if (ev->switch_t >= 0 && ev->switch_t <= static_cast<int64_t>(t_) + 1 && !lo_reshard(*ev))
+      sgd_out_split_ = false;
   if (!split_step_) EDL_TRY(master_sync());
   step_count_ = count;
   if (overlap_mode_ == 1) {  // same epochs on every process
@@ -2335,8 +2462,14 @@ int Job::step(EdlStepReport* out) {
     if (w->remote) continue;  // computed by its own process
     EDL_TRY(mlp_ ? run_worker_mlp(w, slot, last_on[w->rep] == w) : run_worker_linear(w, slot));
   }
+  ht.mark("workers");
+  EDL_TRY(finish_join());  // a newcomer's first mini-batch: its epoch and master shard
   const double* loss_src = nullptr;
   EDL_TRY(reduce_and_update(count, t_, slot, &loss_src));
+  ht.mark("update");
+  if (ht.on && (switched || ht.line.find("install=0") == std::string::npos))
+    fprintf(stderr, "[host rank %d t=%llu%s]%s\n", my_rank_, static_cast<unsigned long long>(t_),
+            switched ? " switch" : "", ht.line.c_str());
   // with the deferred all-gather the mini-batch ends on the side streams (push collective)
   cudaStream_t tail = ag_defer_ ? prim->side : prim->stream;
   EDL_CUDA_TRY(cudaMemcpyAsync(&prim->host_loss[slot], loss_src, sizeof(double),
@@ -2394,6 +2527,7 @@ int Job::sync(EdlStepReport* out) {
     DeviceGuard g(dev);
     EDL_CUDA_TRY(cudaStreamSynchronize(r->stream));
     if (r->side) EDL_CUDA_TRY(cudaStreamSynchronize(r->side));
+    if (r->side3) EDL_CUDA_TRY(cudaStreamSynchronize(r->side3));
   }
   collect_completed();
   if (out) *out = last_;
@@ -2428,7 +2562,7 @@ static bool same_replica(const PeerRep& a, const PeerRep& b) {
 // Bytes of old replica i's shard that lie in other replicas' new shards (old = replicas and
 // sharding before a switch, after = after it; own_segments sharding per layer).
 double Job::reshard_piece_bytes(const std::vector<PeerRep>& old, int i,
-                                const std::vector<PeerRep>& after, bool mom) const {
+                                const std::vector<PeerRep>& after, bool mom, bool lo) const {
   const int n_old = static_cast<int>(old.size()), n_new = static_cast<int>(after.size());
   double b = 0;
   for (int l = 0; l < L_; ++l) {
@@ -2440,7 +2574,7 @@ double Job::reshard_piece_bytes(const std::vector<PeerRep>& old, int i,
       size_t nlo, nhi;
       shard_range(len8, n_new, j, &nlo, &nhi);
       const size_t a8 = std::max(olo, nlo), b8 = std::min(ohi, nhi);
-      if (b8 > a8) b += (b8 - a8) * 8.0 * (mom ? 8.0 : 4.0);
+      if (b8 > a8) b += (b8 - a8) * 8.0 * (lo ? 2.0 : mom ? 8.0 : 4.0);
     }
   }
   return b;
@@ -2458,13 +2592,15 @@ double Job::reshard_piece_bytes(const std::vector<PeerRep>& old, int i,
 // instead of the whole fp32 model after an all-gather ("broadcast the model").
 int Job::add_reshard_copies(MultiCopyArgs* cp, const std::vector<PeerRep>& old, int i,
                             const std::vector<PeerRep>& after, const std::vector<PeerRep>& fresh,
-                            Replica* r) {
+                            Replica* r, bool lo, bool skip_w) {
   const int n_old = static_cast<int>(old.size());
   const bool mom = r->mom != nullptr;
+  if (lo && (mom || !r->mlo || !r->lo_live))
+    return fail(EDL_EINVAL, "reshard: low-half transfer needs this replica's split master");
   const size_t p8 = P_ / 8, jn = fresh.size();  // MLP layers: in % 8 == 0, so P_ % 8 == 0
   std::vector<double> mb(n_old);
   double sum_m = 0;
-  for (int k = 0; k < n_old; ++k) sum_m += (mb[k] = reshard_piece_bytes(old, k, after, mom));
+  for (int k = 0; k < n_old; ++k) sum_m += (mb[k] = reshard_piece_bytes(old, k, after, mom, lo));
   const double wtot = static_cast<double>(jn * p8) * 16.0;  // bytes of weights to ship
   std::vector<double> quota(n_old);
   double qsum = 0;
@@ -2477,6 +2613,7 @@ int Job::add_reshard_copies(MultiCopyArgs* cp, const std::vector<PeerRep>& old, 
     acc = (k == n_old - 1) ? jn * p8 : std::min(jn * p8, acc + share);
     whi = acc;
   }
+  if (skip_w) whi = wlo;  // the caller ships the weights itself (layer by layer)
   for (size_t pos = wlo; pos < whi;) {  // split the range at replica boundaries
     const size_t q = pos / p8, off = pos % p8, end = std::min(whi, (q + 1) * p8);
     EDL_TRY(add_copy(cp, fresh[q].W + off * 8, r->W + off * 8,
@@ -2495,6 +2632,11 @@ int Job::add_reshard_copies(MultiCopyArgs* cp, const std::vector<PeerRep>& old, 
       const size_t a8 = std::max(olo, nlo), b8 = std::min(ohi, nhi);
       if (b8 <= a8) continue;
       const size_t at = base + a8 * 8, n = (b8 - a8) * 8;
+      if (lo) {  // the new owner rebuilds its fp32 shard from the weights and these halves
+        if (!after[j].mlo) return fail(EDL_EINVAL, "reshard: a newcomer has no split-master buffer");
+        EDL_TRY(add_copy(cp, after[j].mlo + at, r->mlo + at, sizeof(uint16_t) * n, r->stream));
+        continue;
+      }
       EDL_TRY(add_copy(cp, after[j].master + at, r->master + at, sizeof(float) * n, r->stream));
       if (mom) {
         if (!after[j].mom) return fail(EDL_EINVAL, "reshard: a replica has no momentum buffer");
@@ -2520,7 +2662,7 @@ int Job::reshard_local(const std::vector<PeerRep>& old, const std::vector<Replic
     Replica* r = old[i].rep;
     DeviceGuard g(r->device);
     MultiCopyArgs cp;
-    EDL_TRY(add_reshard_copies(&cp, old, static_cast<int>(i), peers_, fr, r));
+    EDL_TRY(add_reshard_copies(&cp, old, static_cast<int>(i), peers_, fr, r, false, false));
     EDL_TRY(multi_copy(cp, r->stream));
     launches_ += 1;
     EDL_CUDA_TRY(cudaEventRecord(r->ev_sync, r->stream));
@@ -2549,7 +2691,7 @@ int Job::reshard_in_mp(const Event* ev) {
   Replica* r = peers_[me].rep;
   DeviceGuard g(r->device);
   MultiCopyArgs cp;
-  EDL_TRY(add_reshard_copies(&cp, peers_, me, after, {}, r));
+  EDL_TRY(add_reshard_copies(&cp, peers_, me, after, {}, r, false, false));
   EDL_TRY(multi_copy(cp, r->stream));
   CollArgs a;
   for (const auto& p : peers_) a.flags[a.n_dst++] = p.flags;
@@ -2579,29 +2721,41 @@ int Job::install_out_mp(Event* ev) {
   const int n_src = static_cast<int>(peers_.size());  // the current replicas, rank order
   if (joining_) {
     // this process's newcomer: its buffers are filled by the sources
-    Replica* r = reps_.begin()->second.get();
-    DeviceGuard g(r->device);
-    std::vector<uint32_t> words(kJoinFlagWords);
-    const auto t0 = std::chrono::steady_clock::now();
-    for (;;) {
-      EDL_CUDA_TRY(cudaMemcpy(words.data(), r->flags + kJoinFlagOffset,
-                              sizeof(uint32_t) * kJoinFlagWords, cudaMemcpyDeviceToHost));
-      bool all = true;
-      for (int j = 0; j < n_src; ++j) all = all && words[2 * j + 1] == new_version;
-      if (all) break;
-      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60))
-        return fail(EDL_TIMEOUT, "scale_out: the model did not arrive from the ring");
-      std::this_thread::sleep_for(std::chrono::microseconds(20));
+    std::vector<PeerRep> after = peers_;
+    for (const auto& q : joiners) after.push_back(q);
+    std::sort(after.begin(), after.end(),
+              [](const PeerRep& a, const PeerRep& b) { return a.rank < b.rank; });
+    int me_new = 0;
+    for (size_t k = 0; k < after.size(); ++k)
+      if (after[k].rank == my_rank_) me_new = static_cast<int>(k);
+    join_ = JoinWait{true, new_version, n_src, me_new, static_cast<int>(after.size())};
+    // one source: the first mini-batch's forward GEMMs wait on the per-layer flags the
+    // source writes after each layer's weights, and the join words are read only before its
+    // collective (finish_join); with several sources read them now
+    if (!(mlp_ && n_src == 1 && join_pipeline_enabled())) {
+      EDL_TRY(finish_join());
+    } else {
+      // start once the source has begun shipping (layer 0's flag): a newcomer that runs
+      // ahead in host-only steps waits here, not inside its first GEMM
+      Replica* r = reps_.begin()->second.get();
+      DeviceGuard g(r->device);
+      const auto t0 = std::chrono::steady_clock::now();
+      for (;;) {
+        uint32_t f = 0;
+        EDL_CUDA_TRY(cudaMemcpy(&f, ag_layer_flags(r->flags, 0), sizeof(f), cudaMemcpyDeviceToHost));
+        if (f >= static_cast<uint32_t>(new_version)) break;
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60))
+          return fail(EDL_TIMEOUT, "scale_out: the model did not start arriving from the ring");
+        std::this_thread::sleep_for(std::chrono::microseconds(10));
+      }
     }
-    coll_epoch_ = words[0];
-    for (int j = 1; j < n_src; ++j)
-      if (words[2 * j] != coll_epoch_)
-        return fail(EDL_VERSION_MISMATCH, "scale_out: sources disagree on the collective epoch");
     joining_ = false;
   } else {
     const int me = rep_index();
     Replica* r = peers_[me].rep;
     DeviceGuard g(r->device);
+    bool ship_lo = false;
+    cudaStream_t word_stream = r->stream;
     if (mlp_) {
       // Targeted re-sharding instead of consolidating the whole model: the bf16 weights are
       // current and identical on every replica, so each source ships slice me/n of them to
@@ -2616,14 +2770,63 @@ int Job::install_out_mp(Event* ev) {
       for (const auto& q : joiners) after.push_back(q);
       std::sort(after.begin(), after.end(),
                 [](const PeerRep& a, const PeerRep& b) { return a.rank < b.rank; });
-      EDL_TRY(add_reshard_copies(&cp, peers_, me, after, joiners, r));
-      EDL_TRY(multi_copy(cp, r->stream));  // SM stores over NVLink, one launch
-      launches_ += 1;
+      // (a split-master source that has not run a fused mini-batch yet holds the fp32 one)
+      bool lo = lo_reshard(*ev) && r->lo_live && r->mlo;
+      for (const auto& q : joiners) lo = lo && q.mlo;
+      if (lo_reshard(*ev) && !lo) EDL_TRY(master_sync());
+      ship_lo = lo;
+      // one source: the weights go out layer by layer, each layer followed by its flag word
+      // in every newcomer, whose forward GEMMs start on those flags (join_pipeline)
+      const bool pipe = n_src == 1 && join_pipeline_enabled();
+      EDL_TRY(add_reshard_copies(&cp, peers_, me, after, joiners, r, lo, pipe));
+      // with one source (pipe) the newcomers' model goes out on the copy engines from a side
+      // stream, layer by layer, so this replica's own switch mini-batch starts at once and
+      // the newcomers' forward follows the weights as they land; nothing here waits for the
+      // copies: the newcomers read the join words written after them before their
+      // collective, and this replica's next model write is its push collective, past a
+      // barrier they enter only after that.  Several sources: one SM copy kernel each ahead
+      // of the mini-batch (measured faster than the copy engines when the newcomer waits for
+      // the whole model: 1->2 stall 0.98 vs 1.08 ms; EDL_RESHARD_CE=1 selects them)
+      static int ce_env = -1;
+      if (ce_env < 0) {
+        const char* e = getenv("EDL_RESHARD_CE");
+        ce_env = e ? atoi(e) != 0 : 0;
+      }
+      if (ce_env || pipe) {
+        EDL_CUDA_TRY(cudaEventRecord(r->ev_sync, r->stream));
+        EDL_CUDA_TRY(cudaStreamWaitEvent(r->side3, r->ev_sync, 0));
+        for (int l = 0; pipe && l < L_; ++l) {
+          const size_t bytes = sizeof(__nv_bfloat16) * static_cast<size_t>(in_[l]) * out_[l];
+          for (const auto& q : joiners)
+            EDL_CUDA_TRY(cudaMemcpyAsync(q.W + off_[l], r->W + off_[l], bytes,
+                                         cudaMemcpyDeviceToDevice, r->side3));
+          for (const auto& q : joiners)
+            EDL_TRY(stream_write_u32(ag_layer_flags(q.flags, l) + me,
+                                     static_cast<uint32_t>(new_version), r->side3));
+        }
+        for (int k = 0; k < cp.n; ++k)
+          EDL_CUDA_TRY(cudaMemcpyAsync(cp.seg[k].dst, cp.seg[k].src, cp.seg[k].bytes,
+                                       cudaMemcpyDeviceToDevice, r->side3));
+        word_stream = r->side3;
+        r->copies_pending = true;
+      } else {
+        EDL_TRY(multi_copy(cp, r->stream));  // SM stores over NVLink, one launch
+        launches_ += 1;
+      }
+      if (lo) {  // my own new shard: fp32 master from (W, lo) here
+        int me_new = 0;
+        for (size_t k = 0; k < after.size(); ++k)
+          if (after[k].rank == my_rank_) me_new = static_cast<int>(k);
+        EDL_TRY(join_own_shard(r, me_new, static_cast<int>(after.size())));
+        launches_ += 1;
+      }
     }
     for (const auto& q : joiners) {
-      EDL_TRY(stream_write_u32(q.flags + kJoinFlagOffset + 2 * me, coll_epoch_, r->stream));
+      EDL_TRY(stream_write_u32(q.flags + kJoinFlagOffset + 2 * kCollMaxReplicas + me,
+                               ship_lo ? 1u : 0u, word_stream));
+      EDL_TRY(stream_write_u32(q.flags + kJoinFlagOffset + 2 * me, coll_epoch_, word_stream));
       EDL_TRY(stream_write_u32(q.flags + kJoinFlagOffset + 2 * me + 1,
-                               static_cast<uint32_t>(new_version), r->stream));
+                               static_cast<uint32_t>(new_version), word_stream));
     }
   }
   std::vector<size_t> order(ev->ids.size());
@@ -3028,6 +3231,7 @@ int Job::export_handles(std::vector<uint8_t>* out) const {
   EDL_TRY(w.handle(r->flags));
   EDL_TRY(w.handle(r->recv));
   EDL_TRY(w.handle(r->mom));
+  EDL_TRY(w.handle(r->mlo));
   std::vector<const Worker*> mine;  // local members + this process's scheduled newcomers
   for (const auto& [id, wk] : workers_)
     if (!wk->remote) mine.push_back(wk.get());
@@ -3092,6 +3296,8 @@ int Job::import_handles(const uint8_t* blob, size_t len) {
   peer.recv = static_cast<__nv_bfloat16*>(p);
   EDL_TRY(open(&p));
   peer.mom = static_cast<float*>(p);
+  EDL_TRY(open(&p));
+  peer.mlo = static_cast<uint16_t*>(p);
   const uint32_t n = rd.pod<uint32_t>();
   for (uint32_t i = 0; i < n && rd.ok; ++i) {
     const std::string id = rd.text();

@@ -50,6 +50,9 @@ struct Replica {
   // lo_live the master is (W, mlo) and `master` is stale (Job::master_sync rebuilds it)
   uint16_t* mlo = nullptr;
   bool lo_live = false;
+  // scale-out source: the newcomers' model copies still run on side3 (the next mini-batch's
+  // stream waits for them before anything else)
+  bool copies_pending = false;
   float* mom = nullptr;
   uint32_t* flags = nullptr;
   int64_t rows_cap = 0;
@@ -164,6 +167,7 @@ struct PeerRep {
   uint32_t* flags = nullptr;
   __nv_bfloat16* recv = nullptr;
   float* mom = nullptr;  // momentum (momentum != 0 only)
+  uint16_t* mlo = nullptr;  // split-master low halves (single-replica fused update)
   Replica* rep = nullptr;  // local replicas
 };
 
@@ -342,11 +346,24 @@ class Job {
   int install_out_mp(Event* ev);
   int reshard_in_mp(const Event* ev);
   int add_copy(MultiCopyArgs* cp, void* dst, const void* src, size_t bytes, cudaStream_t s);
+  // scale-out across processes from one replica holding the split master: ship the low
+  // master halves (2 B/param of each new shard) instead of the fp32 master (4 B)
+  bool lo_reshard(const Event& ev) const;
+  // newcomer process: the join words it still has to read (finish_join) once its first
+  // mini-batch's forward is enqueued
+  struct JoinWait {
+    bool pending = false;
+    uint64_t version = 0;
+    int n_src = 0, me_new = 0, n_new = 0;
+  } join_;
+  bool join_pipeline_enabled() const;
+  int finish_join();
   double reshard_piece_bytes(const std::vector<PeerRep>& old, int i,
-                             const std::vector<PeerRep>& after, bool mom) const;
+                             const std::vector<PeerRep>& after, bool mom, bool lo) const;
   int add_reshard_copies(MultiCopyArgs* cp, const std::vector<PeerRep>& old, int i,
                          const std::vector<PeerRep>& after, const std::vector<PeerRep>& fresh,
-                         Replica* r);
+                         Replica* r, bool lo, bool skip_w);
+  int join_own_shard(Replica* r, int me, int n);  // fp32 master of shard me/n from (W, lo)
   int reshard_local(const std::vector<PeerRep>& old, const std::vector<Replica*>& fresh);
   Worker* find_worker(const std::string& id) const;
   int my_rank_ = 0;
