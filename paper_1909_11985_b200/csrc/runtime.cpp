@@ -1997,18 +1997,20 @@ int Job::join_side() {
   return EDL_OK;
 }
 
-// EDL_JOIN_PIPELINE=0: a newcomer waits on the host for the whole model before its first
-// mini-batch instead of starting its forward GEMMs on per-layer flags
-bool Job::join_pipeline_enabled() const {
+// Newcomers start their forward GEMMs on per-layer weight flags (the sources ship the model
+// layer by layer on the copy engines) when the job has one source replica; EDL_JOIN_PIPELINE
+// =0 never (the newcomer waits on the host for the whole model), =2 with any number of
+// sources (measured at 2->4: 0.91 vs 0.84 ms stall, so not the default there)
+bool Job::join_pipeline_enabled(int n_src) const {
   static int on = -1;
   if (on < 0) {
     const char* e = getenv("EDL_JOIN_PIPELINE");
-    on = e ? atoi(e) != 0 : 1;
+    on = e ? atoi(e) : 1;
     // per-layer side-stream collectives (EDL_OVERLAP=1) take their epochs before the forward
     const char* o = getenv("EDL_OVERLAP");
     if (o && atoi(o) == 1) on = 0;
   }
-  return on != 0;
+  return on == 2 || (on == 1 && n_src == 1);
 }
 
 // Newcomer (one process per GPU): wait until every source has written its join words (after
@@ -2732,18 +2734,21 @@ int Job::install_out_mp(Event* ev) {
     // one source: the first mini-batch's forward GEMMs wait on the per-layer flags the
     // source writes after each layer's weights, and the join words are read only before its
     // collective (finish_join); with several sources read them now
-    if (!(mlp_ && n_src == 1 && join_pipeline_enabled())) {
+    if (!(mlp_ && join_pipeline_enabled(n_src))) {
       EDL_TRY(finish_join());
     } else {
-      // start once the source has begun shipping (layer 0's flag): a newcomer that runs
+      // start once the sources have begun shipping (layer 0's flags): a newcomer that runs
       // ahead in host-only steps waits here, not inside its first GEMM
       Replica* r = reps_.begin()->second.get();
       DeviceGuard g(r->device);
       const auto t0 = std::chrono::steady_clock::now();
       for (;;) {
-        uint32_t f = 0;
-        EDL_CUDA_TRY(cudaMemcpy(&f, ag_layer_flags(r->flags, 0), sizeof(f), cudaMemcpyDeviceToHost));
-        if (f >= static_cast<uint32_t>(new_version)) break;
+        std::vector<uint32_t> f(static_cast<size_t>(n_src));
+        EDL_CUDA_TRY(cudaMemcpy(f.data(), ag_layer_flags(r->flags, 0), sizeof(uint32_t) * n_src,
+                                cudaMemcpyDeviceToHost));
+        bool all = true;
+        for (uint32_t v : f) all = all && v >= static_cast<uint32_t>(new_version);
+        if (all) break;
         if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60))
           return fail(EDL_TIMEOUT, "scale_out: the model did not start arriving from the ring");
         std::this_thread::sleep_for(std::chrono::microseconds(10));
@@ -2777,9 +2782,9 @@ int Job::install_out_mp(Event* ev) {
       ship_lo = lo;
       // one source: the weights go out layer by layer, each layer followed by its flag word
       // in every newcomer, whose forward GEMMs start on those flags (join_pipeline)
-      const bool pipe = n_src == 1 && join_pipeline_enabled();
+      const bool pipe = join_pipeline_enabled(n_src);
       EDL_TRY(add_reshard_copies(&cp, peers_, me, after, joiners, r, lo, pipe));
-      // with one source (pipe) the newcomers' model goes out on the copy engines from a side
+      // pipelined join (pipe): the newcomers' model goes out on the copy engines from a side
       // stream, layer by layer, so this replica's own switch mini-batch starts at once and
       // the newcomers' forward follows the weights as they land; nothing here waits for the
       // copies: the newcomers read the join words written after them before their
@@ -2796,10 +2801,15 @@ int Job::install_out_mp(Event* ev) {
         EDL_CUDA_TRY(cudaEventRecord(r->ev_sync, r->stream));
         EDL_CUDA_TRY(cudaStreamWaitEvent(r->side3, r->ev_sync, 0));
         for (int l = 0; pipe && l < L_; ++l) {
-          const size_t bytes = sizeof(__nv_bfloat16) * static_cast<size_t>(in_[l]) * out_[l];
+          // source me of n_src ships its 1/n_src of every layer (16-byte aligned pieces)
+          const size_t len8 = static_cast<size_t>(in_[l]) * out_[l] / 8;
+          size_t lo8, hi8;
+          shard_range(len8, n_src, me, &lo8, &hi8);
+          const size_t at = off_[l] + lo8 * 8, bytes = (hi8 - lo8) * 16;
           for (const auto& q : joiners)
-            EDL_CUDA_TRY(cudaMemcpyAsync(q.W + off_[l], r->W + off_[l], bytes,
-                                         cudaMemcpyDeviceToDevice, r->side3));
+            if (bytes)
+              EDL_CUDA_TRY(cudaMemcpyAsync(q.W + at, r->W + at, bytes, cudaMemcpyDeviceToDevice,
+                                           r->side3));
           for (const auto& q : joiners)
             EDL_TRY(stream_write_u32(ag_layer_flags(q.flags, l) + me,
                                      static_cast<uint32_t>(new_version), r->side3));

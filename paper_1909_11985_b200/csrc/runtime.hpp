@@ -356,7 +356,7 @@ class Job {
     uint64_t version = 0;
     int n_src = 0, me_new = 0, n_new = 0;
   } join_;
-  bool join_pipeline_enabled() const;
+  bool join_pipeline_enabled(int n_src) const;
   int finish_join();
   double reshard_piece_bytes(const std::vector<PeerRep>& old, int i,
                              const std::vector<PeerRep>& after, bool mom, bool lo) const;
