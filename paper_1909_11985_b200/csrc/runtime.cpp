@@ -2308,6 +2308,16 @@ int Job::step(EdlStepReport* out) {
   const int slot = static_cast<int>(launched_ % kSlots);
   // pinned staging for this slot is free once the mini-batch that used it kSlots ago is done
   if (slot_end_[slot]) EDL_CUDA_TRY(cudaEventSynchronize(slot_end_[slot]));
+  // a loss read on the side stream two mini-batches ago (same parity slot of the worker's
+  // loss) must be done before this mini-batch's gather zeroes that slot
+  for (auto& [dev, rr] : reps_) {
+    if (!rr->loss_on_side) continue;
+    const int back = static_cast<int>((launched_ + kSlots - 2) % kSlots);
+    if (launched_ >= 2 && rr->ev_end[back]) {
+      DeviceGuard dg(dev);
+      EDL_CUDA_TRY(cudaStreamWaitEvent(rr->stream, rr->ev_end[back], 0));
+    }
+  }
   collect_completed();
 
   if (exited_) return fail(EDL_EINVAL, "job: this process's workers have left the ring");
@@ -2472,8 +2482,22 @@ int Job::step(EdlStepReport* out) {
   if (ht.on && (switched || ht.line.find("install=0") == std::string::npos))
     fprintf(stderr, "[host rank %d t=%llu%s]%s\n", my_rank_, static_cast<unsigned long long>(t_),
             switched ? " switch" : "", ht.line.c_str());
-  // with the deferred all-gather the mini-batch ends on the side streams (push collective)
+  // with the deferred all-gather the mini-batch ends on the side streams (push collective);
+  // the single-replica fused path reads its loss on the side stream too (EDL_LOSS_SIDE), so
+  // the next mini-batch's first kernel follows this one's last without the copy between them
+  static int loss_side = -1;
+  if (loss_side < 0) {
+    const char* e = getenv("EDL_LOSS_SIDE");
+    loss_side = e ? atoi(e) : 1;
+  }
+  const bool side_tail = !ag_defer_ && loss_side && fused_update_ && mlp_ && prim->side;
   cudaStream_t tail = ag_defer_ ? prim->side : prim->stream;
+  if (side_tail) {
+    EDL_CUDA_TRY(cudaEventRecord(prim->ev_bwd, prim->stream));
+    EDL_CUDA_TRY(cudaStreamWaitEvent(prim->side, prim->ev_bwd, 0));
+    tail = prim->side;
+    prim->loss_on_side = true;
+  }
   EDL_CUDA_TRY(cudaMemcpyAsync(&prim->host_loss[slot], loss_src, sizeof(double),
                                cudaMemcpyDeviceToHost, tail));
   // the primary's end event covers every local replica's share of the mini-batch

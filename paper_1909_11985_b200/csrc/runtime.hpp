@@ -53,6 +53,7 @@ struct Replica {
   // scale-out source: the newcomers' model copies still run on side3 (the next mini-batch's
   // stream waits for them before anything else)
   bool copies_pending = false;
+  bool loss_on_side = false;  // the loss of recent mini-batches was read on `side`
   float* mom = nullptr;
   uint32_t* flags = nullptr;
   int64_t rows_cap = 0;
