@@ -39,6 +39,7 @@ struct EpiParams {
   // ahead in the fused-SGD epilogue.  Defaults from gemm_prefetch_defaults().
   int pf_kb;
   int pf_tiles;
+  int mask_pf;  // L2 prefetch of the ReLU' mask rows before the epilogue waits (dgrad)
   // reduce-scatter routing of a weight-gradient GEMM (N > 1): output rows are owned in
   // blocks of route_rows by replica row / route_rows; blocks owned by another replica are
   // stored through PeerMaps::m[owner] (that replica's receive slot for this one, over NVLink)

@@ -1256,6 +1256,16 @@ __global__ void __launch_bounds__(Cfg2<BN, kSgd, kLo, kAres>::kThreads2, 1)
       const uint32_t acc_phase = (local / C::kAcc) & 1;
       const int row0 = tile_m(w) * 256 + static_cast<int>(pr) * 128 + q * 32;
       const int n0 = tile_n(w) * BN;
+      // the ReLU' mask of this lane's row (dgrad): pull it into L2 while the mainloop runs,
+      // so the epilogue's loads do not pay the HBM latency after the accumulator is ready
+      // (EDL_MASK_PF=1; off by default: no measurable gain)
+      if (ep.mask && ep.mask_pf && row0 + lane < M) {
+        const __nv_bfloat16* mrow =
+            ep.mask + static_cast<size_t>(row0 + lane) * ep.ldm + n0;
+#pragma unroll
+        for (int c = 0; c < BN; c += 64)
+          if (n0 + c < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(mrow + c));
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       if (warp == 2 && local == 0) TL(4);
       tc_fence_after();
@@ -1649,6 +1659,12 @@ static void gemm_prefetch_defaults(EpiParams* ep) {
   }
   ep->pf_kb = kb;
   ep->pf_tiles = tiles;
+  static int mask_pf = -1;
+  if (mask_pf < 0) {
+    const char* e = getenv("EDL_MASK_PF");
+    mask_pf = e ? atoi(e) : 0;  // measured: 816-827k vs 815-820k samples/s, within noise
+  }
+  ep->mask_pf = mask_pf;
   const char* d = getenv("EDL_GEMM_DBG");
   ep->dbg = d ? atoi(d) : 0;
 }
