@@ -2479,7 +2479,7 @@ int Job::step(EdlStepReport* out) {
   const double* loss_src = nullptr;
   EDL_TRY(reduce_and_update(count, t_, slot, &loss_src));
   ht.mark("update");
-  if (ht.on && (switched || ht.line.find("install=0") == std::string::npos))
+  if (ht.on)
     fprintf(stderr, "[host rank %d t=%llu%s]%s\n", my_rank_, static_cast<unsigned long long>(t_),
             switched ? " switch" : "", ht.line.c_str());
   // with the deferred all-gather the mini-batch ends on the side streams (push collective);
